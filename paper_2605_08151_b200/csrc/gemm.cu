@@ -1,0 +1,138 @@
+// gemm.cu — host side of the tcgen05 GEMM: TMA descriptors, planning, launch.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm.h"
+#include "gemm_tcgen05.cuh"
+
+namespace spectre {
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+static int get_encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) {
+    set_last_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return SPECTRE_ECUDA;
+  }
+  return SPECTRE_OK;
+}
+
+// [outer][inner] bf16 row-major, 64-element (128 B) inner boxes, 128B swizzle.
+int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                   uint32_t box_outer) {
+  if (int e = get_encoder()) return e;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (inner * 2) % 16)
+    return arg_fail("tensor map: 16-byte alignment");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return SPECTRE_ECUDA;
+  }
+  return SPECTRE_OK;
+}
+
+static size_t gemm_smem_bytes(int stages, int rows_cap) {
+  return 1024 + (size_t)stages * (16384 + (size_t)rows_cap * 128) + 1024 + 8192;
+}
+
+template <int kEpi, uint32_t kCols>
+static int launch_one(const GemmPlan& p, cudaStream_t s) {
+  auto kern = gemm_bf16_swapab<kEpi, kCols>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    SPECTRE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          232448));
+    configured = true;
+  }
+  kern<<<p.grid, kGemmThreads, p.smem, s>>>(p.tmap_w, p.tmap_x, p.args);
+  SPECTRE_LAUNCH_CHECK("gemm_bf16_swapab");
+  return SPECTRE_OK;
+}
+
+template <int kEpi>
+static int launch_epi(const GemmPlan& p, cudaStream_t s) {
+  switch (p.tmem_cols) {
+    case 32: return launch_one<kEpi, 32>(p, s);
+    case 64: return launch_one<kEpi, 64>(p, s);
+    case 128: return launch_one<kEpi, 128>(p, s);
+    case 256: return launch_one<kEpi, 256>(p, s);
+    default: return launch_one<kEpi, 512>(p, s);
+  }
+}
+
+int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_cap, int epi,
+              int splits, int max_stages) {
+  if (N < 1 || K < 64 || K % 64 || rows_cap < 64 || rows_cap % 64 || rows_cap > 512 ||
+      splits < 1)
+    return arg_fail("gemm_plan: shape (K % 64, rows_cap in 64..512 step 64)");
+  if (epi == kSwiGLU && (N % 128 || splits != 1)) return arg_fail("gemm_plan: swiglu shape");
+  if (epi == kArgmax && splits != 1) return arg_fail("gemm_plan: argmax needs splits == 1");
+  *p = GemmPlan{};
+  if (int e = make_tmap_bf16(&p->tmap_w, W, (uint64_t)K, (uint64_t)N, 128)) return e;
+  if (int e = make_tmap_bf16(&p->tmap_x, X, (uint64_t)K, (uint64_t)rows_cap, 64)) return e;
+  int stages = kGemmMaxStages;
+  if (max_stages > 0 && max_stages < stages) stages = max_stages;
+  while (stages > 2 && gemm_smem_bytes(stages, rows_cap) > 232448) --stages;
+  if (gemm_smem_bytes(stages, rows_cap) > 232448) return arg_fail("gemm_plan: smem");
+  const int n_tiles = (N + kGemmBlockN - 1) / kGemmBlockN;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)rows_cap) cols <<= 1;
+  p->epi = epi;
+  p->tmem_cols = (int)cols;
+  p->grid = n_tiles * splits;
+  p->smem = gemm_smem_bytes(stages, rows_cap);
+  p->args.N = N;
+  p->args.K = K;
+  p->args.rows_cap = rows_cap;
+  p->args.splits = splits;
+  p->args.stages = stages;
+  p->n_tiles = n_tiles;
+  return SPECTRE_OK;
+}
+
+int gemm_run(const GemmPlan& p, cudaStream_t s) {
+  switch (p.epi) {
+    case kPartial: return launch_epi<kPartial>(p, s);
+    case kArgmax: return launch_epi<kArgmax>(p, s);
+    default: return launch_epi<kSwiGLU>(p, s);
+  }
+}
+
+}  // namespace spectre
+
+using namespace spectre;
+
+extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_dev,
+                                 int32_t t_static, int32_t rows_cap, int32_t N, int32_t K,
+                                 int32_t splits, int32_t epilogue, float* partial,
+                                 float* amax_val, int32_t* amax_idx, void* act, int32_t ld_act,
+                                 int32_t max_stages, void* stream) {
+  GemmPlan p;
+  if (int e = gemm_plan(&p, W, N, K, X, rows_cap, epilogue, splits, max_stages)) return e;
+  p.args.t_dev = t_dev;
+  p.args.t_static = t_static;
+  p.args.part = partial;
+  p.args.amax_val = amax_val;
+  p.args.amax_idx = amax_idx;
+  p.args.act = reinterpret_cast<__nv_bfloat16*>(act);
+  p.args.ld_act = ld_act;
+  return gemm_run(p, as_stream(stream));
+}

@@ -1,0 +1,29 @@
+// gemm.h — internal C++ interface of the tcgen05 GEMM (used by engine.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "gemm_tcgen05.cuh"
+
+namespace spectre {
+
+struct GemmPlan {
+  CUtensorMap tmap_w;
+  CUtensorMap tmap_x;
+  GemmArgs args;
+  int grid = 0;
+  size_t smem = 0;
+  int tmem_cols = 0;
+  int epi = 0;
+  int n_tiles = 0;
+};
+
+int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                   uint32_t box_outer);
+// W: [N][K] bf16, X: [rows_cap][K] bf16.  Output pointers are filled by the caller.
+int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_cap, int epi,
+              int splits, int max_stages = 0);
+int gemm_run(const GemmPlan& p, cudaStream_t s);
+
+}  // namespace spectre

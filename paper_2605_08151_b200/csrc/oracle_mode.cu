@@ -285,7 +285,6 @@ k_oracle_decode_loop(SpectreOracleConfig cfg, const double* __restrict__ arrival
       auto ref = [&](int32_t q) { return ref_token(seed, r, (uint64_t)q); };
       int32_t pos = ws.pos[i];
       int32_t prep_len = 0, prep_start = 0;
-      int32_t rep_len = 0;
       const bool queried = spec && ((mode == 'P') || (mode == 'O' && ws.cached_len[i] == 0));
       // parallel: assemble from the state BEFORE the query (sim.py:594-598)
       int32_t kind, cstart, clen;
@@ -332,7 +331,6 @@ k_oracle_decode_loop(SpectreOracleConfig cfg, const double* __restrict__ arrival
           }
           if (mode == 'O') {
             if (hl != pos) block_fail(out.scalars, kErrMisanchored, i);
-            rep_len = count;
           } else {
             prep_len = count;
             prep_start = hl;
@@ -341,7 +339,6 @@ k_oracle_decode_loop(SpectreOracleConfig cfg, const double* __restrict__ arrival
         }
         ws.hist_len[i] = hl;
       }
-      (void)rep_len;
       // ---- verify (oracle.py:90-113)
       const int32_t acc = verify_prefix(cand, clen, cstart, ref);
       const uint64_t bonus = ref(cstart + acc);

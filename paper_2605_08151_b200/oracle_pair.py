@@ -76,12 +76,16 @@ class TokenStreamOracle:
         out = torch.empty(len(counts) * max(maxc, 1), dtype=torch.int64, device="cuda")
         u = t(uniforms, np.float64) if len(uniforms) else torch.zeros(1, dtype=torch.float64,
                                                                       device="cuda")
+        keep = [t(requests, np.int64), t(starts, np.int64), t(counts, np.int32),
+                t(off, np.int64)]                      # alive until the kernel ran
         _native.check(L.spectre_oracle_propose(
-            self.seed & _MASK, float(alpha), t(requests, np.int64).data_ptr(),
-            t(starts, np.int64).data_ptr(), t(counts, np.int32).data_ptr(),
-            t(off, np.int64).data_ptr(), u.data_ptr(), out.data_ptr(), maxc, len(counts),
+            self.seed & _MASK, float(alpha), keep[0].data_ptr(), keep[1].data_ptr(),
+            keep[2].data_ptr(), keep[3].data_ptr(), u.data_ptr(), out.data_ptr(), maxc,
+            len(counts),
             _native.stream_ptr()), "spectre_oracle_propose")
-        return out.cpu().numpy().view(np.uint64).reshape(len(counts), max(maxc, 1))
+        res = out.cpu().numpy().view(np.uint64).reshape(len(counts), max(maxc, 1))
+        del keep
+        return res
 
     # -- reference duck type (oracle.py:53-113) ---------------------------------
     def reference_token(self, request: int, position: int) -> int:

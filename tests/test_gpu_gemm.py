@@ -1,0 +1,127 @@
+"""tcgen05 weight-streaming GEMM vs a plain PyTorch fp32 reference.
+
+Tolerance: inputs are bf16, accumulation fp32 on both sides; only the
+summation order differs, so |err| <= 2e-3 * (|x|.|w| row norm) suffices.
+Batch invariance (row t identical for any token count T) is checked bit-exact:
+it is what makes the speculative stream equal the autoregressive one.
+"""
+
+import ctypes as C
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PARTIAL, ARGMAX, SWIGLU = 0, 1, 2
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2605_08151_b200 import _native
+    L = _native.lib()
+    fn = L.spectre_gemm_bf16
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p] * 3 + [C.c_int32] * 6 + [C.c_void_p] * 4 + [C.c_int32] * 2 + \
+        [C.c_void_p]
+    return torch, _native, fn
+
+
+def _run(env, X, W, T, rows_cap, splits=1, epi=PARTIAL, t_dev=None, max_stages=0):
+    torch, _native, fn = env
+    N, K = W.shape
+    dev = X.device
+    part = torch.zeros(splits, rows_cap, N, dtype=torch.float32, device=dev)
+    n_tiles = (N + 127) // 128
+    av = torch.zeros(n_tiles, rows_cap, dtype=torch.float32, device=dev)
+    ai = torch.zeros(n_tiles, rows_cap, dtype=torch.int32, device=dev)
+    act = torch.zeros(rows_cap, max(N // 2, 1), dtype=torch.bfloat16, device=dev)
+    st = fn(X.data_ptr(), W.data_ptr(), t_dev.data_ptr() if t_dev is not None else None, T,
+            rows_cap, N, K, splits, epi, part.data_ptr(), av.data_ptr(), ai.data_ptr(),
+            act.data_ptr(), act.shape[1], max_stages, _native.stream_ptr())
+    _native.check(st, "spectre_gemm_bf16")
+    torch.cuda.synchronize()
+    return part, av, ai, act
+
+
+def _ref(torch, X, W, T):
+    return X[:T].float() @ W.float().t()
+
+
+@pytest.mark.parametrize("T,rows_cap,N,K,splits", [
+    (1, 64, 256, 64, 1), (16, 64, 384, 512, 1), (64, 64, 1024, 2048, 2),
+    (37, 64, 640, 1024, 3), (256, 256, 6144, 4096, 3), (200, 256, 512, 4096, 4),
+    (320, 320, 1024, 4096, 4), (512, 512, 256, 256, 1), (130, 192, 768, 1024, 1)])
+def test_partial_matches_fp32(env, T, rows_cap, N, K, splits):
+    torch = env[0]
+    g = torch.Generator(device="cuda").manual_seed(T * 7 + N)
+    X = torch.randn(rows_cap, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    part, *_ = _run(env, X, W, T, rows_cap, splits)
+    got = part.sum(0)[:T]
+    want = _ref(torch, X, W, T)
+    scale = (X[:T].float().abs() @ W.float().abs().t()) + 1e-3
+    assert ((got - want).abs() / scale).max().item() < 2e-3
+
+
+def test_runtime_token_count_and_stage_variants(env):
+    torch = env[0]
+    X = torch.randn(256, 1024, device="cuda").bfloat16()
+    W = (torch.randn(512, 1024, device="cuda") * 0.05).bfloat16()
+    want = _ref(torch, X, W, 96)
+    for stages in (2, 3, 8):
+        t_dev = torch.tensor([96], dtype=torch.int32, device="cuda")
+        part, *_ = _run(env, X, W, 0, 256, 2, t_dev=t_dev, max_stages=stages)
+        got = part.sum(0)[:96]
+        assert torch.allclose(got, want, atol=5e-2, rtol=1e-2)
+
+
+def test_batch_invariance_bitwise(env):
+    """Row t of Y must be bit-identical whatever the number of tokens T."""
+    torch = env[0]
+    X = torch.randn(320, 2048, device="cuda").bfloat16()
+    W = (torch.randn(1024, 2048, device="cuda") * 0.05).bfloat16()
+    outs = {}
+    for T in (1, 5, 16, 64, 100, 256, 320):
+        part, *_ = _run(env, X, W, T, 320, 2)
+        outs[T] = part[:, :T].clone()
+    for T, o in outs.items():
+        assert torch.equal(o[:, :1], outs[320][:, :1])
+        assert torch.equal(o, outs[320][:, :T])
+
+
+def test_argmax_epilogue(env):
+    torch = env[0]
+    V, K, T = 128256, 2048, 70
+    X = torch.randn(128, K, device="cuda").bfloat16()
+    W = (torch.randn(V, K, device="cuda") * 0.02).bfloat16()
+    _, av, ai, _ = _run(env, X, W, T, 128, 1, ARGMAX)
+    best = av[:, :T].argmax(0)
+    idx = ai[:, :T].gather(0, best[None]).squeeze(0).long()
+    logits = _ref(torch, X, W, T)
+    want = logits.argmax(1)
+    top2 = logits.topk(2, dim=1).values
+    margin = (top2[:, 0] - top2[:, 1])
+    clear = margin > 1e-2
+    assert torch.equal(idx[clear], want[clear])
+    assert clear.float().mean().item() > 0.9
+    # the reported max equals the fp32 logit at the chosen index (within tolerance)
+    got_max = av[:, :T].max(0).values
+    assert torch.allclose(got_max, logits.gather(1, idx[:, None]).squeeze(1), atol=2e-3, rtol=1e-3)
+
+
+def test_swiglu_epilogue(env):
+    torch = env[0]
+    F, K, T = 512, 1024, 48
+    X = torch.randn(64, K, device="cuda").bfloat16()
+    Wg = (torch.randn(F, K, device="cuda") * 0.05).bfloat16()
+    Wu = (torch.randn(F, K, device="cuda") * 0.05).bfloat16()
+    # interleave per 64 rows: [g0..g63, u0..u63, g64..g127, u64..u127, ...]
+    W = torch.stack([Wg.view(F // 64, 64, K), Wu.view(F // 64, 64, K)], 1).reshape(2 * F, K)
+    _, _, _, act = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU)
+    g = _ref(torch, X, Wg, T)
+    u = _ref(torch, X, Wu, T)
+    want = torch.nn.functional.silu(g) * u
+    assert torch.allclose(act[:T, :F].float(), want, atol=3e-2, rtol=2e-2)
