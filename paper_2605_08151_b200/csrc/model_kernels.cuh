@@ -1,0 +1,36 @@
+// model_kernels.cuh — forward-pass kernels other than the GEMM.
+//
+// Packed ragged batches: request b contributes n_new[b] consecutive token rows
+// starting at q_off[b]; its new tokens sit at absolute positions
+// pos0[b] .. pos0[b]+n_new[b]-1 and attend causally to its KV cache
+// [0, pos0[b]+n_new[b]).  The same kernels serve the target's gamma-token
+// verification pass, the draft's autoregressive steps (n_new = 1, or a short
+// catch-up after a rollback) and prompt prefill chunks.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cstdint>
+
+namespace spectre {
+
+struct AttnArgs {
+  const __nv_bfloat16* q;    // [rows][n_q][hd]
+  const __nv_bfloat16* k;    // layer base [n_slots][n_kv][ctx_cap][hd]
+  const __nv_bfloat16* v;
+  const int* q_off;          // [n_req]
+  const int* n_new;          // [n_req]
+  const int* pos0;           // [n_req]
+  const int* slot;           // [n_req] KV slot
+  int n_req, n_q, n_kv, ctx_cap;
+  int rb_max, split_max;
+  float scale_log2;          // hd^-0.5 * log2(e)
+  float* part_o;             // [n_req][n_kv][rb_max][split_max][rows_blk][hd]
+  float* part_ml;            // [n_req][n_kv][rb_max][split_max][rows_blk][2]
+  __nv_bfloat16* out;        // [rows][n_q][hd]
+};
+
+constexpr int kAttnChunk = 512;   // keys per CTA (one split)
+constexpr int kAttnSub = 32;      // keys per warp iteration
+constexpr int kAttnThreads = 128;
+
+}  // namespace spectre
