@@ -148,6 +148,127 @@ int spectre_oracle_run(const SpectreOracleConfig* cfg, const double* arrivals,
                        void* workspace, const SpectreOracleOutputs* out,
                        void* stream);
 
+
+/* ------------------------------------------------ tcgen05 GEMM (K1/K3) ----
+ * Y[t, n] = sum_k X[t, k] W[n, k]; X [rows_cap, K] bf16, W [N, K] bf16.
+ * The token count is t_dev[0] when t_dev != NULL (graph-capturable), else
+ * t_static.  epilogue 0: fp32 split-K partials [splits][rows_cap][N];
+ * 1: per-128-row-tile (max, argmax) [ceil(N/128)][rows_cap] (lm_head greedy);
+ * 2: SwiGLU over 64-row-interleaved gate/up weights -> act [rows_cap][ld_act]
+ * bf16.  Exposed for unit tests and the roofline bench; the engine calls the
+ * same kernels internally. */
+int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_dev, int32_t t_static,
+                      int32_t rows_cap, int32_t N, int32_t K, int32_t splits,
+                      int32_t epilogue, float* partial, float* amax_val, int32_t* amax_idx,
+                      void* act, int32_t ld_act, int32_t max_stages, void* stream);
+
+/* ------------------------------------------------ model mode (C2..C5) -----
+ * Replaces the reference's model pair (TokenStreamOracle, oracle.py:47-113)
+ * with a Llama-shaped bf16 target and draft on the device, and
+ * specsim.run's round loop (sim.py:514-760) with the device-resident round:
+ * controller -> [ordinary: draft repair] -> assemble -> verify forward ->
+ * [parallel: draft speculation overlapped on a second stream] -> accept.
+ * Weights and KV caches are caller-owned device buffers; the engine owns
+ * only the workspace carved from `workspace`. */
+typedef struct SpectreModelDims {
+  int32_t d_model;
+  int32_t n_layers;
+  int32_t n_q_heads;
+  int32_t n_kv_heads;
+  int32_t head_dim;
+  int32_t ffn;
+  int32_t vocab;
+  float rms_eps;
+  double rope_theta;
+} SpectreModelDims;
+
+typedef struct SpectreModelWeights {
+  const void* embed;        /* [vocab][d] bf16 */
+  const float* attn_norm;   /* [L][d] */
+  const void* wqkv;         /* [L][(nq + 2 nkv) hd][d] bf16 */
+  const void* wo;           /* [L][d][nq hd] bf16 */
+  const float* mlp_norm;    /* [L][d] */
+  const void* wgu;          /* [L][2 ffn][d] bf16, 64-row gate/up interleave */
+  const void* wd;           /* [L][d][ffn] bf16 */
+  const float* final_norm;  /* [d] */
+  const void* lm_head;      /* [vocab][d] bf16 */
+  void* k_cache;            /* [L][n_req][nkv][ctx_cap][hd] bf16 */
+  void* v_cache;
+} SpectreModelWeights;
+
+#define SPECTRE_CTRL_REFERENCE 0  /* r* from config t_target / t_draft (sim.py:431-445) */
+#define SPECTRE_CTRL_MEASURED 1   /* r* from device-timed T_T and T_D (paper Eq.) */
+#define SPECTRE_CTRL_ROUND 2      /* r* from measured parallel / ordinary round times */
+
+typedef struct SpectreDecodeConfig {
+  uint64_t seed;
+  int32_t n_req;
+  int32_t gamma;
+  int32_t output_len;
+  int32_t prompt_len;
+  int32_t variant;          /* SPECTRE_VARIANT_* */
+  int32_t controller;       /* SPECTRE_CTRL_* */
+  int32_t r_kind;           /* 0: r-hat = |R|/B (reference); 1: PADDED fraction */
+  int32_t max_rounds;       /* trace capacity */
+  int32_t ctx_cap;          /* KV capacity per request (absolute positions) */
+  int32_t has_fixed_l;
+  double alpha;             /* draft keep probability (controlled noise) */
+  double t_target;          /* CTRL_REFERENCE latencies (s) */
+  double t_draft;
+  double ema_decay;
+  double fixed_threshold_l;
+} SpectreDecodeConfig;
+
+size_t spectre_engine_workspace_bytes(const SpectreModelDims* target,
+                                      const SpectreModelDims* draft,
+                                      const SpectreDecodeConfig* cfg);
+/* Returns an opaque handle (NULL on error, see spectre_last_error). */
+void* spectre_engine_create(const SpectreModelDims* target, const SpectreModelWeights* tw,
+                            const SpectreModelDims* draft, const SpectreModelWeights* dw,
+                            const SpectreDecodeConfig* cfg, void* workspace,
+                            size_t workspace_bytes);
+int spectre_engine_destroy(void* engine);
+/* Prefill both models with prompts [n_req][prompt_len] (device int32) and
+ * commit output token 0 (target greedy) — admission (target_engine.py:105-126). */
+int spectre_engine_prefill(void* engine, const int32_t* prompts, void* stream);
+/* Run decode rounds on `stream` (draft work forks to an internal stream).
+ * Captures the round into a CUDA graph on first use (conditional nodes pick
+ * ordinary / parallel work on the device; use_graph=0 launches eagerly with
+ * one mode read-back per round).  Stops after max_rounds or when every
+ * request is done; *rounds_run receives the count (host-synchronising). */
+int spectre_engine_run(void* engine, int32_t max_rounds, int32_t use_graph,
+                       int32_t* rounds_run, void* stream);
+/* 1: the device-resident WHILE/IF round graph is in use; 2: graph capture
+ * failed and rounds run eagerly (reason in spectre_last_error); 0: not built. */
+int spectre_engine_graph_status(void* engine);
+/* Copy device state out: committed tokens [n_req][output_len] int64,
+ * committed_pos [n_req] int32, per-round trace (see SpectreRoundTrace). */
+typedef struct SpectreRoundTrace {
+  int32_t* mode;            /* 'O' 'P' 'F' */
+  int32_t* participants;
+  int32_t* delta;
+  int32_t* n_roll;
+  int32_t* content_sum;
+  int32_t* content_n;
+  int32_t* n_padded;
+  int64_t* t_round_ns;      /* device %globaltimer spans */
+  int64_t* t_verify_ns;
+  int64_t* t_draft_ns;
+  double* r_hat_ema;
+  double* accepted_len_ema;
+  double* r_star;
+} SpectreRoundTrace;
+int spectre_engine_read(void* engine, int64_t* committed, int32_t* committed_pos,
+                        const SpectreRoundTrace* trace, int32_t* n_rounds, void* stream);
+/* One forward pass over a packed ragged batch (tests / roofline):
+ * which 0 = target, 1 = draft.  tok/pos/slot [T]; per request q_off, n_new,
+ * pos0 [n_req] (n_new 0 = not participating).  out_tok [T] greedy argmax;
+ * out_x (optional) [T][d] bf16 final-normed hidden state. */
+int spectre_engine_forward(void* engine, int32_t which, const int32_t* tok,
+                           const int32_t* pos, const int32_t* slot, int32_t T,
+                           const int32_t* q_off, const int32_t* n_new, const int32_t* pos0,
+                           int32_t* out_tok, void* out_x, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -89,9 +89,52 @@ def lib():
     return L
 
 
+class ModelDims(C.Structure):
+    _fields_ = [("d_model", C.c_int32), ("n_layers", C.c_int32), ("n_q_heads", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn", C.c_int32),
+                ("vocab", C.c_int32), ("rms_eps", C.c_float), ("rope_theta", C.c_double)]
+
+
+class ModelWeights(C.Structure):
+    _fields_ = [(n, _P) for n in ("embed", "attn_norm", "wqkv", "wo", "mlp_norm", "wgu", "wd",
+                                  "final_norm", "lm_head", "k_cache", "v_cache")]
+
+
+class DecodeConfig(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("n_req", C.c_int32), ("gamma", C.c_int32),
+                ("output_len", C.c_int32), ("prompt_len", C.c_int32), ("variant", C.c_int32),
+                ("controller", C.c_int32), ("r_kind", C.c_int32), ("max_rounds", C.c_int32),
+                ("ctx_cap", C.c_int32), ("has_fixed_l", C.c_int32), ("alpha", C.c_double),
+                ("t_target", C.c_double), ("t_draft", C.c_double), ("ema_decay", C.c_double),
+                ("fixed_threshold_l", C.c_double)]
+
+
+TRACE_FIELDS = ("mode", "participants", "delta", "n_roll", "content_sum", "content_n",
+                "n_padded", "t_round_ns", "t_verify_ns", "t_draft_ns", "r_hat_ema",
+                "accepted_len_ema", "r_star")
+
+
+class RoundTraceBufs(C.Structure):
+    _fields_ = [(n, _P) for n in TRACE_FIELDS]
+
+
 def _bind_model(L) -> None:
-    """Model-mode entry points (bound lazily by .model when present)."""
-    return None
+    i32, i64 = C.c_int32, C.c_int64
+    _sig(L, "spectre_gemm_bf16", C.c_int,
+         [_P, _P, _P, i32, i32, i32, i32, i32, i32, _P, _P, _P, _P, i32, i32, _P])
+    _sig(L, "spectre_engine_workspace_bytes", C.c_size_t,
+         [C.POINTER(ModelDims), C.POINTER(ModelDims), C.POINTER(DecodeConfig)])
+    _sig(L, "spectre_engine_create", C.c_void_p,
+         [C.POINTER(ModelDims), C.POINTER(ModelWeights), C.POINTER(ModelDims),
+          C.POINTER(ModelWeights), C.POINTER(DecodeConfig), _P, C.c_size_t])
+    _sig(L, "spectre_engine_destroy", C.c_int, [_P])
+    _sig(L, "spectre_engine_prefill", C.c_int, [_P, _P, _P])
+    _sig(L, "spectre_engine_run", C.c_int, [_P, i32, i32, C.POINTER(i32), _P])
+    _sig(L, "spectre_engine_graph_status", C.c_int, [_P])
+    _sig(L, "spectre_engine_read", C.c_int,
+         [_P, _P, _P, C.POINTER(RoundTraceBufs), C.POINTER(i32), _P])
+    _sig(L, "spectre_engine_forward", C.c_int,
+         [_P, i32, _P, _P, _P, i32, _P, _P, _P, _P, _P, _P])
 
 
 def check(status: int, what: str) -> None:

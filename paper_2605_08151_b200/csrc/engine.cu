@@ -1,0 +1,662 @@
+// engine.cu — model-mode runtime: forward-pass sequencing for the target and
+// the draft, prefill/admission, and the decode round as a CUDA graph whose
+// ordinary / parallel branches are conditional nodes selected on the device
+// (no host round trip per round), looped by a device-side WHILE node.
+//
+// Round DAG (one WHILE iteration):
+//   round_begin (controller) ──► IF(ordinary){ draft repair: prep, (γ-1)×[fwd, append] }
+//        └────────────────────────┬──────────────────────────────────────────────┘
+//                                 ├──► IF(parallel){ draft speculation: prep, γ×[fwd, append] }  (2nd branch)
+//                                 └──► verify_prep ─► target forward ─┐
+//                                                       accept ◄──────┘◄── (join)
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+#include "engine_state.cuh"
+#include "gemm.h"
+#include "model_kernels.cuh"
+
+namespace spectre {
+
+int launch_attention(const AttnArgs& a, int hd, int mt, cudaStream_t s);
+int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void* E,
+                         const float* w, float* h, void* x, int d, float eps, cudaStream_t s);
+int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const int* t_dev,
+                            int t_cap, const float* w, float* h, void* x, int d, float eps,
+                            cudaStream_t s);
+int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t_dev, int t_cap,
+                       const int* tok_pos, const int* tok_slot, const void* rope, void* q,
+                       void* kc, void* vc, int n_q, int n_kv, int hd, int ctx_cap,
+                       cudaStream_t s);
+int launch_argmax_reduce(const float* val, const int* idx, int n_tiles, int rows_cap,
+                         const int* t_dev, int t_cap, int* out_tok, float* out_val,
+                         cudaStream_t s);
+int launch_rope_table(void* rope, int ctx_cap, int hd, double theta, cudaStream_t s);
+
+#define TRY(x)                 \
+  do {                         \
+    int _r = (x);              \
+    if (_r) return _r;         \
+  } while (0)
+
+struct Bump {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t n) {
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += (n * sizeof(T) + 255) & ~size_t(255);
+    return p;
+  }
+};
+
+static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+static int pick_splits(int n_tiles, int k_iters) {
+  int s = 148 / n_tiles;
+  if (s < 1) s = 1;
+  while (s > 1 && k_iters / s < 3) --s;
+  return s;
+}
+
+// ---------------------------------------------------------------- one model
+struct ModelRT {
+  SpectreModelDims dm{};
+  SpectreModelWeights w{};
+  int n_req = 0, rows_cap = 0, ctx_cap = 0, max_new = 1, split_max = 1, rb_cap = 1;
+  int sp_qkv = 1, sp_o = 1, sp_d = 1;
+  float* h = nullptr;
+  __nv_bfloat16 *x = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
+  float *part = nullptr, *att_o = nullptr, *att_ml = nullptr, *amax_v = nullptr;
+  int* amax_i = nullptr;
+  float2* rope = nullptr;
+  BatchDev bt{};
+  std::vector<GemmPlan> pq, po, pgu, pd;
+  GemmPlan plm{};
+
+  int nqkv() const { return (dm.n_q_heads + 2 * dm.n_kv_heads) * dm.head_dim; }
+  int group() const { return dm.n_q_heads / dm.n_kv_heads; }
+
+  void layout(Bump& b) {
+    const int d = dm.d_model, R = rows_cap;
+    const int qd = dm.n_q_heads * dm.head_dim;
+    sp_qkv = pick_splits((nqkv() + 127) / 128, d / 64);
+    sp_o = pick_splits((d + 127) / 128, qd / 64);
+    sp_d = pick_splits((d + 127) / 128, dm.ffn / 64);
+    size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
+    split_max = (ctx_cap + kAttnChunk - 1) / kAttnChunk;
+    rb_cap = (max_new * group() + 31) / 32;
+    h = b.take<float>((size_t)R * d);
+    x = b.take<__nv_bfloat16>((size_t)R * d);
+    q = b.take<__nv_bfloat16>((size_t)R * qd);
+    attn = b.take<__nv_bfloat16>((size_t)R * qd);
+    act = b.take<__nv_bfloat16>((size_t)R * dm.ffn);
+    part = b.take<float>(part_n * R);
+    const size_t att_rows = (size_t)n_req * dm.n_kv_heads * rb_cap * split_max * 32;
+    att_o = b.take<float>(att_rows * dm.head_dim);
+    att_ml = b.take<float>(att_rows * 2);
+    const int n_tiles = (dm.vocab + 127) / 128;
+    amax_v = b.take<float>((size_t)n_tiles * R);
+    amax_i = b.take<int>((size_t)n_tiles * R);
+    rope = b.take<float2>((size_t)ctx_cap * dm.head_dim / 2);
+    bt.tok = b.take<int>(R);
+    bt.pos = b.take<int>(R);
+    bt.slot = b.take<int>(R);
+    bt.out_tok = b.take<int>(R);
+    bt.t_dev = b.take<int>(1);
+    bt.q_off = b.take<int>(n_req);
+    bt.n_new = b.take<int>(n_req);
+    bt.pos0 = b.take<int>(n_req);
+    bt.rslot = b.take<int>(n_req);
+  }
+
+  int plan() {
+    const int d = dm.d_model, L = dm.n_layers, qd = dm.n_q_heads * dm.head_dim, F = dm.ffn;
+    auto bf = [](const void* p) { return reinterpret_cast<const __nv_bfloat16*>(p); };
+    pq.resize(L);
+    po.resize(L);
+    pgu.resize(L);
+    pd.resize(L);
+    for (int l = 0; l < L; ++l) {
+      TRY(gemm_plan(&pq[l], bf(w.wqkv) + (size_t)l * nqkv() * d, nqkv(), d, x, rows_cap,
+                    kPartial, sp_qkv));
+      TRY(gemm_plan(&po[l], bf(w.wo) + (size_t)l * d * qd, d, qd, attn, rows_cap, kPartial,
+                    sp_o));
+      TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
+                    1));
+      TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d));
+      for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) p->args.part = part;
+      pgu[l].args.act = act;
+      pgu[l].args.ld_act = F;
+      for (GemmPlan* p : {&pq[l], &po[l], &pgu[l], &pd[l]}) p->args.t_dev = bt.t_dev;
+    }
+    TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1));
+    plm.args.amax_val = amax_v;
+    plm.args.amax_idx = amax_i;
+    plm.args.t_dev = bt.t_dev;
+    return SPECTRE_OK;
+  }
+
+  // One forward pass over the packed batch in `bt`; `new_per_req` bounds
+  // n_new[b] (sizes the attention row blocks).
+  int forward(int new_per_req, cudaStream_t s, void* out_x = nullptr) {
+    const int d = dm.d_model, L = dm.n_layers, hd = dm.head_dim;
+    const float eps = dm.rms_eps;
+    const int rows = new_per_req * group();
+    const int mt = rows <= 16 ? 1 : 2;
+    AttnArgs a{};
+    a.q = q;
+    a.q_off = bt.q_off;
+    a.n_new = bt.n_new;
+    a.pos0 = bt.pos0;
+    a.slot = bt.rslot;
+    a.n_req = n_req;
+    a.n_q = dm.n_q_heads;
+    a.n_kv = dm.n_kv_heads;
+    a.ctx_cap = ctx_cap;
+    a.rb_max = (rows + 16 * mt - 1) / (16 * mt);
+    if (a.rb_max * mt > rb_cap * 2) return arg_fail("forward: rows per request exceed capacity");
+    a.split_max = split_max;
+    a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
+    a.part_o = att_o;
+    a.part_ml = att_ml;
+    a.out = attn;
+    const size_t kv_layer = (size_t)n_req * dm.n_kv_heads * ctx_cap * hd;
+    auto* kc = reinterpret_cast<__nv_bfloat16*>(w.k_cache);
+    auto* vc = reinterpret_cast<__nv_bfloat16*>(w.v_cache);
+    TRY(launch_embed_rmsnorm(bt.tok, bt.t_dev, rows_cap, w.embed, w.attn_norm, h, x, d, eps, s));
+    for (int l = 0; l < L; ++l) {
+      TRY(gemm_run(pq[l], s));
+      TRY(launch_qkv_rope_kv(part, sp_qkv, rows_cap, bt.t_dev, rows_cap, bt.pos, bt.slot, rope,
+                             q, kc + l * kv_layer, vc + l * kv_layer, dm.n_q_heads,
+                             dm.n_kv_heads, hd, ctx_cap, s));
+      a.k = kc + l * kv_layer;
+      a.v = vc + l * kv_layer;
+      TRY(launch_attention(a, hd, mt, s));
+      TRY(gemm_run(po[l], s));
+      TRY(launch_residual_rmsnorm(part, sp_o, rows_cap, bt.t_dev, rows_cap,
+                                  w.mlp_norm + (size_t)l * d, h, x, d, eps, s));
+      TRY(gemm_run(pgu[l], s));
+      TRY(gemm_run(pd[l], s));
+      const float* next = (l + 1 < L) ? w.attn_norm + (size_t)(l + 1) * d : w.final_norm;
+      TRY(launch_residual_rmsnorm(part, sp_d, rows_cap, bt.t_dev, rows_cap, next, h, x, d, eps,
+                                  s));
+    }
+    TRY(gemm_run(plm, s));
+    TRY(launch_argmax_reduce(amax_v, amax_i, plm.n_tiles, rows_cap, bt.t_dev, rows_cap,
+                             bt.out_tok, nullptr, s));
+    if (out_x)
+      SPECTRE_CUDA_TRY(cudaMemcpyAsync(out_x, x, (size_t)rows_cap * d * 2,
+                                       cudaMemcpyDeviceToDevice, s));
+    return SPECTRE_OK;
+  }
+};
+
+// ------------------------------------------------------------------- engine
+struct Engine {
+  SpectreDecodeConfig cfg{};
+  ModelRT tgt, drf;
+  DecodeStateDev st{};
+  int prefill_cs = 1;
+  int draft_new_max = 1;
+  cudaStream_t s_draft = nullptr, s_cap = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaGraphExec_t exec_loop = nullptr;
+  cudaGraph_t graph_loop = nullptr;
+  int graph_failed = 0;
+  int* mode_host = nullptr;  // pinned
+  int warmed = 0;
+
+  ~Engine() {
+    if (exec_loop) cudaGraphExecDestroy(exec_loop);
+    if (graph_loop) cudaGraphDestroy(graph_loop);
+    if (s_draft) cudaStreamDestroy(s_draft);
+    if (s_cap) cudaStreamDestroy(s_cap);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (mode_host) cudaFreeHost(mode_host);
+  }
+
+  static void sizes(const SpectreModelDims& t, const SpectreModelDims& d,
+                    const SpectreDecodeConfig& c, int* rows_t, int* rows_d, int* cs, int* dnew) {
+    *cs = std::max(1, std::min(8, 512 / std::max(1, c.n_req)));
+    *dnew = 2 * c.gamma + 4;
+    *rows_t = round_up(std::max(c.n_req * (c.gamma + 1), c.n_req * *cs), 64);
+    *rows_d = round_up(std::max(c.n_req * *dnew, c.n_req * *cs), 64);
+  }
+
+  void layout(Bump& b) {
+    const int n = cfg.n_req, G = cfg.gamma + 1;
+    tgt.layout(b);
+    drf.layout(b);
+    st.pos = b.take<int>(n);
+    st.done = b.take<int>(n);
+    st.synced = b.take<int>(n);
+    st.cached_len = b.take<int>(n);
+    st.cached_start = b.take<int>(n);
+    st.in_rollback = b.take<int>(n);
+    st.hist_len = b.take<int>(n);
+    st.kvd = b.take<int>(n);
+    st.gen_count = b.take<int>(n);
+    st.gen_done = b.take<int>(n);
+    st.gen_start = b.take<int>(n);
+    st.vkind = b.take<int>(n);
+    st.vcand_n = b.take<int>(n);
+    st.delta = b.take<int>(n);
+    st.rolled = b.take<int>(n);
+    st.committed = b.take<uint64_t>((size_t)n * cfg.output_len);
+    st.hist = b.take<uint64_t>((size_t)n * st.hist_cap);
+    st.cached_tok = b.take<uint64_t>((size_t)n * G);
+    st.cand_tok = b.take<uint64_t>((size_t)n * G);
+    st.ctrl = b.take<CtrlDev>(1);
+    const int R = cfg.max_rounds;
+    st.trace.mode = b.take<int>(R);
+    st.trace.participants = b.take<int>(R);
+    st.trace.delta = b.take<int>(R);
+    st.trace.n_roll = b.take<int>(R);
+    st.trace.content_sum = b.take<int>(R);
+    st.trace.content_n = b.take<int>(R);
+    st.trace.n_padded = b.take<int>(R);
+    st.trace.t_round_ns = b.take<long long>(R);
+    st.trace.t_verify_ns = b.take<long long>(R);
+    st.trace.t_draft_ns = b.take<long long>(R);
+    st.trace.r_hat_ema = b.take<double>(R);
+    st.trace.accepted_len_ema = b.take<double>(R);
+    st.trace.r_star = b.take<double>(R);
+  }
+
+  void configure(const SpectreModelDims& t, const SpectreModelWeights& tw,
+                 const SpectreModelDims& d, const SpectreModelWeights& dw,
+                 const SpectreDecodeConfig& c) {
+    cfg = c;
+    int rt, rd;
+    sizes(t, d, c, &rt, &rd, &prefill_cs, &draft_new_max);
+    tgt.dm = t;
+    tgt.w = tw;
+    tgt.n_req = c.n_req;
+    tgt.rows_cap = rt;
+    tgt.ctx_cap = c.ctx_cap;
+    tgt.max_new = std::max(c.gamma + 1, prefill_cs);
+    drf.dm = d;
+    drf.w = dw;
+    drf.n_req = c.n_req;
+    drf.rows_cap = rd;
+    drf.ctx_cap = c.ctx_cap;
+    drf.max_new = std::max(draft_new_max, prefill_cs);
+    st.n_req = c.n_req;
+    st.gamma = c.gamma;
+    st.out_len = c.output_len;
+    st.prompt_len = c.prompt_len;
+    st.vocab = d.vocab;
+    st.variant = c.variant;
+    st.controller = c.controller;
+    st.r_kind = c.r_kind;
+    st.max_rounds = c.max_rounds;
+    st.has_fixed_l = c.has_fixed_l;
+    st.hist_cap = c.ctx_cap - c.prompt_len;
+    st.seed = c.seed;
+    st.alpha = c.alpha;
+    st.t_target = c.t_target;
+    st.t_draft = c.t_draft;
+    st.ema_decay = c.ema_decay;
+    st.fixed_l = c.fixed_threshold_l;
+    st.use_handles = 0;
+  }
+
+  // ---- round pieces
+  int draft_phase(int which, cudaStream_t s) {
+    TRY(launch_draft_prep(st, drf.bt, which, s));
+    const int steps = which == 'O' ? cfg.gamma - 1 : cfg.gamma;
+    for (int i = 0; i < steps; ++i) {
+      TRY(drf.forward(i == 0 ? draft_new_max : 1, s));
+      TRY(launch_draft_append(st, drf.bt, which, i == steps - 1, s));
+    }
+    return SPECTRE_OK;
+  }
+  int verify_phase(cudaStream_t s) {
+    TRY(launch_verify_prep(st, tgt.bt, s));
+    TRY(tgt.forward(cfg.gamma + 1, s));
+    return SPECTRE_OK;
+  }
+
+  int round_eager(cudaStream_t s, int* mode_out) {
+    TRY(launch_round_begin(st, s));
+    SPECTRE_CUDA_TRY(cudaMemcpyAsync(mode_host, &st.ctrl->mode, sizeof(int),
+                                     cudaMemcpyDeviceToHost, s));
+    SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
+    const int mode = *mode_host;
+    *mode_out = mode;
+    if (mode == 0) return SPECTRE_OK;
+    if (mode == 'O') TRY(draft_phase('O', s));
+    if (mode == 'P') {
+      SPECTRE_CUDA_TRY(cudaEventRecord(ev_fork, s));
+      SPECTRE_CUDA_TRY(cudaStreamWaitEvent(s_draft, ev_fork, 0));
+      TRY(draft_phase('P', s_draft));
+      SPECTRE_CUDA_TRY(cudaEventRecord(ev_join, s_draft));
+    }
+    TRY(verify_phase(s));
+    if (mode == 'P') SPECTRE_CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
+    TRY(launch_accept(st, tgt.bt, s));
+    return SPECTRE_OK;
+  }
+
+  // Capture a conditional IF node at the current capture point of `s`, with
+  // its body captured from `fn` on the helper capture stream.
+  template <class Fn>
+  int add_if_node(cudaStream_t s, cudaGraphConditionalHandle hnd, Fn fn, bool update_deps,
+                  cudaGraphNode_t* node_out) {
+    cudaStreamCaptureStatus status;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    SPECTRE_CUDA_TRY(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, &deps, &ndeps));
+    cudaGraphNodeParams p{};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = hnd;
+    p.conditional.type = cudaGraphCondTypeIf;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    SPECTRE_CUDA_TRY(cudaGraphAddNode(&node, g, deps, ndeps, &p));
+    cudaGraph_t body = p.conditional.phGraph_out[0];
+    SPECTRE_CUDA_TRY(cudaStreamBeginCaptureToGraph(s_cap, body, nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeRelaxed));
+    int r = fn(s_cap);
+    cudaGraph_t out;
+    cudaError_t e = cudaStreamEndCapture(s_cap, &out);
+    if (r) return r;
+    SPECTRE_CUDA_TRY(e);
+    if (update_deps)
+      SPECTRE_CUDA_TRY(
+          cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    *node_out = node;
+    return SPECTRE_OK;
+  }
+
+  int build_loop_graph(cudaStream_t s) {
+    cudaGraph_t g;
+    SPECTRE_CUDA_TRY(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_loop, h_ord, h_par;
+    SPECTRE_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault));
+    SPECTRE_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_ord, g, 0, cudaGraphCondAssignDefault));
+    SPECTRE_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_par, g, 0, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams wp{};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = h_loop;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    SPECTRE_CUDA_TRY(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    DecodeStateDev saved = st;
+    st.h_loop = h_loop;
+    st.h_ord = h_ord;
+    st.h_par = h_par;
+    st.use_handles = 1;
+    int r = SPECTRE_OK;
+    SPECTRE_CUDA_TRY(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeRelaxed));
+    do {
+      if ((r = launch_round_begin(st, s))) break;
+      cudaGraphNode_t n_ord, n_par;
+      if ((r = add_if_node(s, h_ord, [&](cudaStream_t cs) { return draft_phase('O', cs); }, true,
+                           &n_ord)))
+        break;
+      // parallel branch hangs off the same point; the stream keeps going
+      if ((r = add_if_node(s, h_par, [&](cudaStream_t cs) { return draft_phase('P', cs); },
+                           false, &n_par)))
+        break;
+      if ((r = verify_phase(s))) break;
+      cudaError_t e =
+          cudaStreamUpdateCaptureDependencies(s, &n_par, 1, cudaStreamAddCaptureDependencies);
+      if (e != cudaSuccess) {
+        r = cuda_fail(e, "cudaStreamUpdateCaptureDependencies");
+        break;
+      }
+      if ((r = launch_accept(st, tgt.bt, s))) break;
+    } while (0);
+    cudaGraph_t captured;
+    cudaError_t e = cudaStreamEndCapture(s, &captured);
+    if (!r && e != cudaSuccess) r = cuda_fail(e, "cudaStreamEndCapture(loop body)");
+    if (!r) {
+      e = cudaGraphInstantiate(&exec_loop, g, 0);
+      if (e != cudaSuccess) r = cuda_fail(e, "cudaGraphInstantiate(loop)");
+    }
+    if (r) {
+      cudaGraphDestroy(g);
+      st = saved;
+      exec_loop = nullptr;
+      cudaGetLastError();
+      return r;
+    }
+    graph_loop = g;
+    return SPECTRE_OK;
+  }
+};
+
+}  // namespace spectre
+
+using namespace spectre;
+
+static bool dims_ok(const SpectreModelDims* m) {
+  return m && m->d_model % 64 == 0 && m->n_layers > 0 && m->n_kv_heads > 0 &&
+         m->n_q_heads % m->n_kv_heads == 0 && (m->head_dim == 64 || m->head_dim == 128) &&
+         m->ffn % 64 == 0 && m->vocab > 1 && (m->n_q_heads * m->head_dim) % 64 == 0;
+}
+
+extern "C" size_t spectre_engine_workspace_bytes(const SpectreModelDims* target,
+                                                 const SpectreModelDims* draft,
+                                                 const SpectreDecodeConfig* cfg) {
+  if (!dims_ok(target) || !dims_ok(draft) || !cfg) return 0;
+  Engine e;
+  e.configure(*target, SpectreModelWeights{}, *draft, SpectreModelWeights{}, *cfg);
+  Bump b{nullptr};
+  e.layout(b);
+  return b.off + 1024;
+}
+
+extern "C" void* spectre_engine_create(const SpectreModelDims* target,
+                                       const SpectreModelWeights* tw,
+                                       const SpectreModelDims* draft,
+                                       const SpectreModelWeights* dw,
+                                       const SpectreDecodeConfig* cfg, void* workspace,
+                                       size_t workspace_bytes) {
+  if (!dims_ok(target) || !dims_ok(draft) || !tw || !dw || !cfg || !workspace) {
+    arg_fail("spectre_engine_create: dims / pointers");
+    return nullptr;
+  }
+  if (cfg->n_req < 1 || cfg->n_req > 1024 || cfg->gamma < 1 || cfg->gamma > 16 ||
+      cfg->output_len < 2 || cfg->prompt_len < 1 || cfg->max_rounds < 1 ||
+      cfg->ctx_cap < cfg->prompt_len + cfg->output_len + 4 * cfg->gamma + 16 ||
+      target->vocab != draft->vocab) {
+    arg_fail("spectre_engine_create: decode config");
+    return nullptr;
+  }
+  auto e = std::make_unique<Engine>();
+  e->configure(*target, *tw, *draft, *dw, *cfg);
+  Bump b{reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255))};
+  e->layout(b);
+  if (b.off + 256 > workspace_bytes) {
+    arg_fail("spectre_engine_create: workspace too small");
+    return nullptr;
+  }
+  if (e->tgt.plan() || e->drf.plan()) return nullptr;
+  if (cudaStreamCreateWithFlags(&e->s_draft, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&e->s_cap, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMallocHost(&e->mode_host, sizeof(int)) != cudaSuccess) {
+    cuda_fail(cudaGetLastError(), "spectre_engine_create: streams");
+    return nullptr;
+  }
+  if (launch_rope_table(e->tgt.rope, cfg->ctx_cap, target->head_dim, target->rope_theta,
+                        nullptr) ||
+      launch_rope_table(e->drf.rope, cfg->ctx_cap, draft->head_dim, draft->rope_theta, nullptr))
+    return nullptr;
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    cuda_fail(cudaGetLastError(), "spectre_engine_create: init");
+    return nullptr;
+  }
+  return e.release();
+}
+
+extern "C" int spectre_engine_destroy(void* engine) {
+  delete reinterpret_cast<Engine*>(engine);
+  return SPECTRE_OK;
+}
+
+extern "C" int spectre_engine_prefill(void* engine, const int32_t* prompts, void* stream) {
+  auto* e = reinterpret_cast<Engine*>(engine);
+  if (!e || !prompts) return arg_fail("spectre_engine_prefill");
+  cudaStream_t s = as_stream(stream);
+  const int P = e->cfg.prompt_len, cs = e->prefill_cs;
+  for (ModelRT* m : {&e->drf, &e->tgt}) {
+    for (int c0 = 0; c0 < P; c0 += cs) {
+      TRY(launch_prefill_batch(prompts, P, e->cfg.n_req, c0, cs, m->bt, s));
+      TRY(m->forward(cs, s));
+    }
+  }
+  TRY(launch_admit(e->st, e->tgt.bt, s));
+  return SPECTRE_OK;
+}
+
+extern "C" int spectre_engine_run(void* engine, int32_t max_rounds, int32_t use_graph,
+                                  int32_t* rounds_run, void* stream) {
+  auto* e = reinterpret_cast<Engine*>(engine);
+  if (!e || max_rounds < 0) return arg_fail("spectre_engine_run");
+  cudaStream_t s = as_stream(stream);
+  // round limit = rounds already done + max_rounds (device-side counter)
+  int done_before = 0;
+  SPECTRE_CUDA_TRY(cudaMemcpyAsync(e->mode_host, &e->st.ctrl->round, sizeof(int),
+                                   cudaMemcpyDeviceToHost, s));
+  SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
+  done_before = *e->mode_host;
+  const int limit = (int)std::min<long long>((long long)done_before + max_rounds, 0x7fffffff);
+  SPECTRE_CUDA_TRY(cudaMemcpyAsync(&e->st.ctrl->round_limit, &limit, sizeof(int),
+                                   cudaMemcpyHostToDevice, s));
+  if (use_graph && !e->graph_failed) {
+    if (!e->exec_loop) {
+      if (!e->warmed) {
+        // one eager round primes every kernel attribute outside capture
+        int mode;
+        TRY(e->round_eager(s, &mode));
+        e->warmed = 1;
+      }
+      if (e->build_loop_graph(s)) {
+        e->graph_failed = 1;  // fall back to eager rounds (reason in spectre_last_error)
+      }
+    }
+    if (e->exec_loop) SPECTRE_CUDA_TRY(cudaGraphLaunch(e->exec_loop, s));
+  }
+  if (!use_graph || e->graph_failed) {
+    for (int i = 0; i < max_rounds + 1; ++i) {
+      int mode;
+      TRY(e->round_eager(s, &mode));
+      if (mode == 0) break;
+    }
+  }
+  if (rounds_run) {
+    SPECTRE_CUDA_TRY(cudaMemcpyAsync(e->mode_host, &e->st.ctrl->round, sizeof(int),
+                                     cudaMemcpyDeviceToHost, s));
+    SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
+    *rounds_run = *e->mode_host - done_before;
+  }
+  return SPECTRE_OK;
+}
+
+extern "C" int spectre_engine_graph_status(void* engine) {
+  auto* e = reinterpret_cast<Engine*>(engine);
+  if (!e) return -1;
+  return e->exec_loop ? 1 : (e->graph_failed ? 2 : 0);
+}
+
+extern "C" int spectre_engine_read(void* engine, int64_t* committed, int32_t* committed_pos,
+                                   const SpectreRoundTrace* trace, int32_t* n_rounds,
+                                   void* stream) {
+  auto* e = reinterpret_cast<Engine*>(engine);
+  if (!e) return arg_fail("spectre_engine_read");
+  cudaStream_t s = as_stream(stream);
+  const int n = e->cfg.n_req;
+  if (committed)
+    SPECTRE_CUDA_TRY(cudaMemcpyAsync(committed, e->st.committed,
+                                     (size_t)n * e->cfg.output_len * 8,
+                                     cudaMemcpyDeviceToDevice, s));
+  if (committed_pos)
+    SPECTRE_CUDA_TRY(
+        cudaMemcpyAsync(committed_pos, e->st.pos, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  CtrlDev c;
+  SPECTRE_CUDA_TRY(cudaMemcpyAsync(&c, e->st.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
+  SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
+  const int R = std::min(c.round, e->cfg.max_rounds);
+  if (n_rounds) *n_rounds = R;
+  if (c.error) {
+    set_last_error("device protocol violation code " + std::to_string(c.error) +
+                   " (request " + std::to_string(c.error_req) + ")");
+    return SPECTRE_EINVAL;
+  }
+  if (trace && R > 0) {
+    const RoundTraceDev& t = e->st.trace;
+    auto cp = [&](void* dst, const void* src, size_t bytes) -> int {
+      if (!dst) return 0;
+      SPECTRE_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+      return 0;
+    };
+    TRY(cp(trace->mode, t.mode, R * 4));
+    TRY(cp(trace->participants, t.participants, R * 4));
+    TRY(cp(trace->delta, t.delta, R * 4));
+    TRY(cp(trace->n_roll, t.n_roll, R * 4));
+    TRY(cp(trace->content_sum, t.content_sum, R * 4));
+    TRY(cp(trace->content_n, t.content_n, R * 4));
+    TRY(cp(trace->n_padded, t.n_padded, R * 4));
+    TRY(cp(trace->t_round_ns, t.t_round_ns, R * 8));
+    TRY(cp(trace->t_verify_ns, t.t_verify_ns, R * 8));
+    TRY(cp(trace->t_draft_ns, t.t_draft_ns, R * 8));
+    TRY(cp(trace->r_hat_ema, t.r_hat_ema, R * 8));
+    TRY(cp(trace->accepted_len_ema, t.accepted_len_ema, R * 8));
+    TRY(cp(trace->r_star, t.r_star, R * 8));
+  }
+  return SPECTRE_OK;
+}
+
+extern "C" int spectre_engine_forward(void* engine, int32_t which, const int32_t* tok,
+                                      const int32_t* pos, const int32_t* slot, int32_t T,
+                                      const int32_t* q_off, const int32_t* n_new,
+                                      const int32_t* pos0, int32_t* out_tok, void* out_x,
+                                      void* stream) {
+  auto* e = reinterpret_cast<Engine*>(engine);
+  if (!e || (which != 0 && which != 1)) return arg_fail("spectre_engine_forward");
+  ModelRT& m = which == 0 ? e->tgt : e->drf;
+  if (T < 0 || T > m.rows_cap) return arg_fail("spectre_engine_forward: T > rows_cap");
+  cudaStream_t s = as_stream(stream);
+  const int n = e->cfg.n_req;
+  auto d2d = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s);
+  };
+  if (T > 0) {
+    SPECTRE_CUDA_TRY(d2d(m.bt.tok, tok, (size_t)T * 4));
+    SPECTRE_CUDA_TRY(d2d(m.bt.pos, pos, (size_t)T * 4));
+    SPECTRE_CUDA_TRY(d2d(m.bt.slot, slot, (size_t)T * 4));
+  }
+  SPECTRE_CUDA_TRY(d2d(m.bt.q_off, q_off, (size_t)n * 4));
+  SPECTRE_CUDA_TRY(d2d(m.bt.n_new, n_new, (size_t)n * 4));
+  SPECTRE_CUDA_TRY(d2d(m.bt.pos0, pos0, (size_t)n * 4));
+  std::vector<int> ident(n);
+  for (int i = 0; i < n; ++i) ident[i] = i;
+  SPECTRE_CUDA_TRY(cudaMemcpyAsync(m.bt.rslot, ident.data(), (size_t)n * 4,
+                                   cudaMemcpyHostToDevice, s));
+  SPECTRE_CUDA_TRY(cudaMemcpyAsync(m.bt.t_dev, &T, 4, cudaMemcpyHostToDevice, s));
+  int max_new = 1;
+  {
+    std::vector<int> nn(n);
+    SPECTRE_CUDA_TRY(cudaMemcpyAsync(nn.data(), n_new, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int v : nn) max_new = std::max(max_new, v);
+  }
+  TRY(m.forward(max_new, s, out_x));
+  if (T > 0) SPECTRE_CUDA_TRY(d2d(out_tok, m.bt.out_tok, (size_t)T * 4));
+  SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
+  return SPECTRE_OK;
+}

@@ -1,0 +1,101 @@
+// engine_state.cuh — device-resident state of the model-mode decode loop.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace spectre {
+
+// Packed ragged batch fed to one forward pass (see model_kernels.cuh).
+struct BatchDev {
+  int* tok;      // [rows_cap]
+  int* pos;      // [rows_cap] absolute positions
+  int* slot;     // [rows_cap] KV slot (request index)
+  int* t_dev;    // [1] token rows this pass
+  int* q_off;    // [n_req]
+  int* n_new;    // [n_req]
+  int* pos0;     // [n_req]
+  int* rslot;    // [n_req] (identity)
+  int* out_tok;  // [rows_cap] greedy argmax per row
+};
+
+// Controller + clock, one instance.
+struct CtrlDev {
+  int mode;          // this round: 'O', 'P', 'F'; 0 = finished
+  int prev_mode;     // hybrid memory (sim.py:281, 466)
+  int has_ema;
+  int has_L;
+  double ema;        // r-hat EMA (sim.py:673-678)
+  double L;          // accepted-length EMA (target_engine.py:386-407)
+  int round;         // rounds completed
+  int round_limit;   // stop after this many rounds (host-set per run call)
+  int n_active;
+  int error;         // protocol violation code (0 = none)
+  int error_req;
+  long long t_round_begin, t_verify_begin, t_verify_end, t_draft_begin, t_draft_end;
+  int draft_steps;   // steps in the draft phase of this round
+  int has_tT, has_tD, has_tpar, has_tord;
+  double tT, tD, tpar, tord;   // measured EMAs (seconds)
+  double r_star;
+};
+
+struct RoundTraceDev {
+  int* mode;
+  int* participants;
+  int* delta;
+  int* n_roll;
+  int* content_sum;
+  int* content_n;
+  int* n_padded;
+  long long* t_round_ns;
+  long long* t_verify_ns;
+  long long* t_draft_ns;
+  double* r_hat_ema;
+  double* accepted_len_ema;
+  double* r_star;
+};
+
+struct DecodeStateDev {
+  int n_req, gamma, out_len, prompt_len, vocab, variant, controller, r_kind, max_rounds;
+  int has_fixed_l;
+  int hist_cap;      // draft history capacity (output positions)
+  uint64_t seed;
+  double alpha, t_target, t_draft, ema_decay, fixed_l;
+  // per request (SoA)
+  int* pos;          // committed_pos
+  int* done;
+  int* synced;
+  int* cached_len;
+  int* cached_start;
+  int* in_rollback;
+  int* hist_len;
+  int* kvd;          // draft KV valid length (output positions)
+  int* gen_count;    // draft tokens to generate this phase (0: not queried)
+  int* gen_done;
+  int* gen_start;
+  int* vkind;        // verify candidate kind this round
+  int* vcand_n;      // non-seed candidate tokens
+  int* delta;
+  int* rolled;
+  uint64_t* committed;   // [n_req][out_len]
+  uint64_t* hist;        // [n_req][hist_cap]
+  uint64_t* cached_tok;  // [n_req][gamma + 1]
+  uint64_t* cand_tok;    // [n_req][gamma + 1]
+  CtrlDev* ctrl;
+  RoundTraceDev trace;
+  cudaGraphConditionalHandle h_ord, h_par, h_loop;
+  int use_handles;
+};
+
+// launchers (model_protocol.cu)
+int launch_prefill_batch(const int* prompts, int prompt_len, int n_req, int c0, int cs,
+                         const BatchDev& bt, cudaStream_t s);
+int launch_admit(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);
+int launch_round_begin(const DecodeStateDev& st, cudaStream_t s);
+int launch_draft_prep(const DecodeStateDev& st, const BatchDev& bt, int which, cudaStream_t s);
+int launch_draft_append(const DecodeStateDev& st, const BatchDev& bt, int which, int last,
+                        cudaStream_t s);
+int launch_verify_prep(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);
+int launch_accept(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);
+
+}  // namespace spectre

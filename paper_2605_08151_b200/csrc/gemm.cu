@@ -80,9 +80,9 @@ static int launch_epi(const GemmPlan& p, cudaStream_t s) {
 
 int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_cap, int epi,
               int splits, int max_stages) {
-  if (N < 1 || K < 64 || K % 64 || rows_cap < 64 || rows_cap % 64 || rows_cap > 512 ||
-      splits < 1)
-    return arg_fail("gemm_plan: shape (K % 64, rows_cap in 64..512 step 64)");
+  if (N < 1 || K < 64 || K % 64 || rows_cap < 64 || rows_cap % 64 || splits < 1)
+    return arg_fail("gemm_plan: shape (K % 64, rows_cap multiple of 64)");
+  const int smem_rows = rows_cap < 512 ? rows_cap : 512;
   if (epi == kSwiGLU && (N % 128 || splits != 1)) return arg_fail("gemm_plan: swiglu shape");
   if (epi == kArgmax && splits != 1) return arg_fail("gemm_plan: argmax needs splits == 1");
   *p = GemmPlan{};
@@ -90,15 +90,16 @@ int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_
   if (int e = make_tmap_bf16(&p->tmap_x, X, (uint64_t)K, (uint64_t)rows_cap, 64)) return e;
   int stages = kGemmMaxStages;
   if (max_stages > 0 && max_stages < stages) stages = max_stages;
-  while (stages > 2 && gemm_smem_bytes(stages, rows_cap) > 232448) --stages;
-  if (gemm_smem_bytes(stages, rows_cap) > 232448) return arg_fail("gemm_plan: smem");
+  while (stages > 2 && gemm_smem_bytes(stages, smem_rows) > 232448) --stages;
+  if (gemm_smem_bytes(stages, smem_rows) > 232448) return arg_fail("gemm_plan: smem");
   const int n_tiles = (N + kGemmBlockN - 1) / kGemmBlockN;
   uint32_t cols = 32;
-  while (cols < (uint32_t)rows_cap) cols <<= 1;
+  while (cols < (uint32_t)smem_rows) cols <<= 1;
   p->epi = epi;
   p->tmem_cols = (int)cols;
   p->grid = n_tiles * splits;
-  p->smem = gemm_smem_bytes(stages, rows_cap);
+  p->smem = gemm_smem_bytes(stages, smem_rows);
+  p->args.smem_rows = smem_rows;
   p->args.N = N;
   p->args.K = K;
   p->args.rows_cap = rows_cap;

@@ -36,7 +36,9 @@ constexpr int kGemmMaxStages = 8;
 
 struct GemmArgs {
   int N, K;                 // weight rows, reduction length
-  int rows_cap;             // X rows staged per stage (multiple of 64, <= 512)
+  int rows_cap;             // X buffer rows (multiple of 64); tokens beyond 512 run
+                            // as extra passes that re-stream the weight tile
+  int smem_rows;            // X rows staged per stage = min(rows_cap, 512)
   const int* t_dev;         // runtime token count (nullptr: use t_static)
   int t_static;
   int splits;               // split-K factor
@@ -65,13 +67,14 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int stages = a.stages;
-  const int x_stage_bytes = a.rows_cap * 128;
+  const int x_stage_bytes = a.smem_rows * 128;
   uint8_t* w_smem = smem;                                    // stages * 16 KB
   uint8_t* x_smem = smem + stages * 16384;                   // stages * rows_cap*128
   uint64_t* full = reinterpret_cast<uint64_t*>(x_smem + stages * x_stage_bytes);
   uint64_t* empty = full + kGemmMaxStages;
   uint64_t* tmem_full = empty + kGemmMaxStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
   float* scratch = reinterpret_cast<float*>(smem + stages * (16384 + x_stage_bytes) + 1024);
 
   const int n_tiles = (a.N + kGemmBlockN - 1) / kGemmBlockN;
@@ -85,8 +88,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
 
   int T = a.t_dev ? *a.t_dev : a.t_static;
   T = T < 0 ? 0 : (T > a.rows_cap ? a.rows_cap : T);
-  const int t_pad = (T + 15) & ~15;
-  const int x_boxes = (T + 63) >> 6;
+  const int n_pass = (T + a.smem_rows - 1) / a.smem_rows;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_w);
@@ -96,6 +98,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
@@ -120,59 +123,79 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();   // weights stream through once
       const uint64_t pol_x = policy_evict_last();    // activations are re-read by every tile
-      const uint32_t tx = 16384u + (uint32_t)x_boxes * 8192u;
-      for (int i = 0; i < n_iters; ++i) {
-        const int s = i % stages;
-        const uint32_t ph = (uint32_t)(i / stages) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        mbar_arrive_expect_tx(&full[s], tx);
-        const int kc = (it_begin + i) * kGemmBlockK;
-        tma_load_2d(w_smem + s * 16384, &tmap_w, &full[s], kc, n0, pol_w);
-        for (int b = 0; b < x_boxes; ++b)
-          tma_load_2d(x_smem + s * x_stage_bytes + b * 8192, &tmap_x, &full[s], kc, b * 64,
-                      pol_x);
+      int g = 0;  // global pipeline iteration
+      for (int pass = 0; pass < n_pass; ++pass) {
+        const int r0 = pass * a.smem_rows;
+        const int rows = min(T - r0, a.smem_rows);
+        const int x_boxes = (rows + 63) >> 6;
+        const uint32_t tx = 16384u + (uint32_t)x_boxes * 8192u;
+        for (int i = 0; i < n_iters; ++i, ++g) {
+          const int s = g % stages;
+          const uint32_t ph = (uint32_t)(g / stages) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_arrive_expect_tx(&full[s], tx);
+          const int kc = (it_begin + i) * kGemmBlockK;
+          tma_load_2d(w_smem + s * 16384, &tmap_w, &full[s], kc, n0, pol_w);
+          for (int b = 0; b < x_boxes; ++b)
+            tma_load_2d(x_smem + s * x_stage_bytes + b * 8192, &tmap_x, &full[s], kc,
+                        r0 + b * 64, pol_x);
+        }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread)
-    const int n_chunk0 = t_pad < 256 ? t_pad : 256;
-    const int n_chunk1 = t_pad - n_chunk0;
-    const uint32_t id0 = idesc_bf16_f32(128, (uint32_t)n_chunk0);
-    const uint32_t id1 = idesc_bf16_f32(128, (uint32_t)(n_chunk1 > 0 ? n_chunk1 : 16));
-    for (int i = 0; i < n_iters; ++i) {
-      const int s = i % stages;
-      const uint32_t ph = (uint32_t)(i / stages) & 1u;
-      mbar_wait(&full[s], ph);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t wa = smem_u32(w_smem + s * 16384);
-        const uint32_t xa = smem_u32(x_smem + s * x_stage_bytes);
-#pragma unroll
-        for (int kk = 0; kk < kGemmBlockK / 16; ++kk) {
-          const uint64_t ad = umma_desc_sw128(wa + kk * 32);
-          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          mma_bf16_ss(tmem_base, ad, umma_desc_sw128(xa + kk * 32), id0, acc);
-          if (n_chunk1 > 0)
-            mma_bf16_ss(tmem_base + 256, ad, umma_desc_sw128(xa + 256 * 128 + kk * 32), id1,
-                        acc);
-        }
-        mma_commit(&empty[s]);
+    int g = 0;
+    for (int pass = 0; pass < n_pass; ++pass) {
+      const int rows = min(T - pass * a.smem_rows, a.smem_rows);
+      const int t_pad = (rows + 15) & ~15;
+      const int n_chunk0 = t_pad < 256 ? t_pad : 256;
+      const int n_chunk1 = t_pad - n_chunk0;
+      const uint32_t id0 = idesc_bf16_f32(128, (uint32_t)n_chunk0);
+      const uint32_t id1 = idesc_bf16_f32(128, (uint32_t)(n_chunk1 > 0 ? n_chunk1 : 16));
+      if (pass > 0) {  // epilogue must have drained the accumulator
+        mbar_wait(tmem_empty, (uint32_t)(pass - 1) & 1u);
+        tc_fence_after();
       }
+      for (int i = 0; i < n_iters; ++i, ++g) {
+        const int s = g % stages;
+        const uint32_t ph = (uint32_t)(g / stages) & 1u;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t wa = smem_u32(w_smem + s * 16384);
+          const uint32_t xa = smem_u32(x_smem + s * x_stage_bytes);
+#pragma unroll
+          for (int kk = 0; kk < kGemmBlockK / 16; ++kk) {
+            const uint64_t ad = umma_desc_sw128(wa + kk * 32);
+            const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+            mma_bf16_ss(tmem_base, ad, umma_desc_sw128(xa + kk * 32), id0, acc);
+            if (n_chunk1 > 0)
+              mma_bf16_ss(tmem_base + 256, ad, umma_desc_sw128(xa + 256 * 128 + kk * 32), id1,
+                          acc);
+          }
+          mma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mma_commit(tmem_full);
       __syncwarp();
     }
-    if (lane == 0) mma_commit(tmem_full);
-    __syncwarp();
   } else {
     // ---------------- epilogue warps 2..5 (TMEM lane quarter = warp % 4)
     const int q = warp & 3;
     const int row = (q << 5) + lane;
     const int n = n0 + row;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
     const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16);
-    for (int c0 = 0; c0 < t_pad; c0 += 16) {
+    for (int pass = 0; pass < n_pass; ++pass) {
+    mbar_wait(tmem_full, (uint32_t)pass & 1u);
+    tc_fence_after();
+    const int r0 = pass * a.smem_rows;
+    const int rows = min(T - r0, a.smem_rows);
+    const int t_pad = (rows + 15) & ~15;
+    for (int cc = 0; cc < t_pad; cc += 16) {
       float v[16];
-      tmem_ld16(tq + (uint32_t)c0, v);
+      tmem_ld16(tq + (uint32_t)cc, v);
+      const int c0 = r0 + cc;
       if (kEpi == kPartial) {
         if (n < a.N) {
           float* dst = a.part + ((size_t)split * a.rows_cap) * a.N + n;
@@ -238,6 +261,9 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
+    }
+    tc_fence_before();
+    mbar_arrive(tmem_empty);   // accumulator drained for the next pass
     }
   }
   tc_fence_before();

@@ -1,0 +1,513 @@
+// model_protocol.cu — the model-mode round: controller, draft sync / rebase /
+// catch-up, candidate assembly, fused accept (greedy verify + bonus + commit +
+// suffix reuse + rollback statistics + EMA updates), all on the device.
+//
+// The per-request rules are the reference's (protocol.cuh cites them); only
+// the "model pair" differs: the target's greedy token at output position q is
+// the argmax row of the verify forward instead of the hash stream, and draft
+// tokens come from the draft forward (+ controlled noise) instead of the
+// alpha-proposer.  Compiled with -fmad=false (controller doubles).
+#include "common.cuh"
+#include "engine_state.cuh"
+#include "protocol.cuh"
+
+namespace spectre {
+
+constexpr int kProtoThreads = 1024;
+
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// block-wide exclusive scan of v (requests strided by blockDim); returns total.
+__device__ int block_exclusive_scan(int v, int* out, int idx, int n, int* sh) {
+  // single pass when n <= blockDim
+  const int tid = threadIdx.x;
+  sh[tid] = (idx < n) ? v : 0;
+  __syncthreads();
+  for (int d = 1; d < blockDim.x; d <<= 1) {
+    const int x = tid >= d ? sh[tid - d] : 0;
+    __syncthreads();
+    sh[tid] += x;
+    __syncthreads();
+  }
+  if (idx < n) *out = sh[tid] - v;
+  const int total = sh[blockDim.x - 1];
+  __syncthreads();
+  return total;
+}
+
+__device__ __forceinline__ double u53(uint64_t h) { return (double)(h >> 11) * (1.0 / 9007199254740992.0); }
+
+// draft "controlled noise": keep the draft's greedy token with probability
+// alpha, else replace it with a different token (deterministic per position).
+__device__ __forceinline__ int noisy_draft_token(const DecodeStateDev& s, int req, int pos,
+                                                 int tok) {
+  if (s.alpha >= 1.0) return tok;
+  const uint64_t h = mix64(s.seed, 2, (uint64_t)req, (uint64_t)pos);
+  if (u53(h) < s.alpha) return tok;
+  const uint64_t r = mix64(s.seed, 3, (uint64_t)req, (uint64_t)pos);
+  return (int)(((uint64_t)tok + 1 + r % (uint64_t)(s.vocab - 1)) % (uint64_t)s.vocab);
+}
+
+// ------------------------------------------------------------ prefill helpers
+__global__ void k_prefill_batch(const int* prompts, int prompt_len, int n_req, int c0, int cs,
+                                BatchDev bt) {
+  const int b = threadIdx.x + blockIdx.x * blockDim.x;
+  const int n = min(cs, prompt_len - c0);
+  if (b == 0) *bt.t_dev = n * n_req;
+  if (b >= n_req) return;
+  bt.q_off[b] = b * n;
+  bt.n_new[b] = n;
+  bt.pos0[b] = c0;
+  bt.rslot[b] = b;
+  for (int j = 0; j < n; ++j) {
+    bt.tok[b * n + j] = prompts[(size_t)b * prompt_len + c0 + j];
+    bt.pos[b * n + j] = c0 + j;
+    bt.slot[b * n + j] = b;
+  }
+}
+
+// After the target's last prompt chunk: admission commits output token 0
+// (target_engine.py:105-126) and resets every round-protocol field.
+__global__ void k_admit(DecodeStateDev s, BatchDev bt) {
+  const int b = threadIdx.x + blockIdx.x * blockDim.x;
+  if (b == 0) {
+    CtrlDev& c = *s.ctrl;
+    c.mode = 0;
+    c.prev_mode = 0;
+    c.has_ema = c.has_L = 0;
+    c.ema = c.L = 0.0;
+    c.round = 0;
+    c.round_limit = 0x7fffffff;
+    c.n_active = s.n_req;
+    c.error = 0;
+    c.error_req = -1;
+    c.has_tT = c.has_tD = c.has_tpar = c.has_tord = 0;
+    c.tT = c.tD = c.tpar = c.tord = 0.0;
+    c.r_star = 0.0;
+  }
+  if (b >= s.n_req) return;
+  const int row = bt.q_off[b] + bt.n_new[b] - 1;
+  s.committed[(size_t)b * s.out_len] = (uint64_t)bt.out_tok[row];
+  s.pos[b] = 1;
+  s.done[b] = s.out_len <= 1;
+  s.synced[b] = 0;
+  s.cached_len[b] = 0;
+  s.in_rollback[b] = 1;
+  s.hist_len[b] = 0;
+  s.kvd[b] = 0;
+  s.gen_count[b] = 0;
+  s.vkind[b] = 0;
+}
+
+// ------------------------------------------------------------ round begin
+// Controller (sim.py:447-467) + conditional-node selection.
+__global__ void k_round_begin(DecodeStateDev s) {
+  if (threadIdx.x != 0) return;
+  CtrlDev& c = *s.ctrl;
+  c.t_round_begin = globaltimer();
+  c.t_draft_begin = c.t_draft_end = 0;
+  c.draft_steps = 0;
+  int mode = 0;
+  if (c.n_active > 0 && c.error == 0 && c.round < s.max_rounds && c.round < c.round_limit) {
+    if (s.variant == SPECTRE_VARIANT_AR) mode = 'F';
+    else if (s.variant == SPECTRE_VARIANT_ORDINARY) mode = 'O';
+    else if (s.variant == SPECTRE_VARIANT_PARALLEL) mode = 'P';
+    else {
+      const bool hasL = s.has_fixed_l ? true : (c.has_L != 0);
+      const double L = s.has_fixed_l ? s.fixed_l : c.L;
+      double r_star;
+      if (s.controller == SPECTRE_CTRL_REFERENCE || !(c.has_tT && c.has_tD)) {
+        if (s.controller == SPECTRE_CTRL_ROUND) {
+          // explore: measure one round of each mode before trusting the model
+          if (!c.has_tord) { mode = 'O'; }
+          else if (!c.has_tpar) { mode = 'P'; }
+        }
+        if (mode == 0)
+          mode = choose_mode_hybrid(c.prev_mode, c.has_ema != 0, c.ema, hasL, L, s.gamma,
+                                    s.t_target, s.t_draft, &r_star);
+        else
+          r_star = 0.0;
+      } else if (s.controller == SPECTRE_CTRL_MEASURED) {
+        mode = choose_mode_hybrid(c.prev_mode, c.has_ema != 0, c.ema, hasL, L, s.gamma, c.tT,
+                                  c.tD, &r_star);
+      } else {  // SPECTRE_CTRL_ROUND: r* = L (1 - T_par / T_ord) / (L - 1)
+        if (!c.has_tord) {
+          mode = 'O';
+          r_star = 0.0;
+        } else if (!c.has_tpar) {
+          mode = 'P';
+          r_star = 0.0;
+        } else {
+          const double r_hat = c.has_ema ? c.ema : 0.0;
+          if (!hasL || L <= 1.0 + 1e-9) {
+            r_star = __longlong_as_double(0x7ff0000000000000ll);
+          } else {
+            r_star = __ddiv_rn(__dmul_rn(L, __dsub_rn(1.0, __ddiv_rn(c.tpar, c.tord))),
+                               __dsub_rn(L, 1.0));
+          }
+          if (c.prev_mode == 'P')
+            mode = (r_hat > __dmul_rn(r_star, kExitParallelMargin)) ? 'O' : 'P';
+          else
+            mode = (r_hat <= r_star) ? 'P' : 'O';
+        }
+      }
+      c.r_star = r_star;
+      c.prev_mode = mode;
+    }
+  }
+  c.mode = mode;
+  if (s.use_handles) {
+    cudaGraphSetConditional(s.h_ord, mode == 'O' ? 1u : 0u);
+    cudaGraphSetConditional(s.h_par, mode == 'P' ? 1u : 0u);
+  }
+}
+
+// ------------------------------------------------------------ draft phase
+// which_mode: 'O' (repair gamma-1 tokens anchored at committed_pos) or 'P'
+// (speculate gamma tokens from the history tail).  Sync + rebase + catch-up
+// batch for the draft's first step (draft_engine.py:246-280, 412-431).
+__global__ void __launch_bounds__(kProtoThreads) k_draft_prep(DecodeStateDev s, BatchDev bt,
+                                                              int which_mode) {
+  __shared__ int sh[kProtoThreads];
+  CtrlDev& c = *s.ctrl;
+  const int mode = c.mode;
+  if (mode != which_mode) {  // phase not selected this round: empty batch
+    if (threadIdx.x == 0) *bt.t_dev = 0;
+    if (threadIdx.x < s.n_req) bt.n_new[threadIdx.x] = 0;
+    return;
+  }
+  if (threadIdx.x == 0) c.t_draft_begin = globaltimer();
+  const int b = threadIdx.x;
+  int n_new = 0, kvd = 0, hl = 0;
+  if (b < s.n_req) {
+    bt.rslot[b] = b;
+    s.gen_count[b] = 0;
+    const bool active = !s.done[b];
+    const bool queried = active && mode == which_mode &&
+                         (which_mode == 'P' || s.cached_len[b] == 0);
+    if (queried) {
+      uint64_t* h = s.hist + (size_t)b * s.hist_cap;
+      const uint64_t* com = s.committed + (size_t)b * s.out_len;
+      const int pos = s.pos[b];
+      const int start = s.synced[b];
+      int inv;
+      auto ref = [&](int32_t q) { return com[q]; };  // verified prefix (q < pos)
+      hl = session_on_sync(h, s.hist_len[b], start, pos - start,
+                           [&](int32_t k) { return com[start + k]; }, ref, &inv);
+      kvd = min(s.kvd[b], inv);
+      s.synced[b] = pos;
+      const int count = which_mode == 'O' ? s.gamma - 1 : s.gamma;
+      if (which_mode == 'O' || hl + count > s.hist_cap) {
+        // repair anchor (sim.py:550-555) / speculation-window cap
+        hl = session_rebase(h, hl, pos, ref, &inv);
+        kvd = min(kvd, inv);
+      }
+      kvd = min(kvd, hl - 1);
+      n_new = hl - kvd;
+      s.hist_len[b] = hl;
+      s.kvd[b] = kvd;
+      s.gen_count[b] = count;
+      s.gen_done[b] = 0;
+      s.gen_start[b] = hl;
+    }
+  }
+  int off = 0;
+  const int total = block_exclusive_scan(n_new, &off, b, s.n_req, sh);
+  if (b < s.n_req) {
+    bt.q_off[b] = off;
+    bt.n_new[b] = n_new;
+    bt.pos0[b] = s.prompt_len + kvd;
+    const uint64_t* h = s.hist + (size_t)b * s.hist_cap;
+    for (int j = 0; j < n_new; ++j) {
+      bt.tok[off + j] = (int)h[kvd + j];
+      bt.pos[off + j] = s.prompt_len + kvd + j;
+      bt.slot[off + j] = b;
+    }
+  }
+  if (threadIdx.x == 0) {
+    *bt.t_dev = total;
+    if (mode == which_mode) c.draft_steps = which_mode == 'O' ? s.gamma - 1 : s.gamma;
+  }
+}
+
+// After each draft forward: append the (noised) greedy token, next 1-token batch.
+__global__ void __launch_bounds__(kProtoThreads) k_draft_append(DecodeStateDev s, BatchDev bt,
+                                                                int which_mode, int last_step) {
+  __shared__ int sh[kProtoThreads];
+  CtrlDev& c = *s.ctrl;
+  if (c.mode != which_mode) {
+    if (threadIdx.x == 0) *bt.t_dev = 0;
+    if (threadIdx.x < s.n_req) bt.n_new[threadIdx.x] = 0;
+    return;
+  }
+  const int b = threadIdx.x;
+  int n_new = 0;
+  if (b < s.n_req && s.gen_count[b] > 0 && s.gen_done[b] < s.gen_count[b]) {
+    const int row = bt.q_off[b] + bt.n_new[b] - 1;
+    uint64_t* h = s.hist + (size_t)b * s.hist_cap;
+    const int hl = s.hist_len[b];
+    const int tok = noisy_draft_token(s, b, hl, bt.out_tok[row]);
+    h[hl] = (uint64_t)tok;
+    s.kvd[b] = hl;            // every fed token now has KV; the new one does not
+    s.hist_len[b] = hl + 1;
+    s.gen_done[b] += 1;
+    if (s.gen_done[b] < s.gen_count[b]) n_new = 1;
+  }
+  int off = 0;
+  const int total = block_exclusive_scan(n_new, &off, b, s.n_req, sh);
+  if (b < s.n_req) {
+    bt.q_off[b] = off;
+    bt.n_new[b] = n_new;
+    const int hl = s.hist_len[b];
+    bt.pos0[b] = s.prompt_len + hl - 1;
+    if (n_new) {
+      bt.tok[off] = (int)s.hist[(size_t)b * s.hist_cap + hl - 1];
+      bt.pos[off] = s.prompt_len + hl - 1;
+      bt.slot[off] = b;
+    }
+  }
+  if (threadIdx.x == 0) {
+    *bt.t_dev = total;
+    if (last_step && c.mode == which_mode) c.t_draft_end = globaltimer();
+  }
+}
+
+// ------------------------------------------------------------ target phase
+// Candidate assembly (target_engine.py:132-221) -> verify batch rows
+// [pending bonus @ pos-1, candidate tokens @ pos ...].
+__global__ void __launch_bounds__(kProtoThreads) k_verify_prep(DecodeStateDev s, BatchDev bt) {
+  __shared__ int sh[kProtoThreads];
+  CtrlDev& c = *s.ctrl;
+  const int mode = c.mode;
+  if (threadIdx.x == 0) c.t_verify_begin = globaltimer();
+  const int b = threadIdx.x;
+  int n_new = 0;
+  int kind = 0, m = 0;
+  if (b < s.n_req && mode != 0 && !s.done[b]) {
+    const int pos = s.pos[b];
+    uint64_t* cand = s.cand_tok + (size_t)b * (s.gamma + 1);
+    if (mode == 'F') {
+      kind = kFallback;
+    } else if (s.cached_len[b] > 0 && !s.in_rollback[b]) {
+      if (s.cached_start[b] != pos) {
+        s.ctrl->error = 7;
+        s.ctrl->error_req = b;
+      }
+      kind = kCached;
+      m = s.cached_len[b];
+      const uint64_t* ct = s.cached_tok + (size_t)b * (s.gamma + 1);
+      for (int j = 0; j < m; ++j) cand[j] = ct[j];
+    } else if (mode == 'O') {
+      kind = kRepaired;
+      m = s.gamma - 1;
+      if (s.gen_start[b] != pos || s.gen_done[b] != m) {
+        s.ctrl->error = 7;
+        s.ctrl->error_req = b;
+      }
+      const uint64_t* h = s.hist + (size_t)b * s.hist_cap;
+      for (int j = 0; j < m; ++j) cand[j] = h[pos + j];
+    } else {
+      kind = kPadded;
+    }
+    n_new = 1 + m;
+  }
+  if (b < s.n_req) {
+    s.vkind[b] = kind;
+    s.vcand_n[b] = m;
+  }
+  int off = 0;
+  const int total = block_exclusive_scan(n_new, &off, b, s.n_req, sh);
+  if (b < s.n_req) {
+    const int pos = s.pos[b];
+    bt.q_off[b] = off;
+    bt.n_new[b] = n_new;
+    bt.pos0[b] = s.prompt_len + pos - 1;
+    bt.rslot[b] = b;
+    if (n_new) {
+      const uint64_t* com = s.committed + (size_t)b * s.out_len;
+      const uint64_t* cand = s.cand_tok + (size_t)b * (s.gamma + 1);
+      bt.tok[off] = (int)com[pos - 1];
+      bt.pos[off] = s.prompt_len + pos - 1;
+      bt.slot[off] = b;
+      for (int j = 0; j < m; ++j) {
+        bt.tok[off + 1 + j] = (int)cand[j];
+        bt.pos[off + 1 + j] = s.prompt_len + pos + j;
+        bt.slot[off + 1 + j] = b;
+      }
+    }
+  }
+  if (threadIdx.x == 0) *bt.t_dev = total;
+}
+
+// Fused accept: greedy exact-prefix verification (oracle.py:90-113 with the
+// target argmax as the reference stream), bonus emission, commit
+// (target_engine.py:227-249), rollback set (:285-302), suffix reuse
+// (:252-279), r-hat / L EMAs (sim.py:673-678, target_engine.py:396-402),
+// trace row, and the decode-loop condition.  KV rollback is implicit: the
+// target's valid KV length is prompt_len + committed_pos - 1 and the draft's
+// is tracked in kvd, so rejected rows are simply overwritten next time.
+__global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, BatchDev bt) {
+  __shared__ long long s_tv;
+  CtrlDev& c = *s.ctrl;
+  const int mode = c.mode;
+  if (threadIdx.x == 0) s_tv = globaltimer();
+  __syncthreads();
+  if (mode == 0) {
+    if (threadIdx.x == 0 && s.use_handles) cudaGraphSetConditional(s.h_loop, 0u);
+    return;
+  }
+  const int b = threadIdx.x;
+  const int G = s.gamma + 1;
+  if (b < s.n_req && s.vkind[b] != 0) {
+    const int kind = s.vkind[b];
+    const int m = s.vcand_n[b];
+    const int row0 = bt.q_off[b];
+    const uint64_t* cand = s.cand_tok + (size_t)b * G;
+    uint64_t* com = s.committed + (size_t)b * s.out_len;
+    int pos = s.pos[b];
+    int a = 0;
+    while (a < m && cand[a] == (uint64_t)bt.out_tok[row0 + a]) ++a;
+    const uint64_t bonus = (uint64_t)bt.out_tok[row0 + a];
+    const int accepted_count = a + (kind == kCached ? 0 : 1);
+    const int real = kind == kRepaired ? s.gamma : (kind == kCached ? m : 1);
+    // this round's prepared segment (parallel mode): the draft's speculation
+    const bool prep = (mode == 'P') && s.gen_count[b] > 0;
+    const uint64_t* h = s.hist + (size_t)b * s.hist_cap;
+    const int pstart = s.gen_start[b];
+    const int plen = prep ? s.gen_done[b] : 0;
+    int rolled = accepted_count < real;
+    if (!rolled && plen > 0 && h[pstart] != bonus) rolled = 1;
+    const int end = min(pos + a + 1, s.out_len);
+    for (int q = pos; q < end; ++q) com[q] = (q - pos < a) ? cand[q - pos] : bonus;
+    const int delta = end - pos;
+    pos = end;
+    const int done = pos >= s.out_len;
+    s.pos[b] = pos;
+    s.done[b] = done;
+    int cst = 0;
+    const int cl = reuse_or_discard(h + pstart, plen, pstart, com, pos, done,
+                                    s.cached_tok + (size_t)b * G, &cst);
+    s.cached_len[b] = cl;
+    s.cached_start[b] = cst;
+    s.in_rollback[b] = cl == 0;
+    s.delta[b] = delta;
+    s.rolled[b] = rolled;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const long long t_now = globaltimer();
+    int P = 0, dsum = 0, nroll = 0, csum = 0, cn = 0, npad = 0;
+    for (int r = 0; r < s.n_req; ++r) {
+      const int k = s.vkind[r];
+      if (k == 0) continue;
+      ++P;
+      dsum += s.delta[r];
+      nroll += s.rolled[r];
+      if (k == kPadded) ++npad;
+      if (k == kCached || k == kRepaired) {
+        csum += s.delta[r];
+        ++cn;
+        const double dv = (double)s.delta[r];
+        if (!c.has_L) {
+          c.L = dv;
+          c.has_L = 1;
+        } else {
+          c.L = ema_step(s.ema_decay, c.L, dv);
+        }
+      }
+      if (s.done[r]) --c.n_active;
+      s.vkind[r] = 0;
+    }
+    const int num = s.r_kind == 1 ? npad : nroll;
+    const double r_hat = __ddiv_rn((double)num, (double)(P > 0 ? P : 1));
+    if (mode != 'F') {
+      if (!c.has_ema) {
+        c.ema = r_hat;
+        c.has_ema = 1;
+      } else {
+        c.ema = ema_step(s.ema_decay, c.ema, r_hat);
+      }
+    }
+    const double tv = (double)(s_tv - c.t_verify_begin) * 1e-9;
+    const double tr = (double)(t_now - c.t_round_begin) * 1e-9;
+    const double d = s.ema_decay;
+    if (!c.has_tT) { c.tT = tv; c.has_tT = 1; } else { c.tT = ema_step(d, c.tT, tv); }
+    if (c.t_draft_end > 0 && c.draft_steps > 0) {
+      const double td = (double)(c.t_draft_end - c.t_draft_begin) * 1e-9 / c.draft_steps;
+      if (!c.has_tD) { c.tD = td; c.has_tD = 1; } else { c.tD = ema_step(d, c.tD, td); }
+    }
+    // per-committed-token cost of each mode, normalised to the round shape
+    if (mode == 'P') {
+      if (!c.has_tpar) { c.tpar = tr; c.has_tpar = 1; } else { c.tpar = ema_step(d, c.tpar, tr); }
+    } else if (mode == 'O') {
+      if (!c.has_tord) { c.tord = tr; c.has_tord = 1; } else { c.tord = ema_step(d, c.tord, tr); }
+    }
+    const int ri = c.round;
+    if (ri < s.max_rounds) {
+      s.trace.mode[ri] = mode;
+      s.trace.participants[ri] = P;
+      s.trace.delta[ri] = dsum;
+      s.trace.n_roll[ri] = nroll;
+      s.trace.content_sum[ri] = csum;
+      s.trace.content_n[ri] = cn;
+      s.trace.n_padded[ri] = npad;
+      s.trace.t_round_ns[ri] = t_now - c.t_round_begin;
+      s.trace.t_verify_ns[ri] = s_tv - c.t_verify_begin;
+      s.trace.t_draft_ns[ri] = c.t_draft_end > 0 ? c.t_draft_end - c.t_draft_begin : 0;
+      s.trace.r_hat_ema[ri] = c.ema;
+      s.trace.accepted_len_ema[ri] = c.has_L ? c.L : 0.0;
+      s.trace.r_star[ri] = c.r_star;
+    }
+    c.round = ri + 1;
+    if (s.use_handles)
+      cudaGraphSetConditional(s.h_loop, (c.n_active > 0 && c.error == 0 &&
+                                         c.round < s.max_rounds && c.round < c.round_limit)
+                                            ? 1u
+                                            : 0u);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+int launch_prefill_batch(const int* prompts, int prompt_len, int n_req, int c0, int cs,
+                         const BatchDev& bt, cudaStream_t s) {
+  k_prefill_batch<<<(n_req + 255) / 256, 256, 0, s>>>(prompts, prompt_len, n_req, c0, cs, bt);
+  SPECTRE_LAUNCH_CHECK("k_prefill_batch");
+  return SPECTRE_OK;
+}
+int launch_admit(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s) {
+  k_admit<<<(st.n_req + 255) / 256, 256, 0, s>>>(st, bt);
+  SPECTRE_LAUNCH_CHECK("k_admit");
+  return SPECTRE_OK;
+}
+int launch_round_begin(const DecodeStateDev& st, cudaStream_t s) {
+  k_round_begin<<<1, 32, 0, s>>>(st);
+  SPECTRE_LAUNCH_CHECK("k_round_begin");
+  return SPECTRE_OK;
+}
+int launch_draft_prep(const DecodeStateDev& st, const BatchDev& bt, int which, cudaStream_t s) {
+  k_draft_prep<<<1, kProtoThreads, 0, s>>>(st, bt, which);
+  SPECTRE_LAUNCH_CHECK("k_draft_prep");
+  return SPECTRE_OK;
+}
+int launch_draft_append(const DecodeStateDev& st, const BatchDev& bt, int which, int last,
+                        cudaStream_t s) {
+  k_draft_append<<<1, kProtoThreads, 0, s>>>(st, bt, which, last);
+  SPECTRE_LAUNCH_CHECK("k_draft_append");
+  return SPECTRE_OK;
+}
+int launch_verify_prep(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s) {
+  k_verify_prep<<<1, kProtoThreads, 0, s>>>(st, bt);
+  SPECTRE_LAUNCH_CHECK("k_verify_prep");
+  return SPECTRE_OK;
+}
+int launch_accept(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s) {
+  k_accept<<<1, kProtoThreads, 0, s>>>(st, bt);
+  SPECTRE_LAUNCH_CHECK("k_accept");
+  return SPECTRE_OK;
+}
+
+}  // namespace spectre

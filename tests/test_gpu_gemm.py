@@ -53,7 +53,8 @@ def _ref(torch, X, W, T):
 @pytest.mark.parametrize("T,rows_cap,N,K,splits", [
     (1, 64, 256, 64, 1), (16, 64, 384, 512, 1), (64, 64, 1024, 2048, 2),
     (37, 64, 640, 1024, 3), (256, 256, 6144, 4096, 3), (200, 256, 512, 4096, 4),
-    (320, 320, 1024, 4096, 4), (512, 512, 256, 256, 1), (130, 192, 768, 1024, 1)])
+    (320, 320, 1024, 4096, 4), (512, 512, 256, 256, 1), (130, 192, 768, 1024, 1),
+    (700, 768, 384, 512, 2), (1280, 1280, 256, 1024, 1)])
 def test_partial_matches_fp32(env, T, rows_cap, N, K, splits):
     torch = env[0]
     g = torch.Generator(device="cuda").manual_seed(T * 7 + N)
@@ -110,6 +111,24 @@ def test_argmax_epilogue(env):
     # the reported max equals the fp32 logit at the chosen index (within tolerance)
     got_max = av[:, :T].max(0).values
     assert torch.allclose(got_max, logits.gather(1, idx[:, None]).squeeze(1), atol=2e-3, rtol=1e-3)
+
+
+def test_multipass_argmax_and_swiglu(env):
+    torch = env[0]
+    X = torch.randn(1024, 512, device="cuda").bfloat16()
+    W = (torch.randn(1024, 512, device="cuda") * 0.05).bfloat16()
+    T = 900
+    _, av, ai, _ = _run(env, X, W, T, 1024, 1, ARGMAX)
+    best = av[:, :T].argmax(0)
+    idx = ai[:, :T].gather(0, best[None]).squeeze(0).long()
+    logits = _ref(torch, X, W, T)
+    top2 = logits.topk(2, dim=1).values
+    clear = (top2[:, 0] - top2[:, 1]) > 1e-2
+    assert torch.equal(idx[clear], logits.argmax(1)[clear])
+    _, _, _, act = _run(env, X, W, T, 1024, 1, SWIGLU)
+    g = _ref(torch, X, W.view(8, 2, 64, 512)[:, 0].reshape(512, 512), T)
+    u = _ref(torch, X, W.view(8, 2, 64, 512)[:, 1].reshape(512, 512), T)
+    assert torch.allclose(act[:T].float(), torch.nn.functional.silu(g) * u, atol=3e-2, rtol=2e-2)
 
 
 def test_swiglu_epilogue(env):

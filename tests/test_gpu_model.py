@@ -1,0 +1,137 @@
+"""Model-mode parity on the B200.
+
+* forward numerics vs the fp32 PyTorch restatement (oracle/model_ref.py):
+  final hidden state within bf16 tolerance; greedy tokens identical wherever
+  the reference's top-2 logit margin exceeds 0.05 (tolerance stated here)
+* batch invariance: a request's outputs are bit-identical whatever else
+  shares the batch (what makes speculative decoding lossless here)
+* losslessness end to end: ordinary / parallel / hybrid (SPECTRE) commit
+  exactly the autoregressive greedy stream, for several draft-noise levels
+"""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+MARGIN = 0.05       # logit margin above which argmax must agree with fp32
+X_RTOL = 3e-2       # final hidden state: |dx| <= X_RTOL * rms(x) (bf16 storage)
+
+
+@pytest.fixture(scope="module")
+def M():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2605_08151_b200 import model
+    return model
+
+
+def _forward_chunks(eng, which, prompts, chunk):
+    import torch
+    n, P = prompts.shape
+    outs, xs = [], []
+    for c0 in range(0, P, chunk):
+        cs = min(chunk, P - c0)
+        tok = prompts[:, c0:c0 + cs].reshape(-1)
+        pos = torch.arange(c0, c0 + cs, device="cuda").repeat(n)
+        slot = torch.arange(n, device="cuda").repeat_interleave(cs)
+        q_off = torch.arange(n, device="cuda") * cs
+        n_new = torch.full((n,), cs, device="cuda")
+        pos0 = torch.full((n,), c0, device="cuda")
+        o, x = eng.forward(which, tok, pos, slot, q_off, n_new, pos0, want_x=True)
+        outs.append(o.view(n, cs))
+        xs.append(x.view(n, cs, -1))
+    return torch.cat(outs, 1), torch.cat(xs, 1)
+
+
+@pytest.mark.parametrize("shapes", ["tiny", "small"])
+def test_forward_vs_fp32_reference(M, shapes):
+    import torch
+    from oracle.model_ref import reference_forward
+    tgt, drf = (M.TINY_TARGET, M.TINY_DRAFT) if shapes == "tiny" else (M.SMALL_TARGET,
+                                                                        M.SMALL_DRAFT)
+    n, P = 4, 40
+    pair = M.build_pair(tgt, drf, n_req=n, ctx_cap=256, seed=3, target_branch=1.0,
+                        draft_branch=1.0)
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=64, prompt_len=P, seed=3)
+    eng = M.SpectreEngine(pair, spec, "hybrid")
+    prompts = M.synthetic_prompts(n, P, tgt.vocab, seed=3)
+    for which, w in ((0, pair.target), (1, pair.draft)):
+        toks, xs = _forward_chunks(eng, which, prompts, 8)
+        for r in range(n):
+            x_ref, logits = reference_forward(w, prompts[r])
+            dx = (xs[r].float() - x_ref).abs()
+            assert dx.max().item() <= X_RTOL * x_ref.pow(2).mean().sqrt().item() * 8
+            assert dx.mean().item() <= X_RTOL * x_ref.abs().mean().item()
+            top2 = logits.topk(2, -1).values
+            clear = (top2[:, 0] - top2[:, 1]) > MARGIN
+            assert torch.equal(toks[r][clear].long(), logits.argmax(-1)[clear])
+            assert clear.float().mean().item() > 0.5
+
+
+def test_forward_batch_invariance(M):
+    import torch
+    n, P = 6, 24
+    pair = M.build_pair(M.SMALL_TARGET, M.SMALL_DRAFT, n_req=n, ctx_cap=256, seed=5)
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=64, prompt_len=P, seed=5)
+    eng = M.SpectreEngine(pair, spec, "ar")
+    prompts = M.synthetic_prompts(n, P, M.SMALL_TARGET.vocab, seed=5)
+    full_tok, full_x = _forward_chunks(eng, 0, prompts, 8)
+    # same requests, one token at a time (autoregressive shape), fresh KV
+    toks, xs = _forward_chunks(eng, 0, prompts, 1)
+    assert torch.equal(toks, full_tok)
+    assert torch.equal(xs, full_x)
+    # ragged: only request 2 participates, chunk of 3
+    tok2, x2 = [], []
+    for c0 in range(0, P, 3):
+        cs = min(3, P - c0)
+        tok = prompts[2, c0:c0 + cs]
+        z = torch.zeros(n, dtype=torch.int32, device="cuda")
+        n_new = z.clone()
+        n_new[2] = cs
+        pos0 = z.clone()
+        pos0[2] = c0
+        o, x = eng.forward(0, tok, torch.arange(c0, c0 + cs, device="cuda"),
+                           torch.full((cs,), 2, device="cuda"), z, n_new, pos0, want_x=True)
+        tok2.append(o)
+        x2.append(x)
+    assert torch.equal(torch.cat(tok2), full_tok[2])
+    assert torch.equal(torch.cat(x2), full_x[2])
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.7])
+@pytest.mark.parametrize("shapes", ["tiny", "small"])
+def test_speculative_decoding_is_lossless(M, shapes, alpha):
+    import torch
+    tgt, drf = (M.TINY_TARGET, M.TINY_DRAFT) if shapes == "tiny" else (M.SMALL_TARGET,
+                                                                        M.SMALL_DRAFT)
+    n = 8
+    pair = M.build_pair(tgt, drf, n_req=n, ctx_cap=256, seed=7)
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=96, prompt_len=32, alpha=alpha, seed=7)
+    ar = M.decode(pair, spec, "ar")
+    assert (ar.committed_pos == spec.output_len).all()
+    for v in ("ordinary", "parallel", "hybrid"):
+        for use_graph in (False, True):
+            got = M.decode(pair, spec, v, use_graph=use_graph)
+            assert (got.committed_pos == spec.output_len).all()
+            assert torch.equal(got.committed, ar.committed), (v, use_graph)
+            assert got.report.total_committed == n * spec.output_len
+
+
+def test_device_graph_is_used(M):
+    n = 4
+    pair = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=n, ctx_cap=256, seed=2)
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=64, prompt_len=16, seed=2)
+    res = M.decode(pair, spec, "hybrid", use_graph=True)
+    assert res.graph == 1, "conditional WHILE/IF round graph was not used"
+
+
+def test_draft_noise_controls_acceptance(M):
+    n = 16
+    pair = M.build_pair(M.SMALL_TARGET, M.SMALL_DRAFT, n_req=n, ctx_cap=512, seed=9)
+    Ls = []
+    for alpha in (1.0, 0.6, 0.2):
+        spec = M.DecodeSpec(n_req=n, gamma=4, output_len=200, prompt_len=32, alpha=alpha, seed=9)
+        res = M.decode(pair, spec, "ordinary")
+        Ls.append(res.report.content_mean_accepted_length)
+    assert Ls[0] > Ls[1] > Ls[2] >= 1.0
