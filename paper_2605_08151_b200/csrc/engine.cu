@@ -203,8 +203,8 @@ struct Engine {
   DecodeStateDev st{};
   int prefill_cs = 1;
   int draft_new_max = 1;
-  cudaStream_t s_draft = nullptr, s_cap = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t s_draft = nullptr, s_cap = nullptr, s_main = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t exec_loop = nullptr;
   cudaGraph_t graph_loop = nullptr;
   int graph_failed = 0;
@@ -216,6 +216,9 @@ struct Engine {
     if (graph_loop) cudaGraphDestroy(graph_loop);
     if (s_draft) cudaStreamDestroy(s_draft);
     if (s_cap) cudaStreamDestroy(s_cap);
+    if (s_main) cudaStreamDestroy(s_main);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (mode_host) cudaFreeHost(mode_host);
@@ -377,56 +380,69 @@ struct Engine {
   }
 
   int build_loop_graph(cudaStream_t s) {
-    cudaGraph_t g;
-    SPECTRE_CUDA_TRY(cudaGraphCreate(&g, 0));
-    cudaGraphConditionalHandle h_loop, h_ord, h_par;
-    SPECTRE_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault));
-    SPECTRE_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_ord, g, 0, cudaGraphCondAssignDefault));
-    SPECTRE_CUDA_TRY(cudaGraphConditionalHandleCreate(&h_par, g, 0, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams wp{};
-    wp.type = cudaGraphNodeTypeConditional;
-    wp.conditional.handle = h_loop;
-    wp.conditional.type = cudaGraphCondTypeWhile;
-    wp.conditional.size = 1;
-    cudaGraphNode_t wnode;
-    SPECTRE_CUDA_TRY(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
-    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    cudaGraph_t g = nullptr;
     DecodeStateDev saved = st;
-    st.h_loop = h_loop;
-    st.h_ord = h_ord;
-    st.h_par = h_par;
-    st.use_handles = 1;
     int r = SPECTRE_OK;
-    SPECTRE_CUDA_TRY(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
-                                                   cudaStreamCaptureModeRelaxed));
+    bool capturing = false;
+    auto fail = [&](cudaError_t e, const char* what) {
+      if (!r) r = cuda_fail(e, what);
+    };
     do {
+      cudaError_t e = cudaGraphCreate(&g, 0);
+      if (e != cudaSuccess) { fail(e, "cudaGraphCreate"); break; }
+      cudaGraphConditionalHandle h_loop, h_ord, h_par;
+      if ((e = cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault)) ||
+          (e = cudaGraphConditionalHandleCreate(&h_ord, g, 0, cudaGraphCondAssignDefault)) ||
+          (e = cudaGraphConditionalHandleCreate(&h_par, g, 0, cudaGraphCondAssignDefault))) {
+        fail(e, "cudaGraphConditionalHandleCreate");
+        break;
+      }
+      cudaGraphNodeParams wp{};
+      wp.type = cudaGraphNodeTypeConditional;
+      wp.conditional.handle = h_loop;
+      wp.conditional.type = cudaGraphCondTypeWhile;
+      wp.conditional.size = 1;
+      cudaGraphNode_t wnode;
+      if ((e = cudaGraphAddNode(&wnode, g, nullptr, 0, &wp))) { fail(e, "cudaGraphAddNode(while)"); break; }
+      cudaGraph_t body = wp.conditional.phGraph_out[0];
+      st.h_loop = h_loop;
+      st.h_ord = h_ord;
+      st.h_par = h_par;
+      st.use_handles = 1;
+      if ((e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeRelaxed))) {
+        fail(e, "cudaStreamBeginCaptureToGraph");
+        break;
+      }
+      capturing = true;
       if ((r = launch_round_begin(st, s))) break;
       cudaGraphNode_t n_ord, n_par;
       if ((r = add_if_node(s, h_ord, [&](cudaStream_t cs) { return draft_phase('O', cs); }, true,
                            &n_ord)))
         break;
-      // parallel branch hangs off the same point; the stream keeps going
+      // the parallel branch hangs off the same point; the stream keeps going
       if ((r = add_if_node(s, h_par, [&](cudaStream_t cs) { return draft_phase('P', cs); },
                            false, &n_par)))
         break;
       if ((r = verify_phase(s))) break;
-      cudaError_t e =
-          cudaStreamUpdateCaptureDependencies(s, &n_par, 1, cudaStreamAddCaptureDependencies);
-      if (e != cudaSuccess) {
-        r = cuda_fail(e, "cudaStreamUpdateCaptureDependencies");
+      if ((e = cudaStreamUpdateCaptureDependencies(s, &n_par, 1,
+                                                   cudaStreamAddCaptureDependencies))) {
+        fail(e, "cudaStreamUpdateCaptureDependencies");
         break;
       }
       if ((r = launch_accept(st, tgt.bt, s))) break;
     } while (0);
-    cudaGraph_t captured;
-    cudaError_t e = cudaStreamEndCapture(s, &captured);
-    if (!r && e != cudaSuccess) r = cuda_fail(e, "cudaStreamEndCapture(loop body)");
+    if (capturing) {
+      cudaGraph_t captured;
+      cudaError_t e = cudaStreamEndCapture(s, &captured);
+      if (e != cudaSuccess) fail(e, "cudaStreamEndCapture(loop body)");
+    }
     if (!r) {
-      e = cudaGraphInstantiate(&exec_loop, g, 0);
-      if (e != cudaSuccess) r = cuda_fail(e, "cudaGraphInstantiate(loop)");
+      cudaError_t e = cudaGraphInstantiate(&exec_loop, g, 0);
+      if (e != cudaSuccess) fail(e, "cudaGraphInstantiate(loop)");
     }
     if (r) {
-      cudaGraphDestroy(g);
+      if (g) cudaGraphDestroy(g);
       st = saved;
       exec_loop = nullptr;
       cudaGetLastError();
@@ -485,6 +501,9 @@ extern "C" void* spectre_engine_create(const SpectreModelDims* target,
   }
   if (e->tgt.plan() || e->drf.plan()) return nullptr;
   if (cudaStreamCreateWithFlags(&e->s_draft, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&e->s_main, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e->ev_out, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithFlags(&e->s_cap, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
@@ -527,13 +546,15 @@ extern "C" int spectre_engine_run(void* engine, int32_t max_rounds, int32_t use_
                                   int32_t* rounds_run, void* stream) {
   auto* e = reinterpret_cast<Engine*>(engine);
   if (!e || max_rounds < 0) return arg_fail("spectre_engine_run");
-  cudaStream_t s = as_stream(stream);
+  cudaStream_t caller = as_stream(stream);
+  cudaStream_t s = e->s_main;  // capturable stream, ordered after the caller's work
+  SPECTRE_CUDA_TRY(cudaEventRecord(e->ev_in, caller));
+  SPECTRE_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_in, 0));
   // round limit = rounds already done + max_rounds (device-side counter)
-  int done_before = 0;
   SPECTRE_CUDA_TRY(cudaMemcpyAsync(e->mode_host, &e->st.ctrl->round, sizeof(int),
                                    cudaMemcpyDeviceToHost, s));
   SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
-  done_before = *e->mode_host;
+  const int done_before = *e->mode_host;
   const int limit = (int)std::min<long long>((long long)done_before + max_rounds, 0x7fffffff);
   SPECTRE_CUDA_TRY(cudaMemcpyAsync(&e->st.ctrl->round_limit, &limit, sizeof(int),
                                    cudaMemcpyHostToDevice, s));
@@ -545,9 +566,7 @@ extern "C" int spectre_engine_run(void* engine, int32_t max_rounds, int32_t use_
         TRY(e->round_eager(s, &mode));
         e->warmed = 1;
       }
-      if (e->build_loop_graph(s)) {
-        e->graph_failed = 1;  // fall back to eager rounds (reason in spectre_last_error)
-      }
+      if (e->build_loop_graph(s)) e->graph_failed = 1;  // eager fallback, see last_error
     }
     if (e->exec_loop) SPECTRE_CUDA_TRY(cudaGraphLaunch(e->exec_loop, s));
   }
@@ -558,6 +577,8 @@ extern "C" int spectre_engine_run(void* engine, int32_t max_rounds, int32_t use_
       if (mode == 0) break;
     }
   }
+  SPECTRE_CUDA_TRY(cudaEventRecord(e->ev_out, s));
+  SPECTRE_CUDA_TRY(cudaStreamWaitEvent(caller, e->ev_out, 0));
   if (rounds_run) {
     SPECTRE_CUDA_TRY(cudaMemcpyAsync(e->mode_host, &e->st.ctrl->round, sizeof(int),
                                      cudaMemcpyDeviceToHost, s));

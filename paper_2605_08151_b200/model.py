@@ -368,7 +368,11 @@ def decode(pair: ModelPair, spec: DecodeSpec, variant, prompts=None, use_graph=T
     rep = report_from_trace(variant, spec.seed, trace, total, dev_s)
     rep = MetricsReport(**{**rep.__dict__, "requests_completed":
                            int((pos >= spec.output_len).sum().item())})
-    return ModelRunResult(rep, variant, committed, pos, trace, rounds, dev_s, eng.graph_status())
+    status = eng.graph_status()
+    extra = {}
+    if status == 2:
+        extra["graph_error"] = _native.lib().spectre_last_error().decode(errors="replace")
+    return ModelRunResult(rep, variant, committed, pos, trace, rounds, dev_s, status, extra)
 
 
 def smoke() -> None:

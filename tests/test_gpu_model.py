@@ -123,7 +123,7 @@ def test_device_graph_is_used(M):
     pair = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=n, ctx_cap=256, seed=2)
     spec = M.DecodeSpec(n_req=n, gamma=4, output_len=64, prompt_len=16, seed=2)
     res = M.decode(pair, spec, "hybrid", use_graph=True)
-    assert res.graph == 1, "conditional WHILE/IF round graph was not used"
+    assert res.graph == 1, f"conditional WHILE/IF round graph was not used: {res.extra}"
 
 
 def test_draft_noise_controls_acceptance(M):
