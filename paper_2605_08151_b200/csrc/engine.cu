@@ -57,7 +57,7 @@ struct Bump {
 static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 static int pick_splits(int n_tiles, int k_iters) {
-  int s = 148 / n_tiles;
+  int s = 148 / n_tiles;  // one wave of CTAs (1 CTA per SM: 512 TMEM columns)
   if (s < 1) s = 1;
   while (s > 1 && k_iters / s < 3) --s;
   return s;
@@ -84,9 +84,9 @@ struct ModelRT {
   void layout(Bump& b) {
     const int d = dm.d_model, R = rows_cap;
     const int qd = dm.n_q_heads * dm.head_dim;
-    sp_qkv = pick_splits((nqkv() + 127) / 128, d / 64);
-    sp_o = pick_splits((d + 127) / 128, qd / 64);
-    sp_d = pick_splits((d + 127) / 128, dm.ffn / 64);
+    sp_qkv = pick_splits((nqkv() + 255) / 256, d / 64);
+    sp_o = pick_splits((d + 255) / 256, qd / 64);
+    sp_d = pick_splits((d + 255) / 256, dm.ffn / 64);
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
     split_max = (ctx_cap + kAttnChunk - 1) / kAttnChunk;
     rb_cap = (max_new * group() + 31) / 32;
@@ -99,9 +99,9 @@ struct ModelRT {
     const size_t att_rows = (size_t)n_req * dm.n_kv_heads * rb_cap * split_max * 32;
     att_o = b.take<float>(att_rows * dm.head_dim);
     att_ml = b.take<float>(att_rows * 2);
-    const int n_tiles = (dm.vocab + 127) / 128;
-    amax_v = b.take<float>((size_t)n_tiles * R);
-    amax_i = b.take<int>((size_t)n_tiles * R);
+    const int n_blocks = (dm.vocab + 31) / 32;
+    amax_v = b.take<float>((size_t)n_blocks * R);
+    amax_i = b.take<int>((size_t)n_blocks * R);
     rope = b.take<float2>((size_t)ctx_cap * dm.head_dim / 2);
     bt.tok = b.take<int>(R);
     bt.pos = b.take<int>(R);
@@ -187,7 +187,7 @@ struct ModelRT {
                                   s));
     }
     TRY(gemm_run(plm, s));
-    TRY(launch_argmax_reduce(amax_v, amax_i, plm.n_tiles, rows_cap, bt.t_dev, rows_cap,
+    TRY(launch_argmax_reduce(amax_v, amax_i, plm.n_amax_blocks, rows_cap, bt.t_dev, rows_cap,
                              bt.out_tok, nullptr, s));
     if (out_x)
       SPECTRE_CUDA_TRY(cudaMemcpyAsync(out_x, x, (size_t)rows_cap * d * 2,
@@ -550,14 +550,7 @@ extern "C" int spectre_engine_run(void* engine, int32_t max_rounds, int32_t use_
   cudaStream_t s = e->s_main;  // capturable stream, ordered after the caller's work
   SPECTRE_CUDA_TRY(cudaEventRecord(e->ev_in, caller));
   SPECTRE_CUDA_TRY(cudaStreamWaitEvent(s, e->ev_in, 0));
-  // round limit = rounds already done + max_rounds (device-side counter)
-  SPECTRE_CUDA_TRY(cudaMemcpyAsync(e->mode_host, &e->st.ctrl->round, sizeof(int),
-                                   cudaMemcpyDeviceToHost, s));
-  SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
-  const int done_before = *e->mode_host;
-  const int limit = (int)std::min<long long>((long long)done_before + max_rounds, 0x7fffffff);
-  SPECTRE_CUDA_TRY(cudaMemcpyAsync(&e->st.ctrl->round_limit, &limit, sizeof(int),
-                                   cudaMemcpyHostToDevice, s));
+  TRY(launch_set_round_limit(e->st, max_rounds, s));  // device-side budget, no host sync
   if (use_graph && !e->graph_failed) {
     if (!e->exec_loop) {
       if (!e->warmed) {
@@ -580,10 +573,10 @@ extern "C" int spectre_engine_run(void* engine, int32_t max_rounds, int32_t use_
   SPECTRE_CUDA_TRY(cudaEventRecord(e->ev_out, s));
   SPECTRE_CUDA_TRY(cudaStreamWaitEvent(caller, e->ev_out, 0));
   if (rounds_run) {
-    SPECTRE_CUDA_TRY(cudaMemcpyAsync(e->mode_host, &e->st.ctrl->round, sizeof(int),
-                                     cudaMemcpyDeviceToHost, s));
+    CtrlDev c;
+    SPECTRE_CUDA_TRY(cudaMemcpyAsync(&c, e->st.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
     SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
-    *rounds_run = *e->mode_host - done_before;
+    *rounds_run = c.round - c.round_base;
   }
   return SPECTRE_OK;
 }

@@ -28,7 +28,8 @@ struct CtrlDev {
   double ema;        // r-hat EMA (sim.py:673-678)
   double L;          // accepted-length EMA (target_engine.py:386-407)
   int round;         // rounds completed
-  int round_limit;   // stop after this many rounds (host-set per run call)
+  int round_limit;   // stop after this many rounds (set per run call)
+  int round_base;    // rounds completed when the current run call started
   int n_active;
   int error;         // protocol violation code (0 = none)
   int error_req;
@@ -92,6 +93,7 @@ int launch_prefill_batch(const int* prompts, int prompt_len, int n_req, int c0, 
                          const BatchDev& bt, cudaStream_t s);
 int launch_admit(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);
 int launch_round_begin(const DecodeStateDev& st, cudaStream_t s);
+int launch_set_round_limit(const DecodeStateDev& st, int extra, cudaStream_t s);
 int launch_draft_prep(const DecodeStateDev& st, const BatchDev& bt, int which, cudaStream_t s);
 int launch_draft_append(const DecodeStateDev& st, const BatchDev& bt, int which, int last,
                         cudaStream_t s);

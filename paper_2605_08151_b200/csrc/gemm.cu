@@ -49,71 +49,47 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t out
   return SPECTRE_OK;
 }
 
-static size_t gemm_smem_bytes(int stages, int rows_cap) {
-  return 1024 + (size_t)stages * (16384 + (size_t)rows_cap * 128) + 1024 + 8192;
-}
-
-template <int kEpi, uint32_t kCols>
+template <int kEpi>
 static int launch_one(const GemmPlan& p, cudaStream_t s) {
-  auto kern = gemm_bf16_swapab<kEpi, kCols>;
+  auto kern = gemm_bf16_swapab<kEpi>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     SPECTRE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          232448));
+                                          kGemmSmemBytes));
     configured = true;
   }
-  kern<<<p.grid, kGemmThreads, p.smem, s>>>(p.tmap_w, p.tmap_x, p.args);
+  kern<<<p.grid, kGemmThreads, kGemmSmemBytes, s>>>(p.tmap_w, p.tmap_x, p.args);
   SPECTRE_LAUNCH_CHECK("gemm_bf16_swapab");
   return SPECTRE_OK;
-}
-
-template <int kEpi>
-static int launch_epi(const GemmPlan& p, cudaStream_t s) {
-  switch (p.tmem_cols) {
-    case 32: return launch_one<kEpi, 32>(p, s);
-    case 64: return launch_one<kEpi, 64>(p, s);
-    case 128: return launch_one<kEpi, 128>(p, s);
-    case 256: return launch_one<kEpi, 256>(p, s);
-    default: return launch_one<kEpi, 512>(p, s);
-  }
 }
 
 int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_cap, int epi,
               int splits, int max_stages) {
   if (N < 1 || K < 64 || K % 64 || rows_cap < 64 || rows_cap % 64 || splits < 1)
     return arg_fail("gemm_plan: shape (K % 64, rows_cap multiple of 64)");
-  const int smem_rows = rows_cap < 512 ? rows_cap : 512;
   if (epi == kSwiGLU && (N % 128 || splits != 1)) return arg_fail("gemm_plan: swiglu shape");
   if (epi == kArgmax && splits != 1) return arg_fail("gemm_plan: argmax needs splits == 1");
   *p = GemmPlan{};
   if (int e = make_tmap_bf16(&p->tmap_w, W, (uint64_t)K, (uint64_t)N, 128)) return e;
   if (int e = make_tmap_bf16(&p->tmap_x, X, (uint64_t)K, (uint64_t)rows_cap, 64)) return e;
-  int stages = kGemmMaxStages;
-  if (max_stages > 0 && max_stages < stages) stages = max_stages;
-  while (stages > 2 && gemm_smem_bytes(stages, smem_rows) > 232448) --stages;
-  if (gemm_smem_bytes(stages, smem_rows) > 232448) return arg_fail("gemm_plan: smem");
-  const int n_tiles = (N + kGemmBlockN - 1) / kGemmBlockN;
-  uint32_t cols = 32;
-  while (cols < (uint32_t)smem_rows) cols <<= 1;
+  const int n_tiles = (N + kGemmTileN - 1) / kGemmTileN;
   p->epi = epi;
-  p->tmem_cols = (int)cols;
   p->grid = n_tiles * splits;
-  p->smem = gemm_smem_bytes(stages, smem_rows);
-  p->args.smem_rows = smem_rows;
   p->args.N = N;
   p->args.K = K;
   p->args.rows_cap = rows_cap;
   p->args.splits = splits;
-  p->args.stages = stages;
+  p->args.max_stages = max_stages;
   p->n_tiles = n_tiles;
+  p->n_amax_blocks = (N + 31) / 32;
   return SPECTRE_OK;
 }
 
 int gemm_run(const GemmPlan& p, cudaStream_t s) {
   switch (p.epi) {
-    case kPartial: return launch_epi<kPartial>(p, s);
-    case kArgmax: return launch_epi<kArgmax>(p, s);
-    default: return launch_epi<kSwiGLU>(p, s);
+    case kPartial: return launch_one<kPartial>(p, s);
+    case kArgmax: return launch_one<kArgmax>(p, s);
+    default: return launch_one<kSwiGLU>(p, s);
   }
 }
 

@@ -13,10 +13,9 @@ struct GemmPlan {
   CUtensorMap tmap_x;
   GemmArgs args;
   int grid = 0;
-  size_t smem = 0;
-  int tmem_cols = 0;
   int epi = 0;
-  int n_tiles = 0;
+  int n_tiles = 0;        // 256-row weight tiles
+  int n_amax_blocks = 0;  // 32-row argmax partial blocks
 };
 
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,

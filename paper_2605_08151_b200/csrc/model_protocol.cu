@@ -471,7 +471,20 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
   }
 }
 
+// host-free round budget: stop after `extra` more rounds
+__global__ void k_set_round_limit(DecodeStateDev s, int extra) {
+  CtrlDev& c = *s.ctrl;
+  const long long lim = (long long)c.round + extra;
+  c.round_limit = lim > 0x7fffffff ? 0x7fffffff : (int)lim;
+  c.round_base = c.round;
+}
+
 // ------------------------------------------------------------------ launchers
+int launch_set_round_limit(const DecodeStateDev& st, int extra, cudaStream_t s) {
+  k_set_round_limit<<<1, 1, 0, s>>>(st, extra);
+  SPECTRE_LAUNCH_CHECK("k_set_round_limit");
+  return SPECTRE_OK;
+}
 int launch_prefill_batch(const int* prompts, int prompt_len, int n_req, int c0, int cs,
                          const BatchDev& bt, cudaStream_t s) {
   k_prefill_batch<<<(n_req + 255) / 256, 256, 0, s>>>(prompts, prompt_len, n_req, c0, cs, bt);

@@ -34,9 +34,9 @@ def _run(env, X, W, T, rows_cap, splits=1, epi=PARTIAL, t_dev=None, max_stages=0
     N, K = W.shape
     dev = X.device
     part = torch.zeros(splits, rows_cap, N, dtype=torch.float32, device=dev)
-    n_tiles = (N + 127) // 128
-    av = torch.zeros(n_tiles, rows_cap, dtype=torch.float32, device=dev)
-    ai = torch.zeros(n_tiles, rows_cap, dtype=torch.int32, device=dev)
+    n_blocks = (N + 31) // 32
+    av = torch.zeros(n_blocks, rows_cap, dtype=torch.float32, device=dev)
+    ai = torch.zeros(n_blocks, rows_cap, dtype=torch.int32, device=dev)
     act = torch.zeros(rows_cap, max(N // 2, 1), dtype=torch.bfloat16, device=dev)
     st = fn(X.data_ptr(), W.data_ptr(), t_dev.data_ptr() if t_dev is not None else None, T,
             rows_cap, N, K, splits, epi, part.data_ptr(), av.data_ptr(), ai.data_ptr(),
@@ -54,7 +54,8 @@ def _ref(torch, X, W, T):
     (1, 64, 256, 64, 1), (16, 64, 384, 512, 1), (64, 64, 1024, 2048, 2),
     (37, 64, 640, 1024, 3), (256, 256, 6144, 4096, 3), (200, 256, 512, 4096, 4),
     (320, 320, 1024, 4096, 4), (512, 512, 256, 256, 1), (130, 192, 768, 1024, 1),
-    (700, 768, 384, 512, 2), (1280, 1280, 256, 1024, 1)])
+    (700, 768, 384, 512, 2), (1280, 1280, 256, 1024, 1), (300, 320, 640, 2048, 3),
+    (256, 256, 28672 // 8, 4096, 1), (77, 128, 1000, 640, 2)])
 def test_partial_matches_fp32(env, T, rows_cap, N, K, splits):
     torch = env[0]
     g = torch.Generator(device="cuda").manual_seed(T * 7 + N)
@@ -72,7 +73,7 @@ def test_runtime_token_count_and_stage_variants(env):
     X = torch.randn(256, 1024, device="cuda").bfloat16()
     W = (torch.randn(512, 1024, device="cuda") * 0.05).bfloat16()
     want = _ref(torch, X, W, 96)
-    for stages in (2, 3, 8):
+    for stages in (1, 2, 3, 8):
         t_dev = torch.tensor([96], dtype=torch.int32, device="cuda")
         part, *_ = _run(env, X, W, 0, 256, 2, t_dev=t_dev, max_stages=stages)
         got = part.sum(0)[:96]
@@ -95,7 +96,7 @@ def test_batch_invariance_bitwise(env):
 
 def test_argmax_epilogue(env):
     torch = env[0]
-    V, K, T = 128256, 2048, 70
+    V, K, T = 128256 - 96, 2048, 70
     X = torch.randn(128, K, device="cuda").bfloat16()
     W = (torch.randn(V, K, device="cuda") * 0.02).bfloat16()
     _, av, ai, _ = _run(env, X, W, T, 128, 1, ARGMAX)
