@@ -1,0 +1,419 @@
+"""SPECTRE decode-loop benchmark (BASELINE config 2) on B200.
+
+Metric: committed output tokens/s of the SPECTRE-adaptive (hybrid) decode
+loop, Llama-3.1-8B-shape target / Llama-3.2-1B-shape draft (random init,
+bf16), B=64 requests per GPU, gamma=4, prompt 128, output 1024 (greedy).
+A "step" is one complete pass of the hot path over one batch: prefill the
+64 prompts and decode every request to 1024 output tokens.  Inputs are
+synthetic; the KV cache (>L2) and weights (15 GB) are streamed every round,
+so no explicit L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): requests are independent, so each
+rank decodes its own batch of 64 (weak scaling); NCCL only gathers counters.
+--impl reference times the CPU restatement of the reference decode loop
+(oracle/lockstep.py — the reference itself is Python and absent on the GPU
+box) on this host's cores for the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_DEFAULT = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+METRIC = "SPECTRE output tok/s (8B target, B=64, gamma=4) vs ordinary/parallel SD; r* crossover"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return PEAKS_DEFAULT, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- helpers
+def dist_setup():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def allreduce_max(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def kernels_per_round(mode: str, gamma: int, tL: int, dL: int) -> int:
+    fwd_t = 1 + 9 * tL + 2
+    fwd_d = 1 + 9 * dL + 2
+    n = 2  # round_begin + accept
+    n += 1 + fwd_t  # verify_prep + target forward
+    if mode == "O":
+        n += 1 + (gamma - 1) * (fwd_d + 1)
+    elif mode == "P":
+        n += 1 + gamma * (fwd_d + 1)
+    return n
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    from paper_2605_08151_b200 import model as M
+    from paper_2605_08151_b200 import _native
+
+    ws, rank, local = dist_setup()
+    dev_index = local
+    B, g = args.batch, args.gamma
+    spec_kw = dict(n_req=B, gamma=g, output_len=args.out_len, prompt_len=args.prompt_len,
+                   alpha=args.alpha, seed=args.seed + rank, controller=args.controller)
+    base = M.DecodeSpec(**spec_kw)
+    pair = M.build_pair(M.LLAMA_31_8B, M.LLAMA_32_1B, n_req=B, ctx_cap=base.ctx_cap(),
+                        seed=args.seed, target_branch=args.branch, draft_branch=args.branch)
+    prompts = M.synthetic_prompts(B, args.prompt_len, M.LLAMA_31_8B.vocab, seed=args.seed + rank)
+    variants = [args.variant] + [v for v in ("ordinary", "parallel") if v != args.variant and
+                                 not args.headline_only]
+    engines = {v: M.SpectreEngine(pair, base, v) for v in variants}
+    stream = torch.cuda.Stream()
+    tokens_per_step = B * args.out_len
+
+    def one_step(eng):
+        eng.prefill(prompts, stream=stream)
+        eng.run(use_graph=True, stream=stream)
+
+    results = {}
+    for v in variants:
+        eng = engines[v]
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                one_step(eng)
+        torch.cuda.synchronize()
+        barrier(ws)
+        clocks = ClockSampler(dev_index)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with clocks:
+            torch.cuda.synchronize()
+            barrier(ws)
+            ev0.record(stream)
+            with torch.cuda.stream(stream):
+                for _ in range(args.steps):
+                    one_step(eng)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        barrier(ws)
+        ms = ev0.elapsed_time(ev1)
+        ms_max = allreduce_max(ms, ws)
+        committed, pos, trace = eng.read()
+        done = int((pos == args.out_len).sum().item())
+        if done != B:
+            raise RuntimeError(f"{v}: only {done}/{B} requests finished")
+        total_tokens = allreduce_sum(tokens_per_step * args.steps, ws)
+        rep = M.report_from_trace(__import__("paper_2605_08151_b200").PolicyVariant.parse(v),
+                                  args.seed, trace, tokens_per_step,
+                                  float(trace["t_round_ns"].sum()) * 1e-9)
+        modes = "".join(chr(int(m)) for m in trace["mode"])
+        launches = sum(kernels_per_round(m, g, M.LLAMA_31_8B.n_layers, M.LLAMA_32_1B.n_layers)
+                       for m in modes)
+        prefill_launches = 2 * ((args.prompt_len + 7) // 8) + 1  # batch kernels + admit
+        prefill_launches += ((args.prompt_len + 7) // 8) * (
+            (1 + 9 * 32 + 2) + (1 + 9 * 16 + 2))
+        results[v] = dict(
+            ms_per_step=ms_max / args.steps, value=total_tokens / (ms_max / 1e3),
+            rounds=len(modes), timeline=modes, clocks=clocks.summary(),
+            mean_L=rep.mean_accepted_length, content_L=rep.content_mean_accepted_length,
+            r_hat=rep.mean_rollback_ratio,
+            pad_frac=float(trace["n_padded"].sum() / max(1, trace["participants"].sum())),
+            t_round_ms=float(trace["t_round_ns"].mean()) * 1e-6,
+            t_verify_ms=float(trace["t_verify_ns"].mean()) * 1e-6,
+            t_draft_ms=float(trace["t_draft_ns"][trace["t_draft_ns"] > 0].mean() * 1e-6)
+            if (trace["t_draft_ns"] > 0).any() else 0.0,
+            gpu_launches=(launches + prefill_launches) * args.steps,
+            ordinary_share=modes.count("O") / max(1, len(modes)))
+
+    head = results[args.variant]
+    # ---- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        eng = engines[args.variant]
+        host_prompts = prompts.cpu().pin_memory()
+        out_host = torch.empty(B, args.out_len, dtype=torch.int64).pin_memory()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dev_prompts = torch.empty_like(prompts)
+        torch.cuda.synchronize()
+        barrier(ws)
+        ev0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                dev_prompts.copy_(host_prompts, non_blocking=True)
+                eng.prefill(dev_prompts, stream=stream)
+                eng.run(use_graph=True, stream=stream)
+                committed = eng.read_committed(stream=stream)
+                out_host.copy_(committed, non_blocking=True)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = allreduce_max(ev0.elapsed_time(ev1), ws)
+        e2e = {"value": allreduce_sum(tokens_per_step * args.steps, ws) / (ms / 1e3),
+               "unit": "tok/s", "h2d_bytes_per_step": int(host_prompts.numel() * 4),
+               "d2h_bytes_per_step": int(out_host.numel() * 8)}
+
+    # ---- roofline of the dominant kernel, timed live (CUDA events, its own stream)
+    roof = None
+    if not args.no_roofline and rank == 0:
+        roof = roofline_gate_up(pair, args)
+    # ---- CPU baseline (oracle port of the reference loop), rank 0, N=1 only
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0 and ws == 1:
+        cpu = cpu_baseline(args, alpha_meas=alpha_from_L(head["content_L"], g))
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(head["value"], 2), "unit": "tok/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(head["ms_per_step"], 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic prompts (TokenStreamOracle prompt stream mod V), random-init "
+                    "coupled weights",
+            "config": {"workload": "C2: llama-3.1-8b-shape target / llama-3.2-1b-shape draft, "
+                                   "B=64/GPU, gamma=4, prompt 128, output 1024, greedy",
+                       "variant": args.variant, "batch_per_gpu": B, "gamma": g,
+                       "output_len": args.out_len, "prompt_len": args.prompt_len,
+                       "draft_alpha": args.alpha, "branch_scale": args.branch,
+                       "controller": args.controller, "parallelism": f"dp{ws} (request shards)",
+                       "l2": "inputs > L2 (15 GB weights + KV streamed per round)"},
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "clocks": head["clocks"], "gpu_launches": head["gpu_launches"],
+            "modes": {v: {k: (round(x, 4) if isinstance(x, float) else x)
+                          for k, x in r.items() if k not in ("clocks", "timeline")}
+                      for v, r in results.items()},
+            "timeline_head": head["timeline"][:80],
+        }
+        print(json.dumps(line))
+
+
+def alpha_from_L(L: float, gamma: int) -> float:
+    """Invert E[delta] = (1 - a^gamma)/(1 - a) for a REPAIRED candidate."""
+    lo, hi = 0.0, 0.999999
+    for _ in range(60):
+        mid = (lo + hi) / 2
+        val = (1 - mid ** gamma) / (1 - mid)
+        if val < L:
+            lo = mid
+        else:
+            hi = mid
+    return round((lo + hi) / 2, 4)
+
+
+def roofline_gate_up(pair, args):
+    """Target verify-pass gate/up GEMM (SwiGLU epilogue) at T = B*gamma rows."""
+    import torch
+    from paper_2605_08151_b200 import _native
+    peaks, src = load_peaks()
+    L = _native.lib()
+    T = args.batch * args.gamma
+    W = pair.target.wgu[0]
+    F2, K = W.shape
+    X = torch.randn(512, K, device="cuda").bfloat16()
+    act = torch.empty(512, F2 // 2, dtype=torch.bfloat16, device="cuda")
+    s = torch.cuda.Stream()
+    times = []
+    with torch.cuda.stream(s):
+        for it in range(25):
+            Wl = pair.target.wgu[it % pair.target.spec.n_layers]  # rotate layers: > L2
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            _native.check(L.spectre_gemm_bf16(X.data_ptr(), Wl.data_ptr(), None, T, 512, F2, K, 1,
+                                              2, None, None, None, act.data_ptr(), F2 // 2, 0,
+                                              int(s.cuda_stream)), "gemm")
+            e1.record(s)
+            e1.synchronize()
+            if it >= 5:
+                times.append(e0.elapsed_time(e1) * 1e-3)
+    t = statistics.median(times)
+    bytes_ = F2 * K * 2 + T * K * 2 + T * (F2 // 2) * 2
+    flops = 2.0 * T * F2 * K
+    gbs = bytes_ / t / 1e9
+    tfs = flops / t / 1e12
+    hbm = peaks["hbm_gbs"]
+    tc = peaks["bf16_tflops"]
+    # bound = whichever roof is closer to binding at this intensity
+    bound = "hbm" if bytes_ / (hbm * 1e9) >= flops / (tc * 1e12) else "tensor"
+    ach, peak, unit = (gbs, hbm, "GB/s") if bound == "hbm" else (tfs, tc, "TFLOP/s")
+    return {"bound": bound, "achieved": round(ach, 1), "peak": peak, "unit": unit,
+            "frac": round(ach / peak, 4), "traffic": None,
+            "kernel": f"gemm_bf16_swapab<SwiGLU> target gate_up T={T} N={F2} K={K}",
+            "us_per_launch": round(t * 1e6, 2), "tflops": round(tfs, 1), "gbs": round(gbs, 1),
+            "peak_source": src + " (MEASURED_PEAKS.json burst)"}
+
+
+def cpu_baseline(args, alpha_meas: float, budget_s: float = 20.0):
+    """oracle/lockstep.py (CPU restatement of specsim.run) on one core."""
+    from oracle import lockstep as L
+    cfg = dict(batch_size=args.batch, n_requests=args.batch, gamma=args.gamma,
+               output_len=args.out_len, alpha=alpha_meas, qps=1e6, seed=args.seed)
+    t0 = time.perf_counter()
+    toks = 0
+    runs = 0
+    while True:
+        r = L.run({**cfg, "seed": args.seed + runs}, "hybrid")
+        toks += r.report["total_committed"]
+        runs += 1
+        if time.perf_counter() - t0 > budget_s * 0.5 or runs >= 8:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(toks / dt, 1), "unit": "tok/s", "cores": 1, "kind": "port",
+            "sample": f"{runs} x oracle/lockstep.run(hybrid, B={args.batch}, gamma={args.gamma}, "
+                      f"output_len={args.out_len}, alpha={alpha_meas}) on 1 host core "
+                      f"({os.cpu_count()} available)"}
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import lockstep as L
+    alpha = args.alpha_meas
+    cfg = dict(batch_size=args.batch, n_requests=args.batch, gamma=args.gamma,
+               output_len=args.out_len, alpha=alpha, qps=1e6, seed=args.seed)
+    for i in range(args.warmup):
+        L.run({**cfg, "seed": args.seed + 1000 + i}, args.variant)
+    t0 = time.perf_counter()
+    toks = 0
+    for i in range(args.steps):
+        r = L.run({**cfg, "seed": args.seed + i}, args.variant)
+        toks += r.report["total_committed"]
+    dt = time.perf_counter() - t0
+    v = toks / dt
+    sample = (f"{args.steps} x oracle/lockstep.run({args.variant}, B={args.batch}, "
+              f"gamma={args.gamma}, output_len={args.out_len}, alpha={alpha}); the reference "
+              f"(specsim, pure Python) cannot travel to the GPU box, this is its CPU port")
+    print(json.dumps({
+        "metric": METRIC, "value": round(v, 2), "unit": "tok/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (reference TokenStreamOracle model pair)", "impl": "reference",
+        "config": {"workload": "C2 protocol shape on the reference's synthetic model pair",
+                   "variant": args.variant, "batch": args.batch, "gamma": args.gamma,
+                   "output_len": args.out_len},
+        "cpu_baseline": {"value": round(v, 2), "unit": "tok/s", "cores": 1, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(v, 2), "unit": "tok/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--variant", default="hybrid")
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--gamma", type=int, default=4)
+    ap.add_argument("--out-len", type=int, default=1024)
+    ap.add_argument("--prompt-len", type=int, default=128)
+    ap.add_argument("--alpha", type=float, default=1.0, help="draft keep probability")
+    ap.add_argument("--alpha-meas", type=float, default=0.8,
+                    help="reference arm: agreement rate of the synthetic pair")
+    ap.add_argument("--branch", type=float, default=0.004)
+    ap.add_argument("--controller", default="round")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--headline-only", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

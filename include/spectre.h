@@ -260,6 +260,9 @@ typedef struct SpectreRoundTrace {
 } SpectreRoundTrace;
 int spectre_engine_read(void* engine, int64_t* committed, int32_t* committed_pos,
                         const SpectreRoundTrace* trace, int32_t* n_rounds, void* stream);
+/* Asynchronous device-to-device copy of the committed tokens (int64,
+ * [n_req][output_len]) on `stream` — the per-step output of the decode. */
+int spectre_engine_read_committed(void* engine, int64_t* committed, void* stream);
 /* One forward pass over a packed ragged batch (tests / roofline):
  * which 0 = target, 1 = draft.  tok/pos/slot [T]; per request q_off, n_new,
  * pos0 [n_req] (n_new 0 = not participating).  out_tok [T] greedy argmax;

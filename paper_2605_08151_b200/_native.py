@@ -133,6 +133,7 @@ def _bind_model(L) -> None:
     _sig(L, "spectre_engine_graph_status", C.c_int, [_P])
     _sig(L, "spectre_engine_read", C.c_int,
          [_P, _P, _P, C.POINTER(RoundTraceBufs), C.POINTER(i32), _P])
+    _sig(L, "spectre_engine_read_committed", C.c_int, [_P, _P, _P])
     _sig(L, "spectre_engine_forward", C.c_int,
          [_P, i32, _P, _P, _P, i32, _P, _P, _P, _P, _P, _P])
 

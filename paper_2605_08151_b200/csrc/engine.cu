@@ -58,6 +58,7 @@ static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 static int pick_splits(int n_tiles, int k_iters) {
   int s = 148 / n_tiles;  // one wave of CTAs (1 CTA per SM: 512 TMEM columns)
+  if (s > 12) s = 12;     // partial traffic grows with s (consumers unroll <= 12)
   if (s < 1) s = 1;
   while (s > 1 && k_iters / s < 3) --s;
   return s;
@@ -632,6 +633,15 @@ extern "C" int spectre_engine_read(void* engine, int64_t* committed, int32_t* co
     TRY(cp(trace->accepted_len_ema, t.accepted_len_ema, R * 8));
     TRY(cp(trace->r_star, t.r_star, R * 8));
   }
+  return SPECTRE_OK;
+}
+
+extern "C" int spectre_engine_read_committed(void* engine, int64_t* committed, void* stream) {
+  auto* e = reinterpret_cast<Engine*>(engine);
+  if (!e || !committed) return arg_fail("spectre_engine_read_committed");
+  SPECTRE_CUDA_TRY(cudaMemcpyAsync(committed, e->st.committed,
+                                   (size_t)e->cfg.n_req * e->cfg.output_len * 8,
+                                   cudaMemcpyDeviceToDevice, as_stream(stream)));
   return SPECTRE_OK;
 }
 

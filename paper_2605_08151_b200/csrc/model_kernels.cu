@@ -69,54 +69,72 @@ __global__ void __launch_bounds__(256) k_embed_rmsnorm(const int* __restrict__ t
 
 // ---------------------------------------------- residual add (+split-K sum)
 // h[t] += sum_s part[s][t]; x[t] = bf16(rmsnorm(h[t]) * w).  One CTA per token
-// row, float4 lanes, every load of a row issued before the reduction.
-template <int kVec>  // float4 per thread
-__global__ void __launch_bounds__(256) k_residual_rmsnorm_v(const float* __restrict__ part,
-                                                            int splits, int rows_cap,
-                                                            const int* __restrict__ t_dev,
-                                                            const float* __restrict__ w,
-                                                            float* __restrict__ h,
-                                                            __nv_bfloat16* __restrict__ x, int d,
-                                                            float eps) {
-  __shared__ float sh[16];
+// row, one float4 per thread; all split partials are loaded before the fixed-
+// order sum so the loads overlap instead of forming a latency chain.
+constexpr int kMaxSplits = 12;
+
+template <int kVec>
+__global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restrict__ part,
+                                                             int splits, int rows_cap,
+                                                             const int* __restrict__ t_dev,
+                                                             const float* __restrict__ w,
+                                                             float* __restrict__ h,
+                                                             __nv_bfloat16* __restrict__ x,
+                                                             int d, float eps) {
+  __shared__ float sh[40];
   const int t = blockIdx.x;
   if (t >= *t_dev) return;
   const int nv = d >> 2;
   float4 v[kVec];
-  float ss = 0.f;
   const float4* h4 = reinterpret_cast<const float4*>(h + (size_t)t * d);
+  const size_t sstride = (size_t)rows_cap * d / 4;
+  const float4* p4 = reinterpret_cast<const float4*>(part + (size_t)t * d);
 #pragma unroll
   for (int j = 0; j < kVec; ++j) {
-    const int i = threadIdx.x + j * 256;
-    if (i < nv) v[j] = h4[i];
-  }
-  for (int sp = 0; sp < splits; ++sp) {
-    const float4* p4 = reinterpret_cast<const float4*>(part + ((size_t)sp * rows_cap + t) * d);
+    const int i = threadIdx.x + j * blockDim.x;
+    if (i < nv) {
+      float4 acc = h4[i];
+      float4 ld[kMaxSplits];
 #pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      const int i = threadIdx.x + j * 256;
-      if (i < nv) {
-        const float4 a = __ldg(p4 + i);
-        v[j].x += a.x; v[j].y += a.y; v[j].z += a.z; v[j].w += a.w;
-      }
+      for (int sp = 0; sp < kMaxSplits; ++sp)
+        if (sp < splits) ld[sp] = __ldg(p4 + sp * sstride + i);
+#pragma unroll
+      for (int sp = 0; sp < kMaxSplits; ++sp)
+        if (sp < splits) {
+          acc.x += ld[sp].x; acc.y += ld[sp].y; acc.z += ld[sp].z; acc.w += ld[sp].w;
+        }
+      v[j] = acc;
     }
   }
+  float ss = 0.f;
   float4* ho = reinterpret_cast<float4*>(h + (size_t)t * d);
 #pragma unroll
   for (int j = 0; j < kVec; ++j) {
-    const int i = threadIdx.x + j * 256;
+    const int i = threadIdx.x + j * blockDim.x;
     if (i < nv) {
       ho[i] = v[j];
       ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
     }
   }
-  ss = block_sum_256(ss, sh);
-  const float r = rsqrtf(ss / (float)d + eps);
+  // deterministic block reduction (fixed shuffle tree + fixed warp order)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const int nw = (blockDim.x + 31) >> 5;
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float r = threadIdx.x < nw ? sh[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (threadIdx.x == 0) sh[32] = r;
+  }
+  __syncthreads();
+  const float r = rsqrtf(sh[32] / (float)d + eps);
   const float4* w4 = reinterpret_cast<const float4*>(w);
   __nv_bfloat162* xo = reinterpret_cast<__nv_bfloat162*>(x + (size_t)t * d);
 #pragma unroll
   for (int j = 0; j < kVec; ++j) {
-    const int i = threadIdx.x + j * 256;
+    const int i = threadIdx.x + j * blockDim.x;
     if (i < nv) {
       const float4 ww = w4[i];
       xo[2 * i] = __floats2bfloat162_rn(v[j].x * r * ww.x, v[j].y * r * ww.y);
@@ -127,8 +145,9 @@ __global__ void __launch_bounds__(256) k_residual_rmsnorm_v(const float* __restr
 
 // ------------------------------------------- qkv epilogue: RoPE + KV write
 // part: [splits][rows_cap][(n_q + 2 n_kv) * hd] fp32.  rope: [ctx_cap][hd/2] (cos, sin)
-// Rotate-half convention: pairs (i, i + hd/2).  One CTA per token row.
-__global__ void __launch_bounds__(256) k_qkv_rope_kv(const float* __restrict__ part, int splits,
+// Rotate-half convention: pairs (i, i + hd/2).  grid (token, pair block); one
+// (i, i+hd/2) pair per thread, all split loads issued up front.
+__global__ void __launch_bounds__(128) k_qkv_rope_kv(const float* __restrict__ part, int splits,
                                                      int rows_cap, const int* __restrict__ t_dev,
                                                      const int* __restrict__ tok_pos,
                                                      const int* __restrict__ tok_slot,
@@ -139,49 +158,47 @@ __global__ void __launch_bounds__(256) k_qkv_rope_kv(const float* __restrict__ p
                                                      int n_kv, int hd, int ctx_cap) {
   const int t = blockIdx.x;
   if (t >= *t_dev) return;
-  const int N = (n_q + 2 * n_kv) * hd;
-  const int pos = tok_pos[t];
-  const int slot = tok_slot[t];
   const int half = hd / 2;
-  const int n_pairs = (n_q + n_kv) * half;     // rotated q and k pairs
-  const int n_v = n_kv * half;                 // v handled as (i, i+half) pairs too
-  const float* p0 = part + (size_t)t * N;
+  const int c = blockIdx.y * 128 + threadIdx.x;
+  const int n_pairs = (n_q + 2 * n_kv) * half;
+  if (c >= n_pairs) return;
+  const int head = c / half, i = c % half;
+  const int N = (n_q + 2 * n_kv) * hd;
+  const float* p0 = part + (size_t)t * N + head * hd + i;
   const size_t sstride = (size_t)rows_cap * N;
-  const float2* rp = rope + (size_t)pos * half;
-#pragma unroll 4
-  for (int c = threadIdx.x; c < n_pairs + n_v; c += 256) {
-    int head, i;
-    if (c < n_pairs) {
-      head = c / half;
-      i = c % half;
+  float la[kMaxSplits], lb[kMaxSplits];
+#pragma unroll
+  for (int sp = 0; sp < kMaxSplits; ++sp)
+    if (sp < splits) {
+      la[sp] = __ldg(p0 + sp * sstride);
+      lb[sp] = __ldg(p0 + sp * sstride + half);
+    }
+  float a = 0.f, b = 0.f;
+#pragma unroll
+  for (int sp = 0; sp < kMaxSplits; ++sp)
+    if (sp < splits) {
+      a += la[sp];
+      b += lb[sp];
+    }
+  const int pos = tok_pos[t];
+  if (head < n_q + n_kv) {
+    const float2 cs = rope[(size_t)pos * half + i];
+    const float ra = a * cs.x - b * cs.y;
+    const float rb = b * cs.x + a * cs.y;
+    if (head < n_q) {
+      __nv_bfloat16* dst = q + ((size_t)t * n_q + head) * hd;
+      dst[i] = __float2bfloat16_rn(ra);
+      dst[i + half] = __float2bfloat16_rn(rb);
     } else {
-      head = n_q + n_kv + (c - n_pairs) / half;
-      i = (c - n_pairs) % half;
+      const size_t off = (((size_t)tok_slot[t] * n_kv + (head - n_q)) * ctx_cap + pos) * hd;
+      kc[off + i] = __float2bfloat16_rn(ra);
+      kc[off + i + half] = __float2bfloat16_rn(rb);
     }
-    const int base = head * hd;
-    float a = 0.f, b = 0.f;
-    for (int sp = 0; sp < splits; ++sp) {
-      a += __ldg(p0 + sp * sstride + base + i);
-      b += __ldg(p0 + sp * sstride + base + i + half);
-    }
-    if (head < n_q + n_kv) {
-      const float2 cs = rp[i];
-      const float ra = a * cs.x - b * cs.y;
-      const float rb = b * cs.x + a * cs.y;
-      if (head < n_q) {
-        __nv_bfloat16* dst = q + ((size_t)t * n_q + head) * hd;
-        dst[i] = __float2bfloat16_rn(ra);
-        dst[i + half] = __float2bfloat16_rn(rb);
-      } else {
-        const size_t off = (((size_t)slot * n_kv + (head - n_q)) * ctx_cap + pos) * hd;
-        kc[off + i] = __float2bfloat16_rn(ra);
-        kc[off + i + half] = __float2bfloat16_rn(rb);
-      }
-    } else {
-      const size_t off = (((size_t)slot * n_kv + (head - n_q - n_kv)) * ctx_cap + pos) * hd;
-      vc[off + i] = __float2bfloat16_rn(a);
-      vc[off + i + half] = __float2bfloat16_rn(b);
-    }
+  } else {
+    const size_t off =
+        (((size_t)tok_slot[t] * n_kv + (head - n_q - n_kv)) * ctx_cap + pos) * hd;
+    vc[off + i] = __float2bfloat16_rn(a);
+    vc[off + i + half] = __float2bfloat16_rn(b);
   }
 }
 
@@ -586,17 +603,20 @@ int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void
 int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const int* t_dev,
                             int t_cap, const float* w, float* h, void* x, int d, float eps,
                             cudaStream_t s) {
-  if (d % 4) return arg_fail("residual_rmsnorm: d % 4");
-  const int vec = (d / 4 + 255) / 256;
+  if (d % 4 || splits > kMaxSplits) return arg_fail("residual_rmsnorm: d % 4 / splits");
+  const int nv = d / 4;
+  const int threads = nv < 512 ? ((nv + 31) / 32) * 32 : 512;
+  const int vec = (nv + threads - 1) / threads;
   auto* xb = reinterpret_cast<__nv_bfloat16*>(x);
   if (vec <= 1)
-    k_residual_rmsnorm_v<1><<<t_cap, 256, 0, s>>>(part, splits, rows_cap, t_dev, w, h, xb, d, eps);
+    k_residual_rmsnorm_v<1><<<t_cap, threads, 0, s>>>(part, splits, rows_cap, t_dev, w, h, xb, d,
+                                                      eps);
   else if (vec <= 2)
-    k_residual_rmsnorm_v<2><<<t_cap, 256, 0, s>>>(part, splits, rows_cap, t_dev, w, h, xb, d, eps);
+    k_residual_rmsnorm_v<2><<<t_cap, threads, 0, s>>>(part, splits, rows_cap, t_dev, w, h, xb, d,
+                                                      eps);
   else if (vec <= 4)
-    k_residual_rmsnorm_v<4><<<t_cap, 256, 0, s>>>(part, splits, rows_cap, t_dev, w, h, xb, d, eps);
-  else if (vec <= 8)
-    k_residual_rmsnorm_v<8><<<t_cap, 256, 0, s>>>(part, splits, rows_cap, t_dev, w, h, xb, d, eps);
+    k_residual_rmsnorm_v<4><<<t_cap, threads, 0, s>>>(part, splits, rows_cap, t_dev, w, h, xb, d,
+                                                      eps);
   else
     return arg_fail("residual_rmsnorm: d > 8192");
   SPECTRE_LAUNCH_CHECK("k_residual_rmsnorm");
@@ -607,7 +627,9 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
                        const int* tok_pos, const int* tok_slot, const void* rope, void* q,
                        void* kc, void* vc, int n_q, int n_kv, int hd, int ctx_cap,
                        cudaStream_t s) {
-  k_qkv_rope_kv<<<t_cap, 256, 0, s>>>(
+  if (splits > kMaxSplits) return arg_fail("qkv_rope_kv: splits");
+  const int pairs = (n_q + 2 * n_kv) * hd / 2;
+  k_qkv_rope_kv<<<dim3(t_cap, (pairs + 127) / 128), 128, 0, s>>>(
       part, splits, rows_cap, t_dev, tok_pos, tok_slot, reinterpret_cast<const float2*>(rope),
       reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<__nv_bfloat16*>(kc),
       reinterpret_cast<__nv_bfloat16*>(vc), n_q, n_kv, hd, ctx_cap);

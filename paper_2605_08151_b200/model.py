@@ -244,12 +244,16 @@ class SpectreEngine:
         _native.check(_native.lib().spectre_engine_prefill(
             self.handle, prompts.data_ptr(), _native.stream_ptr(stream)), "spectre_engine_prefill")
 
-    def run(self, max_rounds: int | None = None, use_graph: bool = True, stream=None) -> int:
+    def run(self, max_rounds: int | None = None, use_graph: bool = True, stream=None,
+            sync: bool = False) -> int | None:
+        """Decode rounds on the device.  Asynchronous unless sync=True (then the
+        number of rounds run is returned)."""
         n = C.c_int32(0)
         _native.check(_native.lib().spectre_engine_run(
             self.handle, int(max_rounds if max_rounds is not None else self.max_rounds),
-            int(use_graph), C.byref(n), _native.stream_ptr(stream)), "spectre_engine_run")
-        return n.value
+            int(use_graph), C.byref(n) if sync else None, _native.stream_ptr(stream)),
+            "spectre_engine_run")
+        return n.value if sync else None
 
     def graph_status(self) -> int:
         return _native.lib().spectre_engine_graph_status(self.handle)
@@ -272,6 +276,16 @@ class SpectreEngine:
         torch.cuda.synchronize()
         trace = {f: v[:nr.value].cpu().numpy() for f, v in bufs.items()}
         return committed, pos, trace
+
+    def read_committed(self, stream=None):
+        """Committed tokens [n_req][output_len] int64 on the device (no host sync)."""
+        torch = _native.require_cuda()
+        out = torch.empty(self.spec.n_req, self.spec.output_len, dtype=torch.int64,
+                          device="cuda")
+        _native.check(_native.lib().spectre_engine_read_committed(
+            self.handle, out.data_ptr(), _native.stream_ptr(stream)),
+            "spectre_engine_read_committed")
+        return out
 
     def forward(self, which: int, tok, pos, slot, q_off, n_new, pos0, want_x=False):
         torch = _native.require_cuda()
@@ -361,7 +375,7 @@ def decode(pair: ModelPair, spec: DecodeSpec, variant, prompts=None, use_graph=T
     if prompts is None:
         prompts = synthetic_prompts(spec.n_req, spec.prompt_len, pair.target.spec.vocab, spec.seed)
     eng.prefill(prompts)
-    rounds = eng.run(use_graph=use_graph)
+    rounds = eng.run(use_graph=use_graph, sync=True)
     committed, pos, trace = eng.read()
     dev_s = float(trace["t_round_ns"].sum()) * 1e-9
     total = int(pos.sum().item())

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--calib-len", type=int, default=160)
     ap.add_argument("--branches", default="0.02,0.05,0.1")
     ap.add_argument("--alpha", type=float, default=1.0)
+    ap.add_argument("--calib-only", action="store_true")
     args = ap.parse_args()
     spec = M.DecodeSpec(n_req=64, gamma=4, output_len=args.out_len, prompt_len=128,
                         alpha=args.alpha, seed=0)
@@ -58,6 +59,10 @@ def main():
         r = M.decode(pair, cal, "ordinary")
         L = r.report.content_mean_accepted_length
         print(json.dumps(dict(branch=br, calib=summarize(r, cal))), flush=True)
+        if args.calib_only:
+            del pair
+            torch.cuda.empty_cache()
+            continue
         for v in ("ordinary", "parallel", "hybrid"):
             r = M.decode(pair, spec, v)
             s = summarize(r, spec)
