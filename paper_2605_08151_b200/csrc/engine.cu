@@ -11,6 +11,7 @@
 //                                                       accept ◄──────┘◄── (join)
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -56,6 +57,12 @@ struct Bump {
 
 static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+static int attn_chunk_default() {
+  const char* v = getenv("SPECTRE_ATTN_CHUNK");
+  const int c = v ? atoi(v) : 512;
+  return (c == 128 || c == 256 || c == 512) ? c : 512;
+}
+
 static int pick_splits(int n_tiles, int k_iters) {
   int s = 148 / n_tiles;  // one wave of CTAs (1 CTA per SM: 512 TMEM columns)
   if (s > 12) s = 12;     // partial traffic grows with s (consumers unroll <= 12)
@@ -70,9 +77,11 @@ struct ModelRT {
   SpectreModelWeights w{};
   int n_req = 0, rows_cap = 0, ctx_cap = 0, max_new = 1, split_max = 1, rb_cap = 1;
   int sp_qkv = 1, sp_o = 1, sp_d = 1;
+  int attn_chunk = 128;
   float* h = nullptr;
   __nv_bfloat16 *x = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
   float *part = nullptr, *att_o = nullptr, *att_ml = nullptr, *amax_v = nullptr;
+  int* att_cnt = nullptr;
   int* amax_i = nullptr;
   float2* rope = nullptr;
   BatchDev bt{};
@@ -89,17 +98,19 @@ struct ModelRT {
     sp_o = pick_splits((d + 255) / 256, qd / 64);
     sp_d = pick_splits((d + 255) / 256, dm.ffn / 64);
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
-    split_max = (ctx_cap + kAttnChunk - 1) / kAttnChunk;
-    rb_cap = (max_new * group() + 31) / 32;
+    attn_chunk = attn_chunk_default();
+    split_max = (ctx_cap + attn_chunk - 1) / attn_chunk;
+    rb_cap = (max_new * group() + 15) / 16;
     h = b.take<float>((size_t)R * d);
     x = b.take<__nv_bfloat16>((size_t)R * d);
     q = b.take<__nv_bfloat16>((size_t)R * qd);
     attn = b.take<__nv_bfloat16>((size_t)R * qd);
     act = b.take<__nv_bfloat16>((size_t)R * dm.ffn);
     part = b.take<float>(part_n * R);
-    const size_t att_rows = (size_t)n_req * dm.n_kv_heads * rb_cap * split_max * 32;
+    const size_t att_rows = (size_t)n_req * dm.n_kv_heads * rb_cap * split_max * 16;
     att_o = b.take<float>(att_rows * dm.head_dim);
     att_ml = b.take<float>(att_rows * 2);
+    att_cnt = b.take<int>((size_t)n_req * dm.n_kv_heads * rb_cap);
     const int n_blocks = (dm.vocab + 31) / 32;
     amax_v = b.take<float>((size_t)n_blocks * R);
     amax_i = b.take<int>((size_t)n_blocks * R);
@@ -148,7 +159,7 @@ struct ModelRT {
     const int d = dm.d_model, L = dm.n_layers, hd = dm.head_dim;
     const float eps = dm.rms_eps;
     const int rows = new_per_req * group();
-    const int mt = rows <= 16 ? 1 : 2;
+    const int mt = 1;
     AttnArgs a{};
     a.q = q;
     a.q_off = bt.q_off;
@@ -159,12 +170,14 @@ struct ModelRT {
     a.n_q = dm.n_q_heads;
     a.n_kv = dm.n_kv_heads;
     a.ctx_cap = ctx_cap;
-    a.rb_max = (rows + 16 * mt - 1) / (16 * mt);
-    if (a.rb_max * mt > rb_cap * 2) return arg_fail("forward: rows per request exceed capacity");
+    a.rb_max = (rows + 15) / 16;
+    if (a.rb_max > rb_cap) return arg_fail("forward: rows per request exceed capacity");
     a.split_max = split_max;
+    a.chunk = attn_chunk;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
     a.part_o = att_o;
     a.part_ml = att_ml;
+    a.done_cnt = att_cnt;
     a.out = attn;
     const size_t kv_layer = (size_t)n_req * dm.n_kv_heads * ctx_cap * hd;
     auto* kc = reinterpret_cast<__nv_bfloat16*>(w.k_cache);

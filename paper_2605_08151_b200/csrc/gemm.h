@@ -16,13 +16,14 @@ struct GemmPlan {
   int epi = 0;
   int n_tiles = 0;        // 256-row weight tiles
   int n_amax_blocks = 0;  // 32-row argmax partial blocks
+  int bk = 32;            // K per pipeline stage (32: 64B swizzle, 64: 128B swizzle)
 };
 
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
-                   uint32_t box_outer);
+                   uint32_t box_outer, uint32_t box_inner = 64);
 // W: [N][K] bf16, X: [rows_cap][K] bf16.  Output pointers are filled by the caller.
 int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_cap, int epi,
-              int splits, int max_stages = 0);
+              int splits, int max_stages = 0, int bk = 0);
 int gemm_run(const GemmPlan& p, cudaStream_t s);
 
 }  // namespace spectre

@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 
+#include "common.cuh"
 #include "ptx.cuh"
 
 namespace spectre {
@@ -34,7 +35,8 @@ enum GemmEpilogue : int { kPartial = 0, kArgmax = 1, kSwiGLU = 2 };
 
 constexpr int kGemmThreads = 320;      // 2 control warps + 8 epilogue warps
 constexpr int kGemmTileN = 256;        // weight rows per CTA
-constexpr int kGemmBlockK = 64;        // K per stage (one 128-byte swizzle row)
+// K per pipeline stage is a template parameter: 64 (128-byte swizzle rows) or
+// 32 (64-byte rows: half-size stages -> twice as many in flight).
 constexpr int kGemmMaxStages = 8;
 constexpr int kGemmSmemBytes = 232448; // dynamic smem requested at launch
 constexpr int kGemmScratch = 2 * 64 * 17 * 4 + 1024;
@@ -83,7 +85,7 @@ __device__ __forceinline__ GemmPhase gemm_phase(int T, int p) {
   return ph;
 }
 
-template <int kEpi>
+template <int kEpi, int BK>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
                  const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
@@ -97,10 +99,13 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
 
   int T = a.t_dev ? *a.t_dev : a.t_static;
   T = T < 0 ? 0 : (T > a.rows_cap ? a.rows_cap : T);
+  constexpr int kRow = BK * 2;              // bytes per K-row segment (swizzle span)
+  constexpr int kWBox = 128 * kRow;         // one 128-row weight box
+  constexpr int kXBox = 64 * kRow;          // one 64-row activation box
   // runtime stage layout: W bytes + X bytes per stage
-  const int w_bytes = (T <= 256) ? 32768 : 16384;
+  const int w_bytes = (T <= 256) ? 2 * kWBox : kWBox;
   const int x_rows = (T <= 256) ? ((T + 63) & ~63) : min((T + 63) & ~63, 512);
-  const int stage_bytes = w_bytes + x_rows * 128;
+  const int stage_bytes = w_bytes + x_rows * kRow;
   int stages = stage_bytes > 0 ? kGemmPipeBytes / stage_bytes : 1;
   stages = stages > kGemmMaxStages ? kGemmMaxStages : (stages < 1 ? 1 : stages);
   if (a.max_stages > 0 && stages > a.max_stages) stages = a.max_stages;
@@ -117,7 +122,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   const int tile = blockIdx.x % n_tiles;
   const int split = blockIdx.x / n_tiles;
   const int n0 = tile * kGemmTileN;
-  const int k_iters_total = a.K / kGemmBlockK;
+  const int k_iters_total = a.K / BK;
   const int it_begin = (int)((long long)k_iters_total * split / a.splits);
   const int it_end = (int)((long long)k_iters_total * (split + 1) / a.splits);
   const int n_iters = it_end - it_begin;
@@ -140,7 +145,16 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  const bool producer = (warp == 0 && lane == 0);
+  if (!producer) {  // everyone but the TMA lane waits for the previous kernel now
+    pdl_wait();
+    pdl_trigger();
+  }
   if (T == 0 || n_iters <= 0) {
+    if (producer) {
+      pdl_wait();
+      pdl_trigger();
+    }
     if (kEpi == kPartial && warp >= 2) {  // K < splits: this split contributes zeros
       for (int r = threadIdx.x - 64; r < kGemmTileN; r += 256) {
         const int n = n0 + r;
@@ -153,24 +167,47 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();   // weights stream through once
       const uint64_t pol_x = policy_evict_last();    // activations are re-read by every tile
+      // Weights never change: the first stages' weight tiles are requested
+      // before waiting on the previous kernel (its tail overlaps our fill).
+      const GemmPhase ph0 = gemm_phase(T, 0);
+      const int pre = n_iters < stages ? n_iters : stages;
+      {
+        const int x_boxes = (ph0.nt + 63) >> 6;
+        const uint32_t tx = (uint32_t)ph0.boxes * kWBox + (uint32_t)x_boxes * kXBox;
+        for (int i = 0; i < pre; ++i) {
+          mbar_arrive_expect_tx(&full[i], tx);
+          const int kc = (it_begin + i) * BK;
+          for (int b = 0; b < ph0.boxes; ++b)
+            tma_load_2d(pipe + i * stage_bytes + b * kWBox, &tmap_w, &full[i], kc,
+                        n0 + ph0.row_off + b * 128, pol_w);
+        }
+      }
+      pdl_wait();
+      pdl_trigger();
       int g = 0;
       for (int p = 0; p < n_phases; ++p) {
         const GemmPhase ph = gemm_phase(T, p);
         const int x_boxes = (ph.nt + 63) >> 6;
-        const uint32_t tx = (uint32_t)ph.boxes * 16384u + (uint32_t)x_boxes * 8192u;
+        const uint32_t tx = (uint32_t)ph.boxes * kWBox + (uint32_t)x_boxes * kXBox;
         for (int i = 0; i < n_iters; ++i, ++g) {
           const int s = g % stages;
-          const uint32_t par = (uint32_t)(g / stages) & 1u;
-          mbar_wait(&empty[s], par ^ 1u);
-          mbar_arrive_expect_tx(&full[s], tx);
           uint8_t* st = pipe + s * stage_bytes;
-          const int kc = (it_begin + i) * kGemmBlockK;
-          for (int b = 0; b < ph.boxes; ++b)
-            tma_load_2d(st + b * 16384, &tmap_w, &full[s], kc, n0 + ph.row_off + b * 128, pol_w);
+          const int kc = (it_begin + i) * BK;
+          if (g >= pre) {
+            const uint32_t par = (uint32_t)(g / stages) & 1u;
+            mbar_wait(&empty[s], par ^ 1u);
+            mbar_arrive_expect_tx(&full[s], tx);
+            for (int b = 0; b < ph.boxes; ++b)
+              tma_load_2d(st + b * kWBox, &tmap_w, &full[s], kc, n0 + ph.row_off + b * 128,
+                          pol_w);
+          }
           for (int b = 0; b < x_boxes; ++b)
-            tma_load_2d(st + w_bytes + b * 8192, &tmap_x, &full[s], kc, ph.t0 + b * 64, pol_x);
+            tma_load_2d(st + w_bytes + b * kXBox, &tmap_x, &full[s], kc, ph.t0 + b * 64, pol_x);
         }
       }
+    } else {
+      pdl_wait();
+      pdl_trigger();
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread)
@@ -195,18 +232,19 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
           const uint32_t sa = smem_u32(pipe + s * stage_bytes);
           const uint32_t xa = sa + (uint32_t)w_bytes;
 #pragma unroll
-          for (int kk = 0; kk < kGemmBlockK / 16; ++kk) {
+          for (int kk = 0; kk < BK / 16; ++kk) {
             const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-            const uint64_t bd = umma_desc_sw128(xa + kk * 32);
+            const uint64_t bd = umma_desc_kmajor<kRow>(xa + kk * 32);
             if (ph.boxes == 2) {
-              mma_bf16_ss(tmem_base, umma_desc_sw128(sa + kk * 32), bd, id0, acc);
-              mma_bf16_ss(tmem_base + 256, umma_desc_sw128(sa + 16384 + kk * 32), bd, id0, acc);
+              mma_bf16_ss(tmem_base, umma_desc_kmajor<kRow>(sa + kk * 32), bd, id0, acc);
+              mma_bf16_ss(tmem_base + 256, umma_desc_kmajor<kRow>(sa + kWBox + kk * 32), bd, id0,
+                          acc);
             } else {
-              const uint64_t ad = umma_desc_sw128(sa + kk * 32);
+              const uint64_t ad = umma_desc_kmajor<kRow>(sa + kk * 32);
               mma_bf16_ss(tmem_base, ad, bd, id0, acc);
               if (nc1 > 0)
-                mma_bf16_ss(tmem_base + 256, ad, umma_desc_sw128(xa + 256 * 128 + kk * 32), id1,
-                            acc);
+                mma_bf16_ss(tmem_base + 256, ad, umma_desc_kmajor<kRow>(xa + 256 * kRow + kk * 32),
+                            id1, acc);
             }
           }
           mma_commit(&empty[s]);

@@ -6,6 +6,7 @@
 // bit-identical in a verify pass and in plain autoregressive decoding.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -51,6 +52,8 @@ __global__ void __launch_bounds__(256) k_embed_rmsnorm(const int* __restrict__ t
                                                        float* __restrict__ h,
                                                        __nv_bfloat16* __restrict__ x, int d,
                                                        float eps) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sh[16];
   const int t = blockIdx.x;
   if (t >= *t_dev) return;
@@ -81,6 +84,8 @@ __global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restr
                                                              float* __restrict__ h,
                                                              __nv_bfloat16* __restrict__ x,
                                                              int d, float eps) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sh[40];
   const int t = blockIdx.x;
   if (t >= *t_dev) return;
@@ -156,6 +161,8 @@ __global__ void __launch_bounds__(128) k_qkv_rope_kv(const float* __restrict__ p
                                                      __nv_bfloat16* __restrict__ kc,
                                                      __nv_bfloat16* __restrict__ vc, int n_q,
                                                      int n_kv, int hd, int ctx_cap) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   if (t >= *t_dev) return;
   const int half = hd / 2;
@@ -236,266 +243,286 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-// grid (split_max, rb_max, n_req * n_kv), 128 threads.  Each CTA: one request,
-// one kv head, a block of 16*MT query rows (token-major x group heads) and up
-// to 512 keys; warp w owns keys [c0 + 128 w, +128) in 4 x 32-key steps with
-// an online softmax, then the 4 warps merge in fixed order.
-template <int HD, int MT>
-__global__ void __launch_bounds__(kAttnThreads) k_attention(AttnArgs a) {
-  constexpr int ROWS = 16 * MT;
-  constexpr int LD = HD + 8;  // padded smem row (elements)
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Persistent attention.  A grid of one or more CTAs per SM walks the work
+// items (request, kv head, block of 16 query rows, split of `chunk` keys).
+// Rows are token-major x GQA heads (4 tokens x 4 heads = one 16-row MMA tile
+// for a gamma=4 verify).  Inside an item, warp w of NW owns keys
+// [c0 + w*chunk/NW, +chunk/NW) and streams them in 16-key steps through two
+// cp.async buffers (step i+1 loading while step i runs S = Q K^T, the online
+// softmax and O += P V on mma.sync m16n8k16).  The NW warps merge in a fixed
+// order, write the split's partial, and the last split of a row block to
+// finish merges all splits in split order into the bf16 output.  Chunk / warp
+// / step boundaries are absolute key positions: a token's result does not
+// depend on the rest of the batch.
+template <int HD, int NW>
+__global__ void __launch_bounds__(NW * 32) k_attention(AttnArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int ROWS = 16;
+  constexpr int STEP = 16;
+  constexpr int LD = HD + 8;           // padded smem row: conflict-free ldmatrix
+  constexpr int TILE = STEP * LD;      // one K or V step tile (elements)
+  constexpr int NT = NW * 32;
   extern __shared__ __align__(16) uint8_t smem_attn[];
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_attn);
-  __nv_bfloat16* sKV = sQ + ROWS * LD;  // per warp: K[32][LD], V[32][LD]
-
-  const int split = blockIdx.x, rb = blockIdx.y;
-  const int b = blockIdx.z / a.n_kv, kvh = blockIdx.z % a.n_kv;
-  const int group = a.n_q / a.n_kv;
-  const int nn = a.n_new[b];
-  const int rows_total = nn * group;
-  if (rb * ROWS >= rows_total) return;
-  const int p0 = a.pos0[b];
-  const int kv_len = p0 + nn;
-  const int c0 = split * kAttnChunk;
-  if (c0 >= kv_len) return;
-  const int last_row = min(rows_total, (rb + 1) * ROWS) - 1;
-  const int p_max = p0 + last_row / group;  // largest query position in this block
-  const int qoff = a.q_off[b];
-  const size_t kv_base = ((size_t)a.slot[b] * a.n_kv + kvh) * a.ctx_cap;
-
+  __nv_bfloat16* sKV = sQ + ROWS * LD;  // per warp: 2 buffers x (K, V)
+  __shared__ int s_last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // ---- Q tile
-  for (int c = tid; c < ROWS * (HD / 8); c += kAttnThreads) {
-    const int r = c / (HD / 8), ch = c % (HD / 8);
-    const int R = rb * ROWS + r;
-    const bool valid = R < rows_total;
-    const int j = valid ? R / group : 0, hh = valid ? R % group : 0;
-    const __nv_bfloat16* src = a.q + (((size_t)(qoff + j) * a.n_q) + kvh * group + hh) * HD + ch * 8;
-    cp_async16(ptx_smem(sQ + r * LD + ch * 8), src, valid);
-  }
-  cp_async_wait_all();
-  __syncthreads();
+  const int group = a.n_q / a.n_kv;
+  const int g = lane >> 2, tq = lane & 3;
+  __nv_bfloat16* wbuf = sKV + warp * 4 * TILE;
+  const int n_items = a.n_req * a.n_kv * a.rb_max * a.split_max;
+  const int per_warp = a.chunk / NW;
 
-  __nv_bfloat16* sK = sKV + warp * 2 * 32 * LD;
-  __nv_bfloat16* sV = sK + 32 * LD;
-  float o[MT][HD / 8][4];
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int split = item % a.split_max;
+    const int rb = (item / a.split_max) % a.rb_max;
+    const int bk = item / (a.split_max * a.rb_max);
+    const int b = bk / a.n_kv, kvh = bk % a.n_kv;
+    const int nn = a.n_new[b];
+    const int rows_total = nn * group;
+    if (rb * ROWS >= rows_total) continue;
+    const int p0 = a.pos0[b];
+    const int c0 = split * a.chunk;
+    const int last_row = min(rows_total, (rb + 1) * ROWS) - 1;
+    const int p_max = p0 + last_row / group;   // largest query position of the block
+    if (c0 > p_max) continue;                  // chunk entirely in the causal future
+    const int kv_len = p0 + nn;
+    const int qoff = a.q_off[b];
+    const size_t kv_base = ((size_t)a.slot[b] * a.n_kv + kvh) * a.ctx_cap;
+
+    for (int c = tid; c < ROWS * (HD / 8); c += NT) {
+      const int r = c / (HD / 8), ch = c % (HD / 8);
+      const int R = rb * ROWS + r;
+      const bool valid = R < rows_total;
+      const int j = valid ? R / group : 0, hh = valid ? R % group : 0;
+      const __nv_bfloat16* src =
+          a.q + (((size_t)(qoff + j) * a.n_q) + kvh * group + hh) * HD + ch * 8;
+      cp_async16(ptx_smem(sQ + r * LD + ch * 8), src, valid);
+    }
+    cp_async_commit();
+
+    const int w0 = c0 + warp * per_warp;
+    const int w_end = min(w0 + per_warp, p_max + 1);
+    const int steps = w_end > w0 ? (w_end - w0 + STEP - 1) / STEP : 0;
+    auto issue = [&](int st) {
+      const int kb = w0 + st * STEP;
+      __nv_bfloat16* sK = wbuf + (st & 1) * 2 * TILE;
+      __nv_bfloat16* sV = sK + TILE;
 #pragma unroll
-  for (int m = 0; m < MT; ++m)
+      for (int c = lane; c < STEP * (HD / 8); c += 32) {
+        const int r = c / (HD / 8), ch = c % (HD / 8);
+        const bool valid = kb + r < kv_len;
+        const size_t off = (kv_base + (valid ? kb + r : 0)) * HD + ch * 8;
+        cp_async16(ptx_smem(sK + r * LD + ch * 8), a.k + off, valid);
+        cp_async16(ptx_smem(sV + r * LD + ch * 8), a.v + off, valid);
+      }
+      cp_async_commit();
+    };
+    if (steps > 0) issue(0);
+    if (steps > 1) issue(1);
+    if (steps > 1) cp_async_wait<2>();
+    else if (steps > 0) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();   // Q tile visible to every warp
+
+    float o[HD / 8][4];
 #pragma unroll
     for (int n = 0; n < HD / 8; ++n)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) o[m][n][e] = 0.f;
-  float mrow[MT][2], lrow[MT][2];
-#pragma unroll
-  for (int m = 0; m < MT; ++m) {
-    mrow[m][0] = mrow[m][1] = -INFINITY;
-    lrow[m][0] = lrow[m][1] = 0.f;
-  }
-  const int g = lane >> 2, tq = lane & 3;
-  // query position of the two rows this thread owns in each m-tile
-  int qpos[MT][2];
-  bool qvalid[MT][2];
-#pragma unroll
-  for (int m = 0; m < MT; ++m)
+      for (int e = 0; e < 4; ++e) o[n][e] = 0.f;
+    float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+    int qpos[2];
+    bool qvalid[2];
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
-      const int R = rb * ROWS + m * 16 + g + hr * 8;
-      qvalid[m][hr] = R < rows_total;
-      qpos[m][hr] = p0 + (qvalid[m][hr] ? R / group : 0);
+      const int R = rb * ROWS + g + hr * 8;
+      qvalid[hr] = R < rows_total;
+      qpos[hr] = p0 + (qvalid[hr] ? R / group : 0);
     }
 
-  for (int it = 0; it < 4; ++it) {
-    const int kb = c0 + warp * 128 + it * kAttnSub;
-    if (kb > p_max || kb >= c0 + kAttnChunk) break;
-    // ---- load 32 keys of K and V (zero-fill beyond kv_len)
-    for (int c = lane; c < 32 * (HD / 8); c += 32) {
-      const int r = c / (HD / 8), ch = c % (HD / 8);
-      const bool valid = kb + r < kv_len;
-      const size_t off = (kv_base + (valid ? kb + r : 0)) * HD + ch * 8;
-      cp_async16(ptx_smem(sK + r * LD + ch * 8), a.k + off, valid);
-      cp_async16(ptx_smem(sV + r * LD + ch * 8), a.v + off, valid);
-    }
-    cp_async_wait_all();
-    __syncwarp();
-    // ---- S = Q K^T  (MT x 4 n-tiles of 8 keys)
-    float s[MT][4][4];
+    // Q fragments stay in registers for the whole item
+    uint32_t qf[HD / 16][4];
 #pragma unroll
-    for (int m = 0; m < MT; ++m)
+    for (int kk = 0; kk < HD / 16; ++kk)
+      ldsm_x4(ptx_smem(sQ + (lane & 15) * LD + kk * 16 + (lane >> 4) * 8), qf[kk][0], qf[kk][1],
+              qf[kk][2], qf[kk][3]);
+
+    for (int st = 0; st < steps; ++st) {
+      if (st + 1 < steps) cp_async_wait<1>();
+      else cp_async_wait<0>();
+      __syncwarp();
+      const int kb = w0 + st * STEP;
+      const __nv_bfloat16* sK = wbuf + (st & 1) * 2 * TILE;
+      const __nv_bfloat16* sV = sK + TILE;
+      // two independent accumulation chains per n-tile (even / odd k-steps)
+      float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+      float t0[4] = {0.f, 0.f, 0.f, 0.f}, t1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int n = 0; n < 4; ++n)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) s[m][n][e] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      uint32_t af[MT][4];
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        const int r = m * 16 + (lane & 15);
-        const int cc = kk * 16 + (lane >> 4) * 8;
-        ldsm_x4(ptx_smem(sQ + r * LD + cc), af[m][0], af[m][1], af[m][2], af[m][3]);
-      }
-#pragma unroll
-      for (int np = 0; np < 2; ++np) {  // n-tile pairs (16 keys)
-        const int mi = lane >> 3;
-        const int r = np * 16 + (mi >> 1) * 8 + (lane & 7);
-        const int cc = kk * 16 + (mi & 1) * 8;
+      for (int kk = 0; kk < HD / 16; ++kk) {
         uint32_t b0, b1, b2, b3;
-        ldsm_x4(ptx_smem(sK + r * LD + cc), b0, b1, b2, b3);
-#pragma unroll
-        for (int m = 0; m < MT; ++m) {
-          mma16816(s[m][2 * np], af[m][0], af[m][1], af[m][2], af[m][3], b0, b1);
-          mma16816(s[m][2 * np + 1], af[m][0], af[m][1], af[m][2], af[m][3], b2, b3);
+        const int mi = lane >> 3;
+        ldsm_x4(ptx_smem(sK + ((mi >> 1) * 8 + (lane & 7)) * LD + kk * 16 + (mi & 1) * 8), b0, b1,
+                b2, b3);
+        if (kk & 1) {
+          mma16816(t0, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b0, b1);
+          mma16816(t1, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b2, b3);
+        } else {
+          mma16816(s0, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b0, b1);
+          mma16816(s1, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b2, b3);
         }
       }
-    }
-    // ---- mask + online softmax (log2 domain)
 #pragma unroll
-    for (int m = 0; m < MT; ++m) {
+      for (int e = 0; e < 4; ++e) {
+        s0[e] += t0[e];
+        s1[e] += t1[e];
+      }
+      // mask + online softmax (log2 domain); s0: keys kb+2tq+{0,1}, s1: kb+8+2tq+{0,1}
+      float p[2][4];
 #pragma unroll
       for (int hr = 0; hr < 2; ++hr) {
+        float v[4] = {s0[hr * 2], s0[hr * 2 + 1], s1[hr * 2], s1[hr * 2 + 1]};
         float mx = -INFINITY;
 #pragma unroll
-        for (int n = 0; n < 4; ++n)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int key = kb + n * 8 + 2 * tq + e;
-            float v = s[m][n][hr * 2 + e] * a.scale_log2;
-            if (!qvalid[m][hr] || key > qpos[m][hr]) v = -INFINITY;
-            s[m][n][hr * 2 + e] = v;
-            mx = fmaxf(mx, v);
-          }
+        for (int e = 0; e < 4; ++e) {
+          const int key = kb + (e >> 1) * 8 + 2 * tq + (e & 1);
+          v[e] *= a.scale_log2;
+          if (!qvalid[hr] || key > qpos[hr]) v[e] = -INFINITY;
+          mx = fmaxf(mx, v[e]);
+        }
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(mrow[m][hr], mx);
-        const float corr = (m_new == -INFINITY) ? 1.f : exp2f(mrow[m][hr] - m_new);
+        const float m_new = fmaxf(mrow[hr], mx);
+        const float corr = (m_new == -INFINITY) ? 1.f : exp2f(mrow[hr] - m_new);
         float rs = 0.f;
 #pragma unroll
-        for (int n = 0; n < 4; ++n)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const float v = s[m][n][hr * 2 + e];
-            const float p = (v == -INFINITY) ? 0.f : exp2f(v - m_new);
-            s[m][n][hr * 2 + e] = p;
-            rs += p;
-          }
+        for (int e = 0; e < 4; ++e) {
+          p[hr][e] = (v[e] == -INFINITY) ? 0.f : exp2f(v[e] - m_new);
+          rs += p[hr][e];
+        }
         rs += __shfl_xor_sync(0xffffffffu, rs, 1);
         rs += __shfl_xor_sync(0xffffffffu, rs, 2);
-        lrow[m][hr] = lrow[m][hr] * corr + rs;
-        mrow[m][hr] = m_new;
+        lrow[hr] = lrow[hr] * corr + rs;
+        mrow[hr] = m_new;
 #pragma unroll
         for (int n = 0; n < HD / 8; ++n) {
-          o[m][n][hr * 2] *= corr;
-          o[m][n][hr * 2 + 1] *= corr;
+          o[n][hr * 2] *= corr;
+          o[n][hr * 2 + 1] *= corr;
         }
       }
-    }
-    // ---- O += P V   (2 k-steps of 16 keys)
+      // P (A fragment of the 16-key k-step) x V
+      const uint32_t pa0 = pack_bf16(p[0][0], p[0][1]);
+      const uint32_t pa1 = pack_bf16(p[1][0], p[1][1]);
+      const uint32_t pa2 = pack_bf16(p[0][2], p[0][3]);
+      const uint32_t pa3 = pack_bf16(p[1][2], p[1][3]);
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      uint32_t pa[MT][4];
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        pa[m][0] = pack_bf16(s[m][2 * ks][0], s[m][2 * ks][1]);
-        pa[m][1] = pack_bf16(s[m][2 * ks][2], s[m][2 * ks][3]);
-        pa[m][2] = pack_bf16(s[m][2 * ks + 1][0], s[m][2 * ks + 1][1]);
-        pa[m][3] = pack_bf16(s[m][2 * ks + 1][2], s[m][2 * ks + 1][3]);
-      }
-#pragma unroll
-      for (int dp = 0; dp < HD / 16; ++dp) {  // dim-tile pairs
+      for (int dp = 0; dp < HD / 16; ++dp) {
         const int mi = lane >> 3;
-        const int r = ks * 16 + (mi & 1) * 8 + (lane & 7);
-        const int cc = dp * 16 + (mi >> 1) * 8;
         uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(ptx_smem(sV + r * LD + cc), b0, b1, b2, b3);
-#pragma unroll
-        for (int m = 0; m < MT; ++m) {
-          mma16816(o[m][2 * dp], pa[m][0], pa[m][1], pa[m][2], pa[m][3], b0, b1);
-          mma16816(o[m][2 * dp + 1], pa[m][0], pa[m][1], pa[m][2], pa[m][3], b2, b3);
-        }
+        ldsm_x4_t(ptx_smem(sV + ((mi & 1) * 8 + (lane & 7)) * LD + dp * 16 + (mi >> 1) * 8), b0,
+                  b1, b2, b3);
+        mma16816(o[2 * dp], pa0, pa1, pa2, pa3, b0, b1);
+        mma16816(o[2 * dp + 1], pa0, pa1, pa2, pa3, b2, b3);
       }
+      __syncwarp();
+      if (st + 2 < steps) issue(st + 2);
     }
-    __syncwarp();
-  }
 
-  // ---- merge the 4 warps in fixed order (smem reuse of the K/V area)
-  __syncthreads();
-  float* sO = reinterpret_cast<float*>(sKV);            // [4][ROWS][HD]
-  float* sML = sO + 4 * ROWS * HD;                      // [4][ROWS][2]
-#pragma unroll
-  for (int m = 0; m < MT; ++m)
+    // ---- merge the NW warps in fixed order (reuses the K/V area)
+    __syncthreads();
+    float* sO = reinterpret_cast<float*>(sKV);   // [NW][ROWS][HD]
+    float* sML = sO + NW * ROWS * HD;            // [NW][ROWS][2]
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
-      const int r = m * 16 + g + hr * 8;
+      const int r = g + hr * 8;
 #pragma unroll
-      for (int n = 0; n < HD / 8; ++n) {
-        sO[(warp * ROWS + r) * HD + n * 8 + 2 * tq] = o[m][n][hr * 2];
-        sO[(warp * ROWS + r) * HD + n * 8 + 2 * tq + 1] = o[m][n][hr * 2 + 1];
-      }
+      for (int n = 0; n < HD / 8; ++n)
+        *reinterpret_cast<float2*>(&sO[(warp * ROWS + r) * HD + n * 8 + 2 * tq]) =
+            make_float2(o[n][hr * 2], o[n][hr * 2 + 1]);
       if (tq == 0) {
-        sML[(warp * ROWS + r) * 2] = mrow[m][hr];
-        sML[(warp * ROWS + r) * 2 + 1] = lrow[m][hr];
+        sML[(warp * ROWS + r) * 2] = mrow[hr];
+        sML[(warp * ROWS + r) * 2 + 1] = lrow[hr];
       }
     }
-  __syncthreads();
-  const size_t pidx =
-      (((size_t)b * a.n_kv + kvh) * a.rb_max + rb) * a.split_max + split;
-  for (int c = tid; c < ROWS * HD; c += kAttnThreads) {
-    const int r = c / HD, dcol = c % HD;
-    float M = -INFINITY;
+    __syncthreads();
+    const size_t pidx = (((size_t)b * a.n_kv + kvh) * a.rb_max + rb) * a.split_max + split;
+    for (int c = tid; c < ROWS * HD / 4; c += NT) {
+      const int r = (c * 4) / HD, dcol = (c * 4) % HD;
+      float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sML[(w * ROWS + r) * 2]);
-    float O = 0.f, Lsum = 0.f;
+      for (int w = 0; w < NW; ++w) M = fmaxf(M, sML[(w * ROWS + r) * 2]);
+      float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+      float Lsum = 0.f;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = sML[(w * ROWS + r) * 2];
-      const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-      O += sO[(w * ROWS + r) * HD + dcol] * f;
-      Lsum += sML[(w * ROWS + r) * 2 + 1] * f;
+      for (int w = 0; w < NW; ++w) {
+        const float mw = sML[(w * ROWS + r) * 2];
+        const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+        const float4 v = *reinterpret_cast<const float4*>(&sO[(w * ROWS + r) * HD + dcol]);
+        O.x += v.x * f;
+        O.y += v.y * f;
+        O.z += v.z * f;
+        O.w += v.w * f;
+        Lsum += sML[(w * ROWS + r) * 2 + 1] * f;
+      }
+      *reinterpret_cast<float4*>(&a.part_o[(pidx * ROWS + r) * HD + dcol]) = O;
+      if (dcol == 0) {
+        a.part_ml[(pidx * ROWS + r) * 2] = M;
+        a.part_ml[(pidx * ROWS + r) * 2 + 1] = Lsum;
+      }
     }
-    a.part_o[(pidx * ROWS + r) * HD + dcol] = O;
-    if (dcol == 0) {
-      a.part_ml[(pidx * ROWS + r) * 2] = M;
-      a.part_ml[(pidx * ROWS + r) * 2 + 1] = Lsum;
+    // ---- last split of this row block merges all splits in split order
+    __threadfence();
+    __syncthreads();
+    const int n_split = (p_max + 1 + a.chunk - 1) / a.chunk;   // splits with c0 <= p_max
+    if (tid == 0) {
+      int* cnt = a.done_cnt + ((size_t)b * a.n_kv + kvh) * a.rb_max + rb;
+      const int prev = atomicAdd(cnt, 1);
+      s_last = (prev == n_split - 1);
+      if (s_last) *cnt = 0;  // self-reset for the next launch
     }
-  }
-}
-
-// grid (rb_max, n_req * n_kv), 128 threads: merge splits -> out (bf16)
-template <int HD, int MT>
-__global__ void __launch_bounds__(128) k_attn_combine(AttnArgs a) {
-  constexpr int ROWS = 16 * MT;
-  const int rb = blockIdx.x;
-  const int b = blockIdx.y / a.n_kv, kvh = blockIdx.y % a.n_kv;
-  const int group = a.n_q / a.n_kv;
-  const int nn = a.n_new[b];
-  const int rows_total = nn * group;
-  if (rb * ROWS >= rows_total) return;
-  const int kv_len = a.pos0[b] + nn;
-  const int n_split = (kv_len + kAttnChunk - 1) / kAttnChunk;
-  const int qoff = a.q_off[b];
-  for (int c = threadIdx.x; c < ROWS * HD; c += 128) {
-    const int r = c / HD, dcol = c % HD;
-    const int R = rb * ROWS + r;
-    if (R >= rows_total) continue;
-    // only splits that start at or before this row's query position hold keys
-    const int qp = a.pos0[b] + R / group;
-    const int ns = min(n_split, qp / kAttnChunk + 1);
-    float M = -INFINITY;
-    for (int s = 0; s < ns; ++s) {
-      const size_t pidx = (((size_t)b * a.n_kv + kvh) * a.rb_max + rb) * a.split_max + s;
-      M = fmaxf(M, a.part_ml[(pidx * ROWS + r) * 2]);
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const size_t base = (((size_t)b * a.n_kv + kvh) * a.rb_max + rb) * a.split_max;
+      for (int c = tid; c < ROWS * HD / 4; c += NT) {
+        const int r = (c * 4) / HD, dcol = (c * 4) % HD;
+        const int R = rb * ROWS + r;
+        if (R >= rows_total) continue;
+        const int qp = p0 + R / group;
+        const int ns = min(n_split, qp / a.chunk + 1);
+        float M = -INFINITY;
+        for (int sp = 0; sp < ns; ++sp)
+          M = fmaxf(M, __ldcg(&a.part_ml[((base + sp) * ROWS + r) * 2]));
+        float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+        float Lsum = 0.f;
+        for (int sp = 0; sp < ns; ++sp) {
+          const float ms = __ldcg(&a.part_ml[((base + sp) * ROWS + r) * 2]);
+          const float f = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(
+              &a.part_o[((base + sp) * ROWS + r) * HD + dcol]));
+          O.x += v.x * f;
+          O.y += v.y * f;
+          O.z += v.z * f;
+          O.w += v.w * f;
+          Lsum += __ldcg(&a.part_ml[((base + sp) * ROWS + r) * 2 + 1]) * f;
+        }
+        const float inv = 1.f / Lsum;
+        const int j = R / group, hh = R % group;
+        __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(
+            a.out + (((size_t)(qoff + j)) * a.n_q + kvh * group + hh) * HD + dcol);
+        dst[0] = __floats2bfloat162_rn(O.x * inv, O.y * inv);
+        dst[1] = __floats2bfloat162_rn(O.z * inv, O.w * inv);
+      }
     }
-    float O = 0.f, Lsum = 0.f;
-    for (int s = 0; s < ns; ++s) {
-      const size_t pidx = (((size_t)b * a.n_kv + kvh) * a.rb_max + rb) * a.split_max + s;
-      const float ms = a.part_ml[(pidx * ROWS + r) * 2];
-      const float f = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
-      O += a.part_o[(pidx * ROWS + r) * HD + dcol] * f;
-      Lsum += a.part_ml[(pidx * ROWS + r) * 2 + 1] * f;
-    }
-    const int j = R / group, hh = R % group;
-    a.out[(((size_t)(qoff + j)) * a.n_q + kvh * group + hh) * HD + dcol] =
-        __float2bfloat16_rn(O / Lsum);
+    __syncthreads();  // smem reused by the next item
   }
 }
 
@@ -507,6 +534,8 @@ __global__ void __launch_bounds__(256) k_argmax_reduce(const float* __restrict__
                                                        const int* __restrict__ t_dev,
                                                        int* __restrict__ out_tok,
                                                        float* __restrict__ out_val) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   if (t >= *t_dev) return;
   float best = -INFINITY;
@@ -560,43 +589,55 @@ __global__ void k_rope_table(float2* rope, int ctx_cap, int hd, double theta) {
 }
 
 // ------------------------------------------------------------------ launchers
-static int attn_smem(int hd, int mt) {
-  const int rows = 16 * mt, ld = hd + 8;
-  const int load = (rows * ld + 4 * 2 * 32 * ld) * 2;
-  const int merge = rows * ld * 2 + (4 * rows * hd + 4 * rows * 2) * 4;
+template <int HD, int NW>
+static int attn_smem() {
+  constexpr int ld = HD + 8;
+  constexpr int load = (16 * ld + NW * 4 * 16 * ld) * 2;
+  constexpr int merge = 16 * ld * 2 + (NW * 16 * HD + NW * 16 * 2) * 4;
   return load > merge ? load : merge;
 }
 
-template <int HD, int MT>
+static int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <int HD, int NW>
 static int launch_attn_t(const AttnArgs& a, cudaStream_t s) {
   static bool cfg = false;
-  const int smem = attn_smem(HD, MT);
+  const int smem = attn_smem<HD, NW>();
   if (!cfg) {
-    SPECTRE_CUDA_TRY(
-        cudaFuncSetAttribute(k_attention<HD, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SPECTRE_CUDA_TRY(cudaFuncSetAttribute(k_attention<HD, NW>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cfg = true;
   }
-  dim3 grid(a.split_max, a.rb_max, a.n_req * a.n_kv);
-  k_attention<HD, MT><<<grid, kAttnThreads, smem, s>>>(a);
-  SPECTRE_LAUNCH_CHECK("k_attention");
-  k_attn_combine<HD, MT><<<dim3(a.rb_max, a.n_req * a.n_kv), 128, 0, s>>>(a);
-  SPECTRE_LAUNCH_CHECK("k_attn_combine");
+  int per_sm = 1;
+  SPECTRE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attention<HD, NW>,
+                                                                 NW * 32, smem));
+  per_sm = std::max(1, per_sm);
+  const int items = a.n_req * a.n_kv * a.rb_max * a.split_max;
+  const int grid = std::min(items, per_sm * num_sms());
+  SPECTRE_LAUNCH_PDL("k_attention", k_attention<HD, NW>, dim3(grid), dim3(NW * 32), smem, s, a);
   return SPECTRE_OK;
 }
 
 int launch_attention(const AttnArgs& a, int hd, int mt, cudaStream_t s) {
-  if (hd == 128 && mt == 1) return launch_attn_t<128, 1>(a, s);
-  if (hd == 128 && mt == 2) return launch_attn_t<128, 2>(a, s);
-  if (hd == 64 && mt == 1) return launch_attn_t<64, 1>(a, s);
-  if (hd == 64 && mt == 2) return launch_attn_t<64, 2>(a, s);
-  return arg_fail("attention: head_dim must be 64 or 128, mt 1 or 2");
+  (void)mt;  // rows are processed in 16-row blocks (rb_max of them)
+  if (hd == 128) return launch_attn_t<128, 8>(a, s);
+  if (hd == 64) return launch_attn_t<64, 8>(a, s);
+  return arg_fail("attention: head_dim must be 64 or 128");
 }
 
 int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void* E,
                          const float* w, float* h, void* x, int d, float eps, cudaStream_t s) {
-  k_embed_rmsnorm<<<t_cap, 256, 0, s>>>(tok, t_dev, reinterpret_cast<const __nv_bfloat16*>(E),
-                                        w, h, reinterpret_cast<__nv_bfloat16*>(x), d, eps);
-  SPECTRE_LAUNCH_CHECK("k_embed_rmsnorm");
+  SPECTRE_LAUNCH_PDL("k_embed_rmsnorm", k_embed_rmsnorm, dim3(t_cap), dim3(256), 0, s, tok, t_dev,
+                     reinterpret_cast<const __nv_bfloat16*>(E), w, h,
+                     reinterpret_cast<__nv_bfloat16*>(x), d, eps);
   return SPECTRE_OK;
 }
 
@@ -609,17 +650,16 @@ int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const i
   const int vec = (nv + threads - 1) / threads;
   auto* xb = reinterpret_cast<__nv_bfloat16*>(x);
   if (vec <= 1)
-    k_residual_rmsnorm_v<1><<<t_cap, threads, 0, s>>>(part, splits, rows_cap, t_dev, w, h, xb, d,
-                                                      eps);
+    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<1>, dim3(t_cap), dim3(threads),
+                       0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
   else if (vec <= 2)
-    k_residual_rmsnorm_v<2><<<t_cap, threads, 0, s>>>(part, splits, rows_cap, t_dev, w, h, xb, d,
-                                                      eps);
+    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<2>, dim3(t_cap), dim3(threads),
+                       0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
   else if (vec <= 4)
-    k_residual_rmsnorm_v<4><<<t_cap, threads, 0, s>>>(part, splits, rows_cap, t_dev, w, h, xb, d,
-                                                      eps);
+    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<4>, dim3(t_cap), dim3(threads),
+                       0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
   else
     return arg_fail("residual_rmsnorm: d > 8192");
-  SPECTRE_LAUNCH_CHECK("k_residual_rmsnorm");
   return SPECTRE_OK;
 }
 
@@ -629,19 +669,19 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
                        cudaStream_t s) {
   if (splits > kMaxSplits) return arg_fail("qkv_rope_kv: splits");
   const int pairs = (n_q + 2 * n_kv) * hd / 2;
-  k_qkv_rope_kv<<<dim3(t_cap, (pairs + 127) / 128), 128, 0, s>>>(
-      part, splits, rows_cap, t_dev, tok_pos, tok_slot, reinterpret_cast<const float2*>(rope),
-      reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<__nv_bfloat16*>(kc),
-      reinterpret_cast<__nv_bfloat16*>(vc), n_q, n_kv, hd, ctx_cap);
-  SPECTRE_LAUNCH_CHECK("k_qkv_rope_kv");
+  SPECTRE_LAUNCH_PDL("k_qkv_rope_kv", k_qkv_rope_kv, dim3(t_cap, (pairs + 127) / 128), dim3(128),
+                     0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
+                     reinterpret_cast<const float2*>(rope), reinterpret_cast<__nv_bfloat16*>(q),
+                     reinterpret_cast<__nv_bfloat16*>(kc), reinterpret_cast<__nv_bfloat16*>(vc),
+                     n_q, n_kv, hd, ctx_cap);
   return SPECTRE_OK;
 }
 
 int launch_argmax_reduce(const float* val, const int* idx, int n_tiles, int rows_cap,
                          const int* t_dev, int t_cap, int* out_tok, float* out_val,
                          cudaStream_t s) {
-  k_argmax_reduce<<<t_cap, 256, 0, s>>>(val, idx, n_tiles, rows_cap, t_dev, out_tok, out_val);
-  SPECTRE_LAUNCH_CHECK("k_argmax_reduce");
+  SPECTRE_LAUNCH_PDL("k_argmax_reduce", k_argmax_reduce, dim3(t_cap), dim3(256), 0, s, val, idx,
+                     n_tiles, rows_cap, t_dev, out_tok, out_val);
   return SPECTRE_OK;
 }
 

@@ -23,13 +23,15 @@ struct AttnArgs {
   const int* slot;           // [n_req] KV slot
   int n_req, n_q, n_kv, ctx_cap;
   int rb_max, split_max;
+  int chunk;                 // keys per CTA (multiple of 128: 4 warps x 32-key steps)
   float scale_log2;          // hd^-0.5 * log2(e)
   float* part_o;             // [n_req][n_kv][rb_max][split_max][rows_blk][hd]
   float* part_ml;            // [n_req][n_kv][rb_max][split_max][rows_blk][2]
+  int* done_cnt;             // [n_req][n_kv][rb_max] split arrivals (self-resetting)
   __nv_bfloat16* out;        // [rows][n_q][hd]
 };
 
-constexpr int kAttnChunk = 512;   // keys per CTA (one split)
+constexpr int kAttnChunkMax = 512;  // largest keys-per-CTA (split) supported
 constexpr int kAttnSub = 32;      // keys per warp iteration
 constexpr int kAttnThreads = 128;
 

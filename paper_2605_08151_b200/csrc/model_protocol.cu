@@ -55,6 +55,8 @@ __device__ __forceinline__ int noisy_draft_token(const DecodeStateDev& s, int re
 // ------------------------------------------------------------ prefill helpers
 __global__ void k_prefill_batch(const int* prompts, int prompt_len, int n_req, int c0, int cs,
                                 BatchDev bt) {
+  pdl_wait();
+  pdl_trigger();
   const int b = threadIdx.x + blockIdx.x * blockDim.x;
   const int n = min(cs, prompt_len - c0);
   if (b == 0) *bt.t_dev = n * n_req;
@@ -73,6 +75,8 @@ __global__ void k_prefill_batch(const int* prompts, int prompt_len, int n_req, i
 // After the target's last prompt chunk: admission commits output token 0
 // (target_engine.py:105-126) and resets every round-protocol field.
 __global__ void k_admit(DecodeStateDev s, BatchDev bt) {
+  pdl_wait();
+  pdl_trigger();
   const int b = threadIdx.x + blockIdx.x * blockDim.x;
   if (b == 0) {
     CtrlDev& c = *s.ctrl;
@@ -106,6 +110,8 @@ __global__ void k_admit(DecodeStateDev s, BatchDev bt) {
 // ------------------------------------------------------------ round begin
 // Controller (sim.py:447-467) + conditional-node selection.
 __global__ void k_round_begin(DecodeStateDev s) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x != 0) return;
   CtrlDev& c = *s.ctrl;
   c.t_round_begin = globaltimer();
@@ -172,6 +178,8 @@ __global__ void k_round_begin(DecodeStateDev s) {
 // batch for the draft's first step (draft_engine.py:246-280, 412-431).
 __global__ void __launch_bounds__(kProtoThreads) k_draft_prep(DecodeStateDev s, BatchDev bt,
                                                               int which_mode) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int sh[kProtoThreads];
   CtrlDev& c = *s.ctrl;
   const int mode = c.mode;
@@ -237,6 +245,8 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_prep(DecodeStateDev s, 
 // After each draft forward: append the (noised) greedy token, next 1-token batch.
 __global__ void __launch_bounds__(kProtoThreads) k_draft_append(DecodeStateDev s, BatchDev bt,
                                                                 int which_mode, int last_step) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int sh[kProtoThreads];
   CtrlDev& c = *s.ctrl;
   if (c.mode != which_mode) {
@@ -280,6 +290,8 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_append(DecodeStateDev s
 // Candidate assembly (target_engine.py:132-221) -> verify batch rows
 // [pending bonus @ pos-1, candidate tokens @ pos ...].
 __global__ void __launch_bounds__(kProtoThreads) k_verify_prep(DecodeStateDev s, BatchDev bt) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int sh[kProtoThreads];
   CtrlDev& c = *s.ctrl;
   const int mode = c.mode;
@@ -351,6 +363,8 @@ __global__ void __launch_bounds__(kProtoThreads) k_verify_prep(DecodeStateDev s,
 // target's valid KV length is prompt_len + committed_pos - 1 and the draft's
 // is tracked in kvd, so rejected rows are simply overwritten next time.
 __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, BatchDev bt) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ long long s_tv;
   CtrlDev& c = *s.ctrl;
   const int mode = c.mode;
@@ -473,6 +487,8 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
 
 // host-free round budget: stop after `extra` more rounds
 __global__ void k_set_round_limit(DecodeStateDev s, int extra) {
+  pdl_wait();
+  pdl_trigger();
   CtrlDev& c = *s.ctrl;
   const long long lim = (long long)c.round + extra;
   c.round_limit = lim > 0x7fffffff ? 0x7fffffff : (int)lim;
@@ -481,45 +497,39 @@ __global__ void k_set_round_limit(DecodeStateDev s, int extra) {
 
 // ------------------------------------------------------------------ launchers
 int launch_set_round_limit(const DecodeStateDev& st, int extra, cudaStream_t s) {
-  k_set_round_limit<<<1, 1, 0, s>>>(st, extra);
-  SPECTRE_LAUNCH_CHECK("k_set_round_limit");
+  SPECTRE_LAUNCH_PDL("k_set_round_limit", k_set_round_limit, dim3(1), dim3(1), 0, s, st, extra);
   return SPECTRE_OK;
 }
 int launch_prefill_batch(const int* prompts, int prompt_len, int n_req, int c0, int cs,
                          const BatchDev& bt, cudaStream_t s) {
-  k_prefill_batch<<<(n_req + 255) / 256, 256, 0, s>>>(prompts, prompt_len, n_req, c0, cs, bt);
-  SPECTRE_LAUNCH_CHECK("k_prefill_batch");
+  SPECTRE_LAUNCH_PDL("k_prefill_batch", k_prefill_batch, dim3((n_req + 255) / 256), dim3(256), 0, s,
+                     prompts, prompt_len, n_req, c0, cs, bt);
   return SPECTRE_OK;
 }
 int launch_admit(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s) {
-  k_admit<<<(st.n_req + 255) / 256, 256, 0, s>>>(st, bt);
-  SPECTRE_LAUNCH_CHECK("k_admit");
+  SPECTRE_LAUNCH_PDL("k_admit", k_admit, dim3((st.n_req + 255) / 256), dim3(256), 0, s, st, bt);
   return SPECTRE_OK;
 }
 int launch_round_begin(const DecodeStateDev& st, cudaStream_t s) {
-  k_round_begin<<<1, 32, 0, s>>>(st);
-  SPECTRE_LAUNCH_CHECK("k_round_begin");
+  SPECTRE_LAUNCH_PDL("k_round_begin", k_round_begin, dim3(1), dim3(32), 0, s, st);
   return SPECTRE_OK;
 }
 int launch_draft_prep(const DecodeStateDev& st, const BatchDev& bt, int which, cudaStream_t s) {
-  k_draft_prep<<<1, kProtoThreads, 0, s>>>(st, bt, which);
-  SPECTRE_LAUNCH_CHECK("k_draft_prep");
+  SPECTRE_LAUNCH_PDL("k_draft_prep", k_draft_prep, dim3(1), dim3(kProtoThreads), 0, s, st, bt, which);
   return SPECTRE_OK;
 }
 int launch_draft_append(const DecodeStateDev& st, const BatchDev& bt, int which, int last,
                         cudaStream_t s) {
-  k_draft_append<<<1, kProtoThreads, 0, s>>>(st, bt, which, last);
-  SPECTRE_LAUNCH_CHECK("k_draft_append");
+  SPECTRE_LAUNCH_PDL("k_draft_append", k_draft_append, dim3(1), dim3(kProtoThreads), 0, s, st, bt,
+                     which, last);
   return SPECTRE_OK;
 }
 int launch_verify_prep(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s) {
-  k_verify_prep<<<1, kProtoThreads, 0, s>>>(st, bt);
-  SPECTRE_LAUNCH_CHECK("k_verify_prep");
+  SPECTRE_LAUNCH_PDL("k_verify_prep", k_verify_prep, dim3(1), dim3(kProtoThreads), 0, s, st, bt);
   return SPECTRE_OK;
 }
 int launch_accept(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s) {
-  k_accept<<<1, kProtoThreads, 0, s>>>(st, bt);
-  SPECTRE_LAUNCH_CHECK("k_accept");
+  SPECTRE_LAUNCH_PDL("k_accept", k_accept, dim3(1), dim3(kProtoThreads), 0, s, st, bt);
   return SPECTRE_OK;
 }
 

@@ -140,6 +140,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// UMMA shared-memory descriptor, K-major, rows of kRowBytes (= swizzle span:
+// 128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B), 8-row atoms kRowBytes*8 apart.
+template <int kRowBytes>
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);              // start address
+  d |= (uint64_t)((kRowBytes * 8) >> 4) << 32;              // SBO: one 8-row atom
+  d |= (uint64_t)1 << 46;                                   // descriptor version (sm_100)
+  d |= (uint64_t)(kRowBytes == 128 ? 2 : 4) << 61;          // SWIZZLE_128B / SWIZZLE_64B
+  return d;
+}
+
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
   uint64_t d = 0;

@@ -56,12 +56,13 @@ def _ref(torch, X, W, T):
     (320, 320, 1024, 4096, 4), (512, 512, 256, 256, 1), (130, 192, 768, 1024, 1),
     (700, 768, 384, 512, 2), (1280, 1280, 256, 1024, 1), (300, 320, 640, 2048, 3),
     (256, 256, 28672 // 8, 4096, 1), (77, 128, 1000, 640, 2)])
-def test_partial_matches_fp32(env, T, rows_cap, N, K, splits):
+@pytest.mark.parametrize("bk_flag", [0, -8])   # 0: default BK=32 (SW64), -8: BK=64 (SW128)
+def test_partial_matches_fp32(env, T, rows_cap, N, K, splits, bk_flag):
     torch = env[0]
     g = torch.Generator(device="cuda").manual_seed(T * 7 + N)
     X = torch.randn(rows_cap, K, device="cuda", generator=g).bfloat16()
     W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
-    part, *_ = _run(env, X, W, T, rows_cap, splits)
+    part, *_ = _run(env, X, W, T, rows_cap, splits, max_stages=bk_flag)
     got = part.sum(0)[:T]
     want = _ref(torch, X, W, T)
     scale = (X[:T].float().abs() @ W.float().abs().t()) + 1e-3
