@@ -57,6 +57,12 @@ struct Bump {
 
 static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+static int tile_rows_default(int fallback) {
+  const char* v = getenv("SPECTRE_TILE_ROWS");
+  if (!v) return fallback;
+  return atoi(v) == 128 ? 128 : 256;
+}
+
 static int attn_chunk_default() {
   const char* v = getenv("SPECTRE_ATTN_CHUNK");
   const int c = v ? atoi(v) : 512;
@@ -77,6 +83,7 @@ struct ModelRT {
   SpectreModelWeights w{};
   int n_req = 0, rows_cap = 0, ctx_cap = 0, max_new = 1, split_max = 1, rb_cap = 1;
   int sp_qkv = 1, sp_o = 1, sp_d = 1;
+  int tile_rows = 256;   // weight rows per GEMM CTA (128 for small-T models)
   int attn_chunk = 128;
   float* h = nullptr;
   __nv_bfloat16 *x = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
@@ -94,9 +101,9 @@ struct ModelRT {
   void layout(Bump& b) {
     const int d = dm.d_model, R = rows_cap;
     const int qd = dm.n_q_heads * dm.head_dim;
-    sp_qkv = pick_splits((nqkv() + 255) / 256, d / 64);
-    sp_o = pick_splits((d + 255) / 256, qd / 64);
-    sp_d = pick_splits((d + 255) / 256, dm.ffn / 64);
+    sp_qkv = pick_splits((nqkv() + tile_rows - 1) / tile_rows, d / 64);
+    sp_o = pick_splits((d + tile_rows - 1) / tile_rows, qd / 64);
+    sp_d = pick_splits((d + tile_rows - 1) / tile_rows, dm.ffn / 64);
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
     attn_chunk = attn_chunk_default();
     split_max = (ctx_cap + attn_chunk - 1) / attn_chunk;
@@ -135,18 +142,22 @@ struct ModelRT {
     pd.resize(L);
     for (int l = 0; l < L; ++l) {
       TRY(gemm_plan(&pq[l], bf(w.wqkv) + (size_t)l * nqkv() * d, nqkv(), d, x, rows_cap,
-                    kPartial, sp_qkv));
+                    kPartial, sp_qkv, 0, 0, tile_rows));
       TRY(gemm_plan(&po[l], bf(w.wo) + (size_t)l * d * qd, d, qd, attn, rows_cap, kPartial,
-                    sp_o));
+                    sp_o, 0, 0, tile_rows));
+      // SwiGLU cannot split K: use 128-row tiles when that still fits one wave
+      const int gu_tiles = (2 * F + 255) / 256;
+      const int gu_rows = (tile_rows == 128 || 2 * gu_tiles <= 148) ? 128 : 256;
       TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
-                    1));
-      TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d));
+                    1, 0, 0, gu_rows));
+      TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
+                    0, 0, tile_rows));
       for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) p->args.part = part;
       pgu[l].args.act = act;
       pgu[l].args.ld_act = F;
       for (GemmPlan* p : {&pq[l], &po[l], &pgu[l], &pd[l]}) p->args.t_dev = bt.t_dev;
     }
-    TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1));
+    TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, tile_rows));
     plm.args.amax_val = amax_v;
     plm.args.amax_idx = amax_i;
     plm.args.t_dev = bt.t_dev;
@@ -304,6 +315,8 @@ struct Engine {
     drf.rows_cap = rd;
     drf.ctx_cap = c.ctx_cap;
     drf.max_new = std::max(draft_new_max, prefill_cs);
+    drf.tile_rows = tile_rows_default(256);
+    tgt.tile_rows = tile_rows_default(256);
     st.n_req = c.n_req;
     st.gamma = c.gamma;
     st.out_len = c.output_len;

@@ -75,7 +75,8 @@ int gemm_default_bk() {
 }
 
 int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_cap, int epi,
-              int splits, int max_stages, int bk) {
+              int splits, int max_stages, int bk, int tile_rows) {
+  if (tile_rows != 128) tile_rows = 256;
   if (bk == 0) bk = gemm_default_bk();
   if (bk != 32 && bk != 64) return arg_fail("gemm_plan: bk must be 32 or 64");
   if (N < 1 || K < 64 || K % 64 || rows_cap < 64 || rows_cap % 64 || splits < 1)
@@ -86,8 +87,9 @@ int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_
   if (int e = make_tmap_bf16(&p->tmap_w, W, (uint64_t)K, (uint64_t)N, 128, bk)) return e;
   if (int e = make_tmap_bf16(&p->tmap_x, X, (uint64_t)K, (uint64_t)rows_cap, 64, bk)) return e;
   p->bk = bk;
-  const int n_tiles = (N + kGemmTileN - 1) / kGemmTileN;
+  const int n_tiles = (N + tile_rows - 1) / tile_rows;
   p->epi = epi;
+  p->args.tile_rows = tile_rows;
   p->grid = n_tiles * splits;
   p->args.N = N;
   p->args.K = K;
@@ -124,9 +126,12 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
                                  float* amax_val, int32_t* amax_idx, void* act, int32_t ld_act,
                                  int32_t max_stages, void* stream) {
   GemmPlan p;
-  const int bk = max_stages < 0 ? 64 : 0;   // negative max_stages: force 64-wide K blocks
+  // test knobs: max_stages < 0 forces 32-wide K blocks; >= 1000 selects 128-row tiles
+  const int tile_rows = max_stages >= 1000 ? 128 : 256;
+  if (max_stages >= 1000) max_stages -= 1000;
+  const int bk = max_stages < 0 ? 32 : 64;
   if (int e = gemm_plan(&p, W, N, K, X, rows_cap, epilogue, splits,
-                        max_stages < 0 ? -max_stages : max_stages, bk))
+                        max_stages < 0 ? -max_stages : max_stages, bk, tile_rows))
     return e;
   p.args.t_dev = t_dev;
   p.args.t_static = t_static;

@@ -14,7 +14,7 @@ struct GemmPlan {
   GemmArgs args;
   int grid = 0;
   int epi = 0;
-  int n_tiles = 0;        // 256-row weight tiles
+  int n_tiles = 0;        // weight tiles (args.tile_rows rows each)
   int n_amax_blocks = 0;  // 32-row argmax partial blocks
   int bk = 32;            // K per pipeline stage (32: 64B swizzle, 64: 128B swizzle)
 };
@@ -23,7 +23,7 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t out
                    uint32_t box_outer, uint32_t box_inner = 64);
 // W: [N][K] bf16, X: [rows_cap][K] bf16.  Output pointers are filled by the caller.
 int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_cap, int epi,
-              int splits, int max_stages = 0, int bk = 0);
+              int splits, int max_stages = 0, int bk = 0, int tile_rows = 256);
 int gemm_run(const GemmPlan& p, cudaStream_t s);
 
 }  // namespace spectre

@@ -49,6 +49,7 @@ struct GemmArgs {
   int t_static;
   int splits;               // split-K factor
   int max_stages;           // cap on pipeline depth (tests / tuning)
+  int tile_rows;            // weight rows per CTA: 256 (two accumulators) or 128
   float* part;              // kPartial: [splits][rows_cap][N]
   float* amax_val;          // kArgmax: [ceil(N/32)][rows_cap]
   int* amax_idx;
@@ -64,13 +65,15 @@ struct GemmPhase {
   int t0, nt;    // token rows of this phase
 };
 
-__device__ __forceinline__ int gemm_n_phases(int T) {
-  if (T <= 256) return 1;
-  return 2 * ((T + 511) / 512);
+// Phases of one CTA's work: T <= 256 with a 256-row tile -> one phase, both
+// 128-row boxes per stage; otherwise one phase per (128-row box, 512-token pass).
+__device__ __forceinline__ int gemm_n_phases(int T, int tile_rows) {
+  if (T <= 256 && tile_rows == 256) return 1;
+  return (tile_rows / 128) * ((T + 511) / 512);
 }
-__device__ __forceinline__ GemmPhase gemm_phase(int T, int p) {
+__device__ __forceinline__ GemmPhase gemm_phase(int T, int tile_rows, int p) {
   GemmPhase ph;
-  if (T <= 256) {
+  if (T <= 256 && tile_rows == 256) {
     ph.row_off = 0;
     ph.boxes = 2;
     ph.t0 = 0;
@@ -103,8 +106,9 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   constexpr int kWBox = 128 * kRow;         // one 128-row weight box
   constexpr int kXBox = 64 * kRow;          // one 64-row activation box
   // runtime stage layout: W bytes + X bytes per stage
-  const int w_bytes = (T <= 256) ? 2 * kWBox : kWBox;
-  const int x_rows = (T <= 256) ? ((T + 63) & ~63) : min((T + 63) & ~63, 512);
+  const bool wide = (T <= 256 && a.tile_rows == 256);
+  const int w_bytes = wide ? 2 * kWBox : kWBox;
+  const int x_rows = wide ? ((T + 63) & ~63) : min((T + 63) & ~63, 512);
   const int stage_bytes = w_bytes + x_rows * kRow;
   int stages = stage_bytes > 0 ? kGemmPipeBytes / stage_bytes : 1;
   stages = stages > kGemmMaxStages ? kGemmMaxStages : (stages < 1 ? 1 : stages);
@@ -118,15 +122,15 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
   float* scratch = reinterpret_cast<float*>(smem + kGemmPipeBytes + 1024);
 
-  const int n_tiles = (a.N + kGemmTileN - 1) / kGemmTileN;
+  const int n_tiles = (a.N + a.tile_rows - 1) / a.tile_rows;
   const int tile = blockIdx.x % n_tiles;
   const int split = blockIdx.x / n_tiles;
-  const int n0 = tile * kGemmTileN;
+  const int n0 = tile * a.tile_rows;
   const int k_iters_total = a.K / BK;
   const int it_begin = (int)((long long)k_iters_total * split / a.splits);
   const int it_end = (int)((long long)k_iters_total * (split + 1) / a.splits);
   const int n_iters = it_end - it_begin;
-  const int n_phases = gemm_n_phases(T);
+  const int n_phases = gemm_n_phases(T, a.tile_rows);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_w);
@@ -156,7 +160,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       pdl_trigger();
     }
     if (kEpi == kPartial && warp >= 2) {  // K < splits: this split contributes zeros
-      for (int r = threadIdx.x - 64; r < kGemmTileN; r += 256) {
+      for (int r = threadIdx.x - 64; r < a.tile_rows; r += 256) {
         const int n = n0 + r;
         if (n < a.N)
           for (int t = 0; t < T; ++t) a.part[((size_t)split * a.rows_cap + t) * a.N + n] = 0.0f;
@@ -169,7 +173,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       const uint64_t pol_x = policy_evict_last();    // activations are re-read by every tile
       // Weights never change: the first stages' weight tiles are requested
       // before waiting on the previous kernel (its tail overlaps our fill).
-      const GemmPhase ph0 = gemm_phase(T, 0);
+      const GemmPhase ph0 = gemm_phase(T, a.tile_rows, 0);
       const int pre = n_iters < stages ? n_iters : stages;
       {
         const int x_boxes = (ph0.nt + 63) >> 6;
@@ -186,7 +190,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       pdl_trigger();
       int g = 0;
       for (int p = 0; p < n_phases; ++p) {
-        const GemmPhase ph = gemm_phase(T, p);
+        const GemmPhase ph = gemm_phase(T, a.tile_rows, p);
         const int x_boxes = (ph.nt + 63) >> 6;
         const uint32_t tx = (uint32_t)ph.boxes * kWBox + (uint32_t)x_boxes * kXBox;
         for (int i = 0; i < n_iters; ++i, ++g) {
@@ -213,7 +217,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     // ---------------- MMA issuer (one thread)
     int g = 0;
     for (int p = 0; p < n_phases; ++p) {
-      const GemmPhase ph = gemm_phase(T, p);
+      const GemmPhase ph = gemm_phase(T, a.tile_rows, p);
       const int t_pad = (ph.nt + 15) & ~15;
       const int nc0 = t_pad < 256 ? t_pad : 256;
       const int nc1 = t_pad - nc0;
@@ -262,7 +266,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16);
     float* up = scratch + grp * (64 * 17);
     for (int p = 0; p < n_phases; ++p) {
-      const GemmPhase ph = gemm_phase(T, p);
+      const GemmPhase ph = gemm_phase(T, a.tile_rows, p);
       mbar_wait(tmem_full, (uint32_t)p & 1u);
       tc_fence_after();
       const int t_pad = (ph.nt + 15) & ~15;

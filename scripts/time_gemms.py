@@ -22,7 +22,7 @@ for name, N, K, epi, splits, T in SHAPES:
     av = torch.empty((N + 31) // 32, 512, device="cuda")
     ai = torch.empty((N + 31) // 32, 512, dtype=torch.int32, device="cuda")
     act = torch.empty(512, N // 2, dtype=torch.bfloat16, device="cuda")
-    for bk, ms in ((32, 0), (64, -8)):
+    for bk, ms in (("256rows", 0), ("128rows", 1000)):
         ts = []
         for it in range(30):
             W = Ws[it % copies]

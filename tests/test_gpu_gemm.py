@@ -56,7 +56,8 @@ def _ref(torch, X, W, T):
     (320, 320, 1024, 4096, 4), (512, 512, 256, 256, 1), (130, 192, 768, 1024, 1),
     (700, 768, 384, 512, 2), (1280, 1280, 256, 1024, 1), (300, 320, 640, 2048, 3),
     (256, 256, 28672 // 8, 4096, 1), (77, 128, 1000, 640, 2)])
-@pytest.mark.parametrize("bk_flag", [0, -8])   # 0: default BK=32 (SW64), -8: BK=64 (SW128)
+# 0: defaults (BK=64, 256-row tiles); -8: BK=32 (64B swizzle); 1000: 128-row tiles
+@pytest.mark.parametrize("bk_flag", [0, -8, 1000])
 def test_partial_matches_fp32(env, T, rows_cap, N, K, splits, bk_flag):
     torch = env[0]
     g = torch.Generator(device="cuda").manual_seed(T * 7 + N)
@@ -74,7 +75,7 @@ def test_runtime_token_count_and_stage_variants(env):
     X = torch.randn(256, 1024, device="cuda").bfloat16()
     W = (torch.randn(512, 1024, device="cuda") * 0.05).bfloat16()
     want = _ref(torch, X, W, 96)
-    for stages in (1, 2, 3, 8):
+    for stages in (1, 2, 3, 8, 1002):
         t_dev = torch.tensor([96], dtype=torch.int32, device="cuda")
         part, *_ = _run(env, X, W, 0, 256, 2, t_dev=t_dev, max_stages=stages)
         got = part.sum(0)[:96]
@@ -142,6 +143,8 @@ def test_swiglu_epilogue(env):
     # interleave per 64 rows: [g0..g63, u0..u63, g64..g127, u64..u127, ...]
     W = torch.stack([Wg.view(F // 64, 64, K), Wu.view(F // 64, 64, K)], 1).reshape(2 * F, K)
     _, _, _, act = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU)
+    _, _, _, act128 = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU, max_stages=1000)
+    assert torch.equal(act, act128)
     g = _ref(torch, X, Wg, T)
     u = _ref(torch, X, Wu, T)
     want = torch.nn.functional.silu(g) * u
