@@ -23,7 +23,8 @@
 
 namespace spectre {
 
-int launch_attention(const AttnArgs& a, int hd, int mt, cudaStream_t s);
+int launch_attention(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, int hd,
+                     int rows_per_req, cudaStream_t s);
 int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void* E,
                          const float* w, float* h, void* x, int d, float eps, cudaStream_t s);
 int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const int* t_dev,
@@ -65,8 +66,8 @@ static int tile_rows_default(int fallback) {
 
 static int attn_chunk_default() {
   const char* v = getenv("SPECTRE_ATTN_CHUNK");
-  const int c = v ? atoi(v) : 512;
-  return (c == 128 || c == 256 || c == 512) ? c : 512;
+  const int c = v ? atoi(v) : 1024;
+  return (c >= 64 && c % 64 == 0 && c <= 8192) ? c : 1024;
 }
 
 static int pick_splits(int n_tiles, int k_iters) {
@@ -91,6 +92,7 @@ struct ModelRT {
   int* att_cnt = nullptr;
   int* amax_i = nullptr;
   float2* rope = nullptr;
+  CUtensorMap tm_k{}, tm_v{};   // whole K / V cache as [L*slots*n_kv*ctx_cap][hd] rows
   BatchDev bt{};
   std::vector<GemmPlan> pq, po, pgu, pd;
   GemmPlan plm{};
@@ -107,7 +109,8 @@ struct ModelRT {
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
     attn_chunk = attn_chunk_default();
     split_max = (ctx_cap + attn_chunk - 1) / attn_chunk;
-    rb_cap = (max_new * group() + 15) / 16;
+    // m-tiles per request, in whole attention row blocks (2 m-tiles at hd 128, 3 at hd 64)
+    rb_cap = round_up((max_new * group() + 15) / 16, dm.head_dim == 128 ? 2 : 3);
     h = b.take<float>((size_t)R * d);
     x = b.take<__nv_bfloat16>((size_t)R * d);
     q = b.take<__nv_bfloat16>((size_t)R * qd);
@@ -158,6 +161,9 @@ struct ModelRT {
       for (GemmPlan* p : {&pq[l], &po[l], &pgu[l], &pd[l]}) p->args.t_dev = bt.t_dev;
     }
     TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, tile_rows));
+    const uint64_t kv_rows = (uint64_t)L * n_req * dm.n_kv_heads * ctx_cap;
+    TRY(make_tmap_bf16(&tm_k, w.k_cache, dm.head_dim, kv_rows, 64, 64));
+    TRY(make_tmap_bf16(&tm_v, w.v_cache, dm.head_dim, kv_rows, 64, 64));
     plm.args.amax_val = amax_v;
     plm.args.amax_idx = amax_i;
     plm.args.t_dev = bt.t_dev;
@@ -170,7 +176,6 @@ struct ModelRT {
     const int d = dm.d_model, L = dm.n_layers, hd = dm.head_dim;
     const float eps = dm.rms_eps;
     const int rows = new_per_req * group();
-    const int mt = 1;
     AttnArgs a{};
     a.q = q;
     a.q_off = bt.q_off;
@@ -186,6 +191,7 @@ struct ModelRT {
     a.split_max = split_max;
     a.chunk = attn_chunk;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
+    if (const char* dbg = getenv("SPECTRE_ATTN_DEBUG")) a.debug = atoi(dbg);
     a.part_o = att_o;
     a.part_ml = att_ml;
     a.done_cnt = att_cnt;
@@ -199,9 +205,8 @@ struct ModelRT {
       TRY(launch_qkv_rope_kv(part, sp_qkv, rows_cap, bt.t_dev, rows_cap, bt.pos, bt.slot, rope,
                              q, kc + l * kv_layer, vc + l * kv_layer, dm.n_q_heads,
                              dm.n_kv_heads, hd, ctx_cap, s));
-      a.k = kc + l * kv_layer;
-      a.v = vc + l * kv_layer;
-      TRY(launch_attention(a, hd, mt, s));
+      a.layer_row0 = l * n_req * dm.n_kv_heads * ctx_cap;
+      TRY(launch_attention(tm_k, tm_v, a, hd, rows, s));
       TRY(gemm_run(po[l], s));
       TRY(launch_residual_rmsnorm(part, sp_o, rows_cap, bt.t_dev, rows_cap,
                                   w.mlp_norm + (size_t)l * d, h, x, d, eps, s));

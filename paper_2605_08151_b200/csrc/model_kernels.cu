@@ -209,323 +209,6 @@ __global__ void __launch_bounds__(128) k_qkv_rope_kv(const float* __restrict__ p
   }
 }
 
-// ------------------------------------------------------------- attention
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
-                                        uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1,
-                                          uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
-                                         uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-               "r"(valid ? 16 : 0)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// Persistent attention.  A grid of one or more CTAs per SM walks the work
-// items (request, kv head, block of 16 query rows, split of `chunk` keys).
-// Rows are token-major x GQA heads (4 tokens x 4 heads = one 16-row MMA tile
-// for a gamma=4 verify).  Inside an item, warp w of NW owns keys
-// [c0 + w*chunk/NW, +chunk/NW) and streams them in 16-key steps through two
-// cp.async buffers (step i+1 loading while step i runs S = Q K^T, the online
-// softmax and O += P V on mma.sync m16n8k16).  The NW warps merge in a fixed
-// order, write the split's partial, and the last split of a row block to
-// finish merges all splits in split order into the bf16 output.  Chunk / warp
-// / step boundaries are absolute key positions: a token's result does not
-// depend on the rest of the batch.
-template <int HD, int NW>
-__global__ void __launch_bounds__(NW * 32) k_attention(AttnArgs a) {
-  pdl_wait();
-  pdl_trigger();
-  constexpr int ROWS = 16;
-  constexpr int STEP = 16;
-  constexpr int LD = HD + 8;           // padded smem row: conflict-free ldmatrix
-  constexpr int TILE = STEP * LD;      // one K or V step tile (elements)
-  constexpr int NT = NW * 32;
-  extern __shared__ __align__(16) uint8_t smem_attn[];
-  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_attn);
-  __nv_bfloat16* sKV = sQ + ROWS * LD;  // per warp: 2 buffers x (K, V)
-  __shared__ int s_last;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int group = a.n_q / a.n_kv;
-  const int g = lane >> 2, tq = lane & 3;
-  __nv_bfloat16* wbuf = sKV + warp * 4 * TILE;
-  const int n_items = a.n_req * a.n_kv * a.rb_max * a.split_max;
-  const int per_warp = a.chunk / NW;
-
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int split = item % a.split_max;
-    const int rb = (item / a.split_max) % a.rb_max;
-    const int bk = item / (a.split_max * a.rb_max);
-    const int b = bk / a.n_kv, kvh = bk % a.n_kv;
-    const int nn = a.n_new[b];
-    const int rows_total = nn * group;
-    if (rb * ROWS >= rows_total) continue;
-    const int p0 = a.pos0[b];
-    const int c0 = split * a.chunk;
-    const int last_row = min(rows_total, (rb + 1) * ROWS) - 1;
-    const int p_max = p0 + last_row / group;   // largest query position of the block
-    if (c0 > p_max) continue;                  // chunk entirely in the causal future
-    const int kv_len = p0 + nn;
-    const int qoff = a.q_off[b];
-    const size_t kv_base = ((size_t)a.slot[b] * a.n_kv + kvh) * a.ctx_cap;
-
-    for (int c = tid; c < ROWS * (HD / 8); c += NT) {
-      const int r = c / (HD / 8), ch = c % (HD / 8);
-      const int R = rb * ROWS + r;
-      const bool valid = R < rows_total;
-      const int j = valid ? R / group : 0, hh = valid ? R % group : 0;
-      const __nv_bfloat16* src =
-          a.q + (((size_t)(qoff + j) * a.n_q) + kvh * group + hh) * HD + ch * 8;
-      cp_async16(ptx_smem(sQ + r * LD + ch * 8), src, valid);
-    }
-    cp_async_commit();
-
-    const int w0 = c0 + warp * per_warp;
-    const int w_end = min(w0 + per_warp, p_max + 1);
-    const int steps = w_end > w0 ? (w_end - w0 + STEP - 1) / STEP : 0;
-    auto issue = [&](int st) {
-      const int kb = w0 + st * STEP;
-      __nv_bfloat16* sK = wbuf + (st & 1) * 2 * TILE;
-      __nv_bfloat16* sV = sK + TILE;
-#pragma unroll
-      for (int c = lane; c < STEP * (HD / 8); c += 32) {
-        const int r = c / (HD / 8), ch = c % (HD / 8);
-        const bool valid = kb + r < kv_len;
-        const size_t off = (kv_base + (valid ? kb + r : 0)) * HD + ch * 8;
-        cp_async16(ptx_smem(sK + r * LD + ch * 8), a.k + off, valid);
-        cp_async16(ptx_smem(sV + r * LD + ch * 8), a.v + off, valid);
-      }
-      cp_async_commit();
-    };
-    if (steps > 0) issue(0);
-    if (steps > 1) issue(1);
-    if (steps > 1) cp_async_wait<2>();
-    else if (steps > 0) cp_async_wait<1>();
-    else cp_async_wait<0>();
-    __syncthreads();   // Q tile visible to every warp
-
-    float o[HD / 8][4];
-#pragma unroll
-    for (int n = 0; n < HD / 8; ++n)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) o[n][e] = 0.f;
-    float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
-    int qpos[2];
-    bool qvalid[2];
-#pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      const int R = rb * ROWS + g + hr * 8;
-      qvalid[hr] = R < rows_total;
-      qpos[hr] = p0 + (qvalid[hr] ? R / group : 0);
-    }
-
-    // Q fragments stay in registers for the whole item
-    uint32_t qf[HD / 16][4];
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk)
-      ldsm_x4(ptx_smem(sQ + (lane & 15) * LD + kk * 16 + (lane >> 4) * 8), qf[kk][0], qf[kk][1],
-              qf[kk][2], qf[kk][3]);
-
-    for (int st = 0; st < steps; ++st) {
-      if (st + 1 < steps) cp_async_wait<1>();
-      else cp_async_wait<0>();
-      __syncwarp();
-      const int kb = w0 + st * STEP;
-      const __nv_bfloat16* sK = wbuf + (st & 1) * 2 * TILE;
-      const __nv_bfloat16* sV = sK + TILE;
-      // two independent accumulation chains per n-tile (even / odd k-steps)
-      float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-      float t0[4] = {0.f, 0.f, 0.f, 0.f}, t1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        uint32_t b0, b1, b2, b3;
-        const int mi = lane >> 3;
-        ldsm_x4(ptx_smem(sK + ((mi >> 1) * 8 + (lane & 7)) * LD + kk * 16 + (mi & 1) * 8), b0, b1,
-                b2, b3);
-        if (kk & 1) {
-          mma16816(t0, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b0, b1);
-          mma16816(t1, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b2, b3);
-        } else {
-          mma16816(s0, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b0, b1);
-          mma16816(s1, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b2, b3);
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        s0[e] += t0[e];
-        s1[e] += t1[e];
-      }
-      // mask + online softmax (log2 domain); s0: keys kb+2tq+{0,1}, s1: kb+8+2tq+{0,1}
-      float p[2][4];
-#pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        float v[4] = {s0[hr * 2], s0[hr * 2 + 1], s1[hr * 2], s1[hr * 2 + 1]};
-        float mx = -INFINITY;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int key = kb + (e >> 1) * 8 + 2 * tq + (e & 1);
-          v[e] *= a.scale_log2;
-          if (!qvalid[hr] || key > qpos[hr]) v[e] = -INFINITY;
-          mx = fmaxf(mx, v[e]);
-        }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(mrow[hr], mx);
-        const float corr = (m_new == -INFINITY) ? 1.f : exp2f(mrow[hr] - m_new);
-        float rs = 0.f;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          p[hr][e] = (v[e] == -INFINITY) ? 0.f : exp2f(v[e] - m_new);
-          rs += p[hr][e];
-        }
-        rs += __shfl_xor_sync(0xffffffffu, rs, 1);
-        rs += __shfl_xor_sync(0xffffffffu, rs, 2);
-        lrow[hr] = lrow[hr] * corr + rs;
-        mrow[hr] = m_new;
-#pragma unroll
-        for (int n = 0; n < HD / 8; ++n) {
-          o[n][hr * 2] *= corr;
-          o[n][hr * 2 + 1] *= corr;
-        }
-      }
-      // P (A fragment of the 16-key k-step) x V
-      const uint32_t pa0 = pack_bf16(p[0][0], p[0][1]);
-      const uint32_t pa1 = pack_bf16(p[1][0], p[1][1]);
-      const uint32_t pa2 = pack_bf16(p[0][2], p[0][3]);
-      const uint32_t pa3 = pack_bf16(p[1][2], p[1][3]);
-#pragma unroll
-      for (int dp = 0; dp < HD / 16; ++dp) {
-        const int mi = lane >> 3;
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(ptx_smem(sV + ((mi & 1) * 8 + (lane & 7)) * LD + dp * 16 + (mi >> 1) * 8), b0,
-                  b1, b2, b3);
-        mma16816(o[2 * dp], pa0, pa1, pa2, pa3, b0, b1);
-        mma16816(o[2 * dp + 1], pa0, pa1, pa2, pa3, b2, b3);
-      }
-      __syncwarp();
-      if (st + 2 < steps) issue(st + 2);
-    }
-
-    // ---- merge the NW warps in fixed order (reuses the K/V area)
-    __syncthreads();
-    float* sO = reinterpret_cast<float*>(sKV);   // [NW][ROWS][HD]
-    float* sML = sO + NW * ROWS * HD;            // [NW][ROWS][2]
-#pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      const int r = g + hr * 8;
-#pragma unroll
-      for (int n = 0; n < HD / 8; ++n)
-        *reinterpret_cast<float2*>(&sO[(warp * ROWS + r) * HD + n * 8 + 2 * tq]) =
-            make_float2(o[n][hr * 2], o[n][hr * 2 + 1]);
-      if (tq == 0) {
-        sML[(warp * ROWS + r) * 2] = mrow[hr];
-        sML[(warp * ROWS + r) * 2 + 1] = lrow[hr];
-      }
-    }
-    __syncthreads();
-    const size_t pidx = (((size_t)b * a.n_kv + kvh) * a.rb_max + rb) * a.split_max + split;
-    for (int c = tid; c < ROWS * HD / 4; c += NT) {
-      const int r = (c * 4) / HD, dcol = (c * 4) % HD;
-      float M = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) M = fmaxf(M, sML[(w * ROWS + r) * 2]);
-      float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-      float Lsum = 0.f;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const float mw = sML[(w * ROWS + r) * 2];
-        const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-        const float4 v = *reinterpret_cast<const float4*>(&sO[(w * ROWS + r) * HD + dcol]);
-        O.x += v.x * f;
-        O.y += v.y * f;
-        O.z += v.z * f;
-        O.w += v.w * f;
-        Lsum += sML[(w * ROWS + r) * 2 + 1] * f;
-      }
-      *reinterpret_cast<float4*>(&a.part_o[(pidx * ROWS + r) * HD + dcol]) = O;
-      if (dcol == 0) {
-        a.part_ml[(pidx * ROWS + r) * 2] = M;
-        a.part_ml[(pidx * ROWS + r) * 2 + 1] = Lsum;
-      }
-    }
-    // ---- last split of this row block merges all splits in split order
-    __threadfence();
-    __syncthreads();
-    const int n_split = (p_max + 1 + a.chunk - 1) / a.chunk;   // splits with c0 <= p_max
-    if (tid == 0) {
-      int* cnt = a.done_cnt + ((size_t)b * a.n_kv + kvh) * a.rb_max + rb;
-      const int prev = atomicAdd(cnt, 1);
-      s_last = (prev == n_split - 1);
-      if (s_last) *cnt = 0;  // self-reset for the next launch
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      const size_t base = (((size_t)b * a.n_kv + kvh) * a.rb_max + rb) * a.split_max;
-      for (int c = tid; c < ROWS * HD / 4; c += NT) {
-        const int r = (c * 4) / HD, dcol = (c * 4) % HD;
-        const int R = rb * ROWS + r;
-        if (R >= rows_total) continue;
-        const int qp = p0 + R / group;
-        const int ns = min(n_split, qp / a.chunk + 1);
-        float M = -INFINITY;
-        for (int sp = 0; sp < ns; ++sp)
-          M = fmaxf(M, __ldcg(&a.part_ml[((base + sp) * ROWS + r) * 2]));
-        float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-        float Lsum = 0.f;
-        for (int sp = 0; sp < ns; ++sp) {
-          const float ms = __ldcg(&a.part_ml[((base + sp) * ROWS + r) * 2]);
-          const float f = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
-          const float4 v = __ldcg(reinterpret_cast<const float4*>(
-              &a.part_o[((base + sp) * ROWS + r) * HD + dcol]));
-          O.x += v.x * f;
-          O.y += v.y * f;
-          O.z += v.z * f;
-          O.w += v.w * f;
-          Lsum += __ldcg(&a.part_ml[((base + sp) * ROWS + r) * 2 + 1]) * f;
-        }
-        const float inv = 1.f / Lsum;
-        const int j = R / group, hh = R % group;
-        __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(
-            a.out + (((size_t)(qoff + j)) * a.n_q + kvh * group + hh) * HD + dcol);
-        dst[0] = __floats2bfloat162_rn(O.x * inv, O.y * inv);
-        dst[1] = __floats2bfloat162_rn(O.z * inv, O.w * inv);
-      }
-    }
-    __syncthreads();  // smem reused by the next item
-  }
-}
-
 // ------------------------------------------------------------ argmax reduce
 // (max, lowest index) over the lm_head tiles for each token row.
 __global__ void __launch_bounds__(256) k_argmax_reduce(const float* __restrict__ val,
@@ -589,50 +272,6 @@ __global__ void k_rope_table(float2* rope, int ctx_cap, int hd, double theta) {
 }
 
 // ------------------------------------------------------------------ launchers
-template <int HD, int NW>
-static int attn_smem() {
-  constexpr int ld = HD + 8;
-  constexpr int load = (16 * ld + NW * 4 * 16 * ld) * 2;
-  constexpr int merge = 16 * ld * 2 + (NW * 16 * HD + NW * 16 * 2) * 4;
-  return load > merge ? load : merge;
-}
-
-static int num_sms() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
-
-template <int HD, int NW>
-static int launch_attn_t(const AttnArgs& a, cudaStream_t s) {
-  static bool cfg = false;
-  const int smem = attn_smem<HD, NW>();
-  if (!cfg) {
-    SPECTRE_CUDA_TRY(cudaFuncSetAttribute(k_attention<HD, NW>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    cfg = true;
-  }
-  int per_sm = 1;
-  SPECTRE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attention<HD, NW>,
-                                                                 NW * 32, smem));
-  per_sm = std::max(1, per_sm);
-  const int items = a.n_req * a.n_kv * a.rb_max * a.split_max;
-  const int grid = std::min(items, per_sm * num_sms());
-  SPECTRE_LAUNCH_PDL("k_attention", k_attention<HD, NW>, dim3(grid), dim3(NW * 32), smem, s, a);
-  return SPECTRE_OK;
-}
-
-int launch_attention(const AttnArgs& a, int hd, int mt, cudaStream_t s) {
-  (void)mt;  // rows are processed in 16-row blocks (rb_max of them)
-  if (hd == 128) return launch_attn_t<128, 8>(a, s);
-  if (hd == 64) return launch_attn_t<64, 8>(a, s);
-  return arg_fail("attention: head_dim must be 64 or 128");
-}
-
 int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void* E,
                          const float* w, float* h, void* x, int d, float eps, cudaStream_t s) {
   SPECTRE_LAUNCH_PDL("k_embed_rmsnorm", k_embed_rmsnorm, dim3(t_cap), dim3(256), 0, s, tok, t_dev,

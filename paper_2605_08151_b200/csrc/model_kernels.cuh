@@ -15,24 +15,21 @@ namespace spectre {
 
 struct AttnArgs {
   const __nv_bfloat16* q;    // [rows][n_q][hd]
-  const __nv_bfloat16* k;    // layer base [n_slots][n_kv][ctx_cap][hd]
-  const __nv_bfloat16* v;
   const int* q_off;          // [n_req]
   const int* n_new;          // [n_req]
   const int* pos0;           // [n_req]
   const int* slot;           // [n_req] KV slot
   int n_req, n_q, n_kv, ctx_cap;
-  int rb_max, split_max;
-  int chunk;                 // keys per CTA (multiple of 128: 4 warps x 32-key steps)
+  int layer_row0;            // first cache row of this layer in the K/V tensor maps
+  int rb_max, split_max;     // 16-row m-tiles per request, key splits per request
+  int chunk;                 // keys per split (multiple of 64)
   float scale_log2;          // hd^-0.5 * log2(e)
   float* part_o;             // [n_req][n_kv][rb_max][split_max][rows_blk][hd]
   float* part_ml;            // [n_req][n_kv][rb_max][split_max][rows_blk][2]
   int* done_cnt;             // [n_req][n_kv][rb_max] split arrivals (self-resetting)
   __nv_bfloat16* out;        // [rows][n_q][hd]
+  int debug;                 // diagnostics: 1 skip math, 2 skip merge (timing only)
 };
 
-constexpr int kAttnChunkMax = 512;  // largest keys-per-CTA (split) supported
-constexpr int kAttnSub = 32;      // keys per warp iteration
-constexpr int kAttnThreads = 128;
 
 }  // namespace spectre

@@ -135,3 +135,49 @@ def test_draft_noise_controls_acceptance(M):
         res = M.decode(pair, spec, "ordinary")
         Ls.append(res.report.content_mean_accepted_length)
     assert Ls[0] > Ls[1] > Ls[2] >= 1.0
+
+
+@pytest.mark.parametrize("chunk", [8, 12])
+@pytest.mark.parametrize("attn_split", [128, 1024])
+def test_long_context_forward_vs_fp32_reference(M, chunk, attn_split, monkeypatch):
+    """Contexts past several attention key splits, 1-3 m-tiles per item."""
+    import torch
+    monkeypatch.setenv("SPECTRE_ATTN_CHUNK", str(attn_split))
+    from oracle.model_ref import reference_forward
+    n, P = 3, 600
+    pair = M.build_pair(M.SMALL_TARGET, M.SMALL_DRAFT, n_req=n, ctx_cap=704, seed=11,
+                        target_branch=1.0, draft_branch=1.0)
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=32, prompt_len=P, seed=11)
+    eng = M.SpectreEngine(pair, spec, "hybrid")
+    prompts = M.synthetic_prompts(n, P, M.SMALL_TARGET.vocab, seed=11)
+    # the target's packed batch holds <= 8 new tokens per request, the draft's 12
+    models = ((0, pair.target), (1, pair.draft)) if chunk <= 8 else ((1, pair.draft),)
+    for which, w in models:
+        toks, xs = _forward_chunks(eng, which, prompts, chunk)
+        for r in range(n):
+            x_ref, logits = reference_forward(w, prompts[r])
+            dx = (xs[r].float() - x_ref).abs()
+            assert dx.max().item() <= X_RTOL * x_ref.pow(2).mean().sqrt().item() * 8
+            assert dx.mean().item() <= X_RTOL * x_ref.abs().mean().item()
+            top2 = logits.topk(2, -1).values
+            clear = (top2[:, 0] - top2[:, 1]) > MARGIN
+            assert torch.equal(toks[r][clear].long(), logits.argmax(-1)[clear])
+
+
+@pytest.mark.parametrize("which", [0, 1])
+@pytest.mark.parametrize("attn_split", [128, 1024])
+def test_long_context_batch_invariance(M, which, attn_split, monkeypatch):
+    """Verify-shaped (5 / 12 new tokens) and one-token passes agree bit for bit
+    across attention split boundaries."""
+    import torch
+    monkeypatch.setenv("SPECTRE_ATTN_CHUNK", str(attn_split))
+    n, P = 4, 300
+    pair = M.build_pair(M.SMALL_TARGET, M.SMALL_DRAFT, n_req=n, ctx_cap=384, seed=13)
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=32, prompt_len=P, seed=13)
+    eng = M.SpectreEngine(pair, spec, "ar")
+    prompts = M.synthetic_prompts(n, P, M.SMALL_TARGET.vocab, seed=13)
+    ref_tok, ref_x = _forward_chunks(eng, which, prompts, 1)
+    for chunk in ((5, 8) if which == 0 else (5, 12)):
+        tok, x = _forward_chunks(eng, which, prompts, chunk)
+        assert torch.equal(tok, ref_tok), chunk
+        assert torch.equal(x, ref_x), chunk
