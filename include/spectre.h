@@ -153,10 +153,12 @@ int spectre_oracle_run(const SpectreOracleConfig* cfg, const double* arrivals,
  * Y[t, n] = sum_k X[t, k] W[n, k]; X [rows_cap, K] bf16, W [N, K] bf16.
  * The token count is t_dev[0] when t_dev != NULL (graph-capturable), else
  * t_static.  epilogue 0: fp32 split-K partials [splits][rows_cap][N];
- * 1: per-128-row-tile (max, argmax) [ceil(N/128)][rows_cap] (lm_head greedy);
- * 2: SwiGLU over 64-row-interleaved gate/up weights -> act [rows_cap][ld_act]
- * bf16.  Exposed for unit tests and the roofline bench; the engine calls the
+ * 1: (max, argmax) partials [spectre_gemm_argmax_blocks(N, K)][rows_cap]
+ * (lm_head greedy; reduce over the first dimension, lowest index on ties);
+ * 2: SwiGLU over row-pair-interleaved gate/up weights [g0, u0, g1, u1, ...]
+ * -> act [rows_cap][ld_act] bf16.  Exposed for unit tests and the roofline bench; the engine calls the
  * same kernels internally. */
+int32_t spectre_gemm_argmax_blocks(int32_t N, int32_t K);
 int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_dev, int32_t t_static,
                       int32_t rows_cap, int32_t N, int32_t K, int32_t splits,
                       int32_t epilogue, float* partial, float* amax_val, int32_t* amax_idx,
@@ -188,7 +190,7 @@ typedef struct SpectreModelWeights {
   const void* wqkv;         /* [L][(nq + 2 nkv) hd][d] bf16 */
   const void* wo;           /* [L][d][nq hd] bf16 */
   const float* mlp_norm;    /* [L][d] */
-  const void* wgu;          /* [L][2 ffn][d] bf16, 64-row gate/up interleave */
+  const void* wgu;          /* [L][2 ffn][d] bf16, row-pair gate/up interleave */
   const void* wd;           /* [L][d][ffn] bf16 */
   const float* final_norm;  /* [d] */
   const void* lm_head;      /* [vocab][d] bf16 */

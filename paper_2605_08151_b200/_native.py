@@ -122,6 +122,7 @@ def _bind_model(L) -> None:
     i32, i64 = C.c_int32, C.c_int64
     _sig(L, "spectre_gemm_bf16", C.c_int,
          [_P, _P, _P, i32, i32, i32, i32, i32, i32, _P, _P, _P, _P, i32, i32, _P])
+    _sig(L, "spectre_gemm_argmax_blocks", i32, [i32, i32])
     _sig(L, "spectre_engine_workspace_bytes", C.c_size_t,
          [C.POINTER(ModelDims), C.POINTER(ModelDims), C.POINTER(DecodeConfig)])
     _sig(L, "spectre_engine_create", C.c_void_p,

@@ -1,0 +1,118 @@
+// diag_stream.cu — diagnostics: per-SM streaming rate of the data-movement
+// engines the hot kernels use (timing only; not on the decode path).
+//   mode 0: 2-D TMA boxes {64 el, 128 rows} of a [rows][K] bf16 matrix (GEMM weights)
+//   mode 1: 1-D cp.async.bulk of `stage_bytes` contiguous bytes
+//   mode 2: 2-D TMA boxes {64 el, 256 rows}
+// One CTA per SM, one producer lane keeping `stages` stages in flight, one
+// consumer warp releasing them.  Each CTA streams its own contiguous share.
+#include <cuda.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "gemm.h"
+#include "ptx.cuh"
+
+namespace spectre {
+
+__global__ void __launch_bounds__(64, 1)
+k_diag_stream(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tx,
+              const uint8_t* src, size_t bytes_per_cta, int mode, int stages, int stage_bytes,
+              int K, int rows_per_cta, int x_boxes, int stagger) {
+  using namespace ptx;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);   // X boxes at +4096
+  uint64_t* empty = full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int n = (int)(bytes_per_cta / stage_bytes);
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const int kb = K / 64;                        // 64-element k blocks per row
+      const int box_rows = mode == 2 ? 256 : 128;
+      for (int g = 0; g < n; ++g) {
+        const int s = g % stages;
+        if (g >= stages) mbar_wait(&empty[s], (uint32_t)((g / stages) - 1) & 1u);
+        uint8_t* st = smem + s * stage_bytes;
+        mbar_arrive_expect_tx(&full[s], stage_bytes + x_boxes * 8192);
+        if (x_boxes) {   // shared activation boxes (same for every CTA) at this k block
+          const int kx = stagger ? (g + blockIdx.x * 7) % kb : g % kb;
+          for (int b = 0; b < x_boxes; ++b)
+            tma_load_2d(smem + stages * stage_bytes + 4096 + (s * x_boxes + b) * 8192, &tx,
+                        &full[s], kx * 64, b * 64, policy_evict_last());
+        }
+        if (mode == 1) {
+          bulk_load(st, src + (size_t)blockIdx.x * bytes_per_cta + (size_t)g * stage_bytes,
+                    stage_bytes, &full[s]);
+        } else {
+          // stage = stage_bytes / (box_rows*128) boxes walking k then rows (GEMM order)
+          // GEMM order: a stage = the same 64-element k block of `boxes` row boxes
+          const int boxes = stage_bytes / (box_rows * 128);
+          const int kblk = g % kb, rg = g / kb;
+          for (int b = 0; b < boxes; ++b)
+            tma_load_2d(st + b * box_rows * 128, &tm, &full[s], kblk * 64,
+                        blockIdx.x * rows_per_cta + (rg * boxes + b) * box_rows, pol);
+        }
+      }
+    }
+  } else {
+    for (int g = 0; g < n; ++g) {
+      const int s = g % stages;
+      mbar_wait(&full[s], (uint32_t)(g / stages) & 1u);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+}
+
+}  // namespace spectre
+
+using namespace spectre;
+
+// Streams `bytes_per_cta` per CTA over `grid` CTAs; returns elapsed ms via events.
+extern "C" int spectre_diag_stream(const void* buf, int64_t bytes_per_cta, int32_t grid,
+                                   int32_t mode, int32_t stages, int32_t stage_bytes, int32_t K,
+                                   int32_t x_boxes, int32_t stagger, const void* xbuf,
+                                   float* ms_out, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  CUtensorMap tm{};
+  const int box_rows = mode == 2 ? 256 : 128;
+  const int rows_per_cta = (int)(bytes_per_cta / (K * 2));
+  if (mode != 1) {
+    if (int e = make_tmap_bf16(&tm, buf, (uint64_t)K, (uint64_t)rows_per_cta * grid, box_rows, 64))
+      return e;
+  }
+  if (mode != 1 && stage_bytes % (box_rows * 128)) return arg_fail("diag: stage < box");
+  CUtensorMap tx{};
+  if (x_boxes) {
+    if (int e = make_tmap_bf16(&tx, xbuf, (uint64_t)K, (uint64_t)64 * x_boxes, 64, 64)) return e;
+  }
+  const int smem = stages * stage_bytes + 4096 + stages * x_boxes * 8192 + 1024;
+  if (smem > 232448) return arg_fail("diag: smem");
+  SPECTRE_CUDA_TRY(cudaFuncSetAttribute(k_diag_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        smem));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  k_diag_stream<<<grid, 64, smem, s>>>(tm, tx, reinterpret_cast<const uint8_t*>(buf),
+                                       (size_t)bytes_per_cta, mode, stages, stage_bytes, K,
+                                       rows_per_cta, x_boxes, stagger);
+  cudaEventRecord(e1, s);
+  SPECTRE_CUDA_TRY(cudaEventSynchronize(e1));
+  SPECTRE_LAUNCH_CHECK("k_diag_stream");
+  cudaEventElapsedTime(ms_out, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return SPECTRE_OK;
+}

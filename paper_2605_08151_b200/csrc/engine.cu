@@ -89,6 +89,8 @@ struct ModelRT {
   float* h = nullptr;
   __nv_bfloat16 *x = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
   float *part = nullptr, *att_o = nullptr, *att_ml = nullptr, *amax_v = nullptr;
+  float* sk_part = nullptr;   // stream-K segment partials (SwiGLU / lm_head GEMMs)
+  int* sk_flag = nullptr;
   int* att_cnt = nullptr;
   int* amax_i = nullptr;
   float2* rope = nullptr;
@@ -121,10 +123,12 @@ struct ModelRT {
     att_o = b.take<float>(att_rows * dm.head_dim);
     att_ml = b.take<float>(att_rows * 2);
     att_cnt = b.take<int>((size_t)n_req * dm.n_kv_heads * rb_cap);
-    const int n_blocks = (dm.vocab + 31) / 32;
+    const int n_blocks = gemm_sk_grid() * 8;   // argmax partials: one per CTA epilogue warp
     amax_v = b.take<float>((size_t)n_blocks * R);
     amax_i = b.take<int>((size_t)n_blocks * R);
     rope = b.take<float2>((size_t)ctx_cap * dm.head_dim / 2);
+    sk_part = b.take<float>(gemm_sk_part_floats());
+    sk_flag = b.take<int>(gemm_sk_grid());
     bt.tok = b.take<int>(R);
     bt.pos = b.take<int>(R);
     bt.slot = b.take<int>(R);
@@ -148,11 +152,9 @@ struct ModelRT {
                     kPartial, sp_qkv, 0, 0, tile_rows));
       TRY(gemm_plan(&po[l], bf(w.wo) + (size_t)l * d * qd, d, qd, attn, rows_cap, kPartial,
                     sp_o, 0, 0, tile_rows));
-      // SwiGLU cannot split K: use 128-row tiles when that still fits one wave
-      const int gu_tiles = (2 * F + 255) / 256;
-      const int gu_rows = (tile_rows == 128 || 2 * gu_tiles <= 148) ? 128 : 256;
+      // SwiGLU needs full K per tile: stream-K over every SM
       TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
-                    1, 0, 0, gu_rows));
+                    1, 0, 0, 256, sk_part, sk_flag));
       TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
                     0, 0, tile_rows));
       for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) p->args.part = part;
@@ -160,7 +162,8 @@ struct ModelRT {
       pgu[l].args.ld_act = F;
       for (GemmPlan* p : {&pq[l], &po[l], &pgu[l], &pd[l]}) p->args.t_dev = bt.t_dev;
     }
-    TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, tile_rows));
+    TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, 256, sk_part,
+                  sk_flag));
     const uint64_t kv_rows = (uint64_t)L * n_req * dm.n_kv_heads * ctx_cap;
     TRY(make_tmap_bf16(&tm_k, w.k_cache, dm.head_dim, kv_rows, 64, 64));
     TRY(make_tmap_bf16(&tm_v, w.v_cache, dm.head_dim, kv_rows, 64, 64));

@@ -1,7 +1,10 @@
 // gemm.cu — host side of the tcgen05 GEMM: TMA descriptors, planning, launch.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <cstdio>
+#include <vector>
 #include <mutex>
 
 #include "common.cuh"
@@ -61,8 +64,8 @@ static int launch_one(const GemmPlan& p, cudaStream_t s) {
                                           kGemmSmemBytes));
     configured = true;
   }
-  SPECTRE_LAUNCH_PDL("gemm_bf16_swapab", kern, dim3(p.grid), dim3(kGemmThreads), kGemmSmemBytes, s,
-                     p.tmap_w, p.tmap_x, p.args);
+  SPECTRE_LAUNCH_PDL("gemm_bf16_swapab", kern, dim3(p.grid), dim3(kGemmThreads), kGemmSmemBytes,
+                     s, p.tmap_w, p.tmap_x, p.args);
   return SPECTRE_OK;
 }
 
@@ -74,14 +77,27 @@ int gemm_default_bk() {
   return bk;
 }
 
+static int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+size_t gemm_sk_part_floats() { return (size_t)num_sms() * 256 * 256; }
+int gemm_sk_grid() { return num_sms(); }
+
 int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_cap, int epi,
-              int splits, int max_stages, int bk, int tile_rows) {
+              int splits, int max_stages, int bk, int tile_rows, float* sk_part, int* sk_flag) {
   if (tile_rows != 128) tile_rows = 256;
   if (bk == 0) bk = gemm_default_bk();
   if (bk != 32 && bk != 64) return arg_fail("gemm_plan: bk must be 32 or 64");
   if (N < 1 || K < 64 || K % 64 || rows_cap < 64 || rows_cap % 64 || splits < 1)
     return arg_fail("gemm_plan: shape (K % 64, rows_cap multiple of 64)");
-  if (epi == kSwiGLU && (N % 128 || splits != 1)) return arg_fail("gemm_plan: swiglu shape");
+  if (epi == kSwiGLU && (N % 2 || splits != 1)) return arg_fail("gemm_plan: swiglu shape");
   if (epi == kArgmax && splits != 1) return arg_fail("gemm_plan: argmax needs splits == 1");
   *p = GemmPlan{};
   if (int e = make_tmap_bf16(&p->tmap_w, W, (uint64_t)K, (uint64_t)N, 128, bk)) return e;
@@ -90,14 +106,23 @@ int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_
   const int n_tiles = (N + tile_rows - 1) / tile_rows;
   p->epi = epi;
   p->args.tile_rows = tile_rows;
-  p->grid = n_tiles * splits;
+  // persistent: at most one CTA per SM.  Full-K epilogues with a stream-K
+  // workspace partition the iteration space over every SM (T <= 256).
+  // stream-K only when every CTA owns >= a quarter of a tile's iterations
+  // (a tile then spans <= 5 CTAs: the owner's fix-up stays short)
+  const int k_iters = K / bk, total_iters = n_tiles * k_iters;
+  p->args.stream_k = (epi != kPartial && sk_part && sk_flag && tile_rows == 256 &&
+                      total_iters >= num_sms() * std::max(4, k_iters / 4)) ? 1 : 0;
+  p->args.sk_part = sk_part;
+  p->args.sk_flag = sk_flag;
+  p->grid = p->args.stream_k ? num_sms() : std::min(n_tiles * splits, num_sms());
   p->args.N = N;
   p->args.K = K;
   p->args.rows_cap = rows_cap;
   p->args.splits = splits;
   p->args.max_stages = max_stages;
   p->n_tiles = n_tiles;
-  p->n_amax_blocks = (N + 31) / 32;
+  p->n_amax_blocks = p->grid * 8;   // one (max, index) partial per CTA epilogue warp
   return SPECTRE_OK;
 }
 
@@ -120,18 +145,49 @@ int gemm_run(const GemmPlan& p, cudaStream_t s) {
 
 using namespace spectre;
 
+// stream-K workspace for the C-ABI entry point (tests, roofline bench)
+static float* g_sk_part = nullptr;
+static int* g_sk_flag = nullptr;
+static int sk_workspace(float** part, int** flag) {
+  if (!g_sk_part) {
+    SPECTRE_CUDA_TRY(cudaMalloc(&g_sk_part, gemm_sk_part_floats() * sizeof(float)));
+    SPECTRE_CUDA_TRY(cudaMalloc(&g_sk_flag, gemm_sk_grid() * sizeof(int)));
+    SPECTRE_CUDA_TRY(cudaMemset(g_sk_flag, 0, gemm_sk_grid() * sizeof(int)));
+  }
+  *part = g_sk_part;
+  *flag = g_sk_flag;
+  return SPECTRE_OK;
+}
+
+// Partial (max, index) rows the argmax epilogue writes for an [N, K] weight.
+extern "C" int32_t spectre_gemm_argmax_blocks(int32_t N, int32_t K) {
+  (void)N;
+  (void)K;
+  return gemm_sk_grid() * 8;
+}
+
 extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_dev,
                                  int32_t t_static, int32_t rows_cap, int32_t N, int32_t K,
                                  int32_t splits, int32_t epilogue, float* partial,
                                  float* amax_val, int32_t* amax_idx, void* act, int32_t ld_act,
                                  int32_t max_stages, void* stream) {
   GemmPlan p;
-  // test knobs: max_stages < 0 forces 32-wide K blocks; >= 1000 selects 128-row tiles
+  // test knobs: max_stages < 0 forces 32-wide K blocks; >= 2000 disables stream-K;
+  // >= 1000 selects 128-row tiles
+  bool sk = true;
+  if (max_stages >= 2000) {
+    sk = false;
+    max_stages -= 2000;
+  }
   const int tile_rows = max_stages >= 1000 ? 128 : 256;
   if (max_stages >= 1000) max_stages -= 1000;
   const int bk = max_stages < 0 ? 32 : 64;
+  float* skp = nullptr;
+  int* skf = nullptr;
+  if (sk)
+    if (int e = sk_workspace(&skp, &skf)) return e;
   if (int e = gemm_plan(&p, W, N, K, X, rows_cap, epilogue, splits,
-                        max_stages < 0 ? -max_stages : max_stages, bk, tile_rows))
+                        max_stages < 0 ? -max_stages : max_stages, bk, tile_rows, skp, skf))
     return e;
   p.args.t_dev = t_dev;
   p.args.t_static = t_static;
@@ -140,5 +196,25 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
   p.args.amax_idx = amax_idx;
   p.args.act = reinterpret_cast<__nv_bfloat16*>(act);
   p.args.ld_act = ld_act;
+  if (const char* dg = getenv("SPECTRE_GEMM_DIAG")) p.args.diag = atoi(dg);
+  static unsigned long long* dbg = nullptr;
+  if (getenv("SPECTRE_GEMM_DBG")) {
+    if (!dbg) SPECTRE_CUDA_TRY(cudaMalloc(&dbg, 148 * 8 * 8));
+    SPECTRE_CUDA_TRY(cudaMemsetAsync(dbg, 0, 148 * 8 * 8, as_stream(stream)));
+    p.args.dbg = dbg;
+    int r = gemm_run(p, as_stream(stream));
+    std::vector<unsigned long long> h(148 * 8);
+    SPECTRE_CUDA_TRY(cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, as_stream(stream)));
+    SPECTRE_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+    unsigned long long t0 = ~0ull;
+    for (int c = 0; c < p.grid; ++c) if (h[c * 8] && h[c * 8] < t0) t0 = h[c * 8];
+    for (int c = 0; c < p.grid; ++c) {
+      printf("cta %3d start %7.2f", c, (h[c * 8] - t0) * 1e-3);
+      for (int k = 1; k < 6; ++k) if (h[c * 8 + k]) printf("  j%d(r%llu) %7.2f", k - 1, h[c*8+k] >> 62, ((h[c * 8 + k] & ((1ull << 62) - 1)) - t0) * 1e-3);
+      printf("  mma0done %7.2f  pollok %7.2f\n", (h[c * 8 + 7] - t0) * 1e-3, h[c*8+6] ? (h[c * 8 + 6] - t0) * 1e-3 : -1.0);
+    }
+    fflush(stdout);
+    return r;
+  }
   return gemm_run(p, as_stream(stream));
 }

@@ -15,15 +15,20 @@ struct GemmPlan {
   int grid = 0;
   int epi = 0;
   int n_tiles = 0;        // weight tiles (args.tile_rows rows each)
-  int n_amax_blocks = 0;  // 32-row argmax partial blocks
+  int n_amax_blocks = 0;  // argmax partial rows (grid * 8 epilogue warps)
   int bk = 32;            // K per pipeline stage (32: 64B swizzle, 64: 128B swizzle)
 };
 
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
                    uint32_t box_outer, uint32_t box_inner = 64);
 // W: [N][K] bf16, X: [rows_cap][K] bf16.  Output pointers are filled by the caller.
+// sk_part / sk_flag: stream-K workspace (gemm_sk_part_floats() floats, gemm_sk_grid()
+// zeroed ints) for full-K epilogues; nullptr keeps one CTA per tile.
 int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_cap, int epi,
-              int splits, int max_stages = 0, int bk = 0, int tile_rows = 256);
+              int splits, int max_stages = 0, int bk = 0, int tile_rows = 256,
+              float* sk_part = nullptr, int* sk_flag = nullptr);
+size_t gemm_sk_part_floats();
+int gemm_sk_grid();
 int gemm_run(const GemmPlan& p, cudaStream_t s);
 
 }  // namespace spectre

@@ -1,25 +1,40 @@
-// gemm_tcgen05.cuh — weight-streaming GEMM for the verify / draft forward passes.
+// gemm_tcgen05.cuh — persistent weight-streaming GEMM for the verify / draft
+// forward passes.
 //
 //   Y[t, n] = sum_k X[t, k] * W[n, k]        X: [T, K] bf16, W: [N, K] bf16 (both K-major)
 //
 // Decode-shaped: N (weights) is large and streamed once from HBM; T (tokens:
 // B*gamma on the target, ~B on the draft) is small and known only on the
 // device.  The MMA is issued "swap-AB": UMMA_M = 128 weight rows, UMMA_N = T.
-// One CTA owns a 256-row weight tile and a K range (split-K):
-//   T <= 256 : one phase, two 128x(T) accumulators in TMEM (cols 0 / 256),
-//              every X stage feeds both -> X is read from L2 once per 256 W rows
-//   T  > 256 : per 128-row half, N = up to 512 tokens in two MMA chunks
-// The pipeline depth is chosen at run time from T (small T -> up to 8
-// stages in flight), so one launch configuration serves the gamma-token
-// verify pass, 1-token draft steps and prefill chunks (CUDA-graph friendly).
+// A tile is 256 weight rows (two TMEM accumulators share every activation
+// stage, so X is read from L2 once per 256 W rows) or 128.
+//
+// Persistent: one CTA per SM walks a static schedule of accumulation jobs.
+//   * stream-K (full-K epilogues, T <= 256): the n_tiles x K/BK iteration
+//     space is cut into equal contiguous ranges, one per CTA, so every SM
+//     streams the same number of weight bytes whatever N is (no wave
+//     quantisation).  A tile cut by a range boundary is finished by its HEAD
+//     owner (the CTA holding k = 0, which reaches it last in time): it adds
+//     the fp32 partials of the tile's later segments (each the first
+//     segment of the next CTAs) in k order, then runs the epilogue.  The cut
+//     points depend only on (N, K, grid), never on T: results stay bit-
+//     identical for any token count.
+//   * split-K units (partial epilogue) / whole tiles (T > 256, prefill).
+// TMEM accumulators are double-buffered whenever two fit (T <= 128 with
+// 256-row tiles), so one job's epilogue overlaps the next job's MMAs, and the
+// TMA ring runs across job boundaries.  The first stages' weight tiles are
+// requested before griddepcontrol.wait (PDL): the weight stream starts while
+// the previous kernel drains.
 // Warp roles: warp 0 TMA producer, warp 1 TMEM allocator + single-thread
 // tcgen05.mma issuer, warps 2..9 epilogue (tcgen05.ld -> fused epilogue).
 // Epilogues:
 //   kPartial  fp32 split-K partials [split][t][n]; the consumer reduces them
 //             in a fixed order (deterministic, batch invariant)
-//   kArgmax   (max, lowest index) per 32-row block and token: lm_head greedy
-//             decoding without materialising logits
-//   kSwiGLU   weight rows interleaved [64 gate | 64 up]: a = silu(g) * u (bf16)
+//   kArgmax   (max, lowest index) per (CTA, epilogue warp) and token over every
+//             weight row the warp saw: lm_head greedy decoding without
+//             materialising logits ([grid * 8][rows_cap] partials)
+//   kSwiGLU   weight rows interleaved per pair [gate_i, up_i]: a = silu(g) * u
+//             (bf16), combined with one shuffle (no shared-memory exchange)
 #pragma once
 
 #include <cuda.h>
@@ -34,12 +49,10 @@ namespace spectre {
 enum GemmEpilogue : int { kPartial = 0, kArgmax = 1, kSwiGLU = 2 };
 
 constexpr int kGemmThreads = 320;      // 2 control warps + 8 epilogue warps
-constexpr int kGemmTileN = 256;        // weight rows per CTA
-// K per pipeline stage is a template parameter: 64 (128-byte swizzle rows) or
-// 32 (64-byte rows: half-size stages -> twice as many in flight).
+constexpr int kGemmTileN = 256;        // weight rows per CTA tile
 constexpr int kGemmMaxStages = 8;
 constexpr int kGemmSmemBytes = 232448; // dynamic smem requested at launch
-constexpr int kGemmScratch = 2 * 64 * 17 * 4 + 1024;
+constexpr int kGemmScratch = 1024;
 constexpr int kGemmPipeBytes = kGemmSmemBytes - 1024 - 1024 - kGemmScratch;
 
 struct GemmArgs {
@@ -47,46 +60,112 @@ struct GemmArgs {
   int rows_cap;             // X buffer rows (multiple of 64)
   const int* t_dev;         // runtime token count (nullptr: use t_static)
   int t_static;
-  int splits;               // split-K factor
+  int splits;               // split-K factor (kPartial without stream-K)
   int max_stages;           // cap on pipeline depth (tests / tuning)
-  int tile_rows;            // weight rows per CTA: 256 (two accumulators) or 128
+  int tile_rows;            // weight rows per tile: 256 (two accumulators) or 128
+  int stream_k;             // full-K epilogues: equal iteration ranges per CTA
   float* part;              // kPartial: [splits][rows_cap][N]
-  float* amax_val;          // kArgmax: [ceil(N/32)][rows_cap]
+  float* amax_val;          // kArgmax: [grid * 8][rows_cap]
   int* amax_idx;
   __nv_bfloat16* act;       // kSwiGLU: [rows_cap][ld_act]
   int ld_act;
+  float* sk_part;           // stream-K: [grid][256 tokens][256 rows] fp32 segment partials
+  int* sk_flag;             // stream-K: [grid] segment-ready flags (self-resetting)
+  unsigned long long* dbg;  // diagnostics: per-CTA [8] globaltimer stamps (nullptr: off)
+  int diag;                 // diagnostics (timing only): 1 skip MMAs, 2 skip epilogue math
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
 
-struct GemmPhase {
-  int row_off;   // first weight row of this phase within the tile (0 or 128)
-  int boxes;     // 128-row weight boxes per stage (2: T<=256, 1: T>256)
-  int t0, nt;    // token rows of this phase
+// One accumulation job of a CTA: a k-range of one tile and one token pass.
+struct GemmJob {
+  int tile, k0, k1;   // weight tile, k-iteration range [k0, k1)
+  int row_off;        // first weight row of this pass within the tile (0 or 128)
+  int boxes;          // 128-row weight boxes per stage (2: wide, 1 otherwise)
+  int t0, nt;         // token rows of this pass
+  int split;          // kPartial output slice
+  int role;           // 0 plain, 1 stream-K head owner (has later segments), 2 contributor
 };
 
-// Phases of one CTA's work: T <= 256 with a 256-row tile -> one phase, both
-// 128-row boxes per stage; otherwise one phase per (128-row box, 512-token pass).
-__device__ __forceinline__ int gemm_n_phases(int T, int tile_rows) {
-  if (T <= 256 && tile_rows == 256) return 1;
-  return (tile_rows / 128) * ((T + 511) / 512);
-}
-__device__ __forceinline__ GemmPhase gemm_phase(int T, int tile_rows, int p) {
-  GemmPhase ph;
-  if (T <= 256 && tile_rows == 256) {
-    ph.row_off = 0;
-    ph.boxes = 2;
-    ph.t0 = 0;
-    ph.nt = T;
-  } else {
-    const int per = (T + 511) / 512;
-    ph.row_off = (p / per) * 128;
-    ph.boxes = 1;
-    ph.t0 = (p % per) * 512;
-    ph.nt = min(512, T - ph.t0);
+// The static schedule, computed identically by the three warp roles.
+struct GemmSched {
+  int n_tiles, KI, G, c, T, tile_rows, splits, n_phases;
+  bool sk, wide;
+  int it, hi, unit, phase;
+
+  __device__ __forceinline__ static int iter_lo(int c, int G, int total) {
+    return (int)((long long)total * c / G);
   }
-  return ph;
-}
+
+  __device__ __forceinline__ bool has_iters(int cc) const {
+    const int total = n_tiles * KI;
+    return iter_lo(cc + 1, G, total) > iter_lo(cc, G, total);
+  }
+
+  __device__ __forceinline__ void init(const GemmArgs& a, int T_, int BK) {
+    T = T_;
+    tile_rows = a.tile_rows;
+    n_tiles = (a.N + tile_rows - 1) / tile_rows;
+    KI = a.K / BK;
+    G = gridDim.x;
+    c = blockIdx.x;
+    wide = (T <= 256 && tile_rows == 256);
+    sk = a.stream_k && wide;
+    splits = sk ? 1 : a.splits;
+    n_phases = wide ? 1 : (tile_rows / 128) * ((T + 511) / 512);
+    const int total = n_tiles * KI;
+    it = sk ? iter_lo(c, G, total) : 0;
+    hi = sk ? iter_lo(c + 1, G, total) : 0;
+    unit = c;
+    phase = 0;
+  }
+
+  __device__ __forceinline__ bool next(GemmJob& j) {
+    if (sk) {
+      if (it >= hi) return false;
+      j.tile = it / KI;
+      j.k0 = it % KI;
+      j.k1 = min(KI, j.k0 + (hi - it));
+      it += j.k1 - j.k0;
+      j.row_off = 0;
+      j.boxes = 2;
+      j.t0 = 0;
+      j.nt = T;
+      j.split = 0;
+      j.role = j.k0 > 0 ? 2 : (j.k1 < KI ? 1 : 0);
+      return true;
+    }
+    if (unit >= n_tiles * splits) return false;
+    j.tile = unit % n_tiles;
+    j.split = unit / n_tiles;
+    j.k0 = (int)((long long)KI * j.split / splits);
+    j.k1 = (int)((long long)KI * (j.split + 1) / splits);
+    j.role = 0;
+    if (wide) {
+      j.row_off = 0;
+      j.boxes = 2;
+      j.t0 = 0;
+      j.nt = T;
+    } else {
+      const int per = (T + 511) / 512;
+      j.row_off = (phase / per) * 128;
+      j.boxes = 1;
+      j.t0 = (phase % per) * 512;
+      j.nt = min(512, T - j.t0);
+    }
+    if (++phase >= n_phases) {
+      phase = 0;
+      unit += G;
+    }
+    return true;
+  }
+};
 
 template <int kEpi, int BK>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -105,7 +184,6 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   constexpr int kRow = BK * 2;              // bytes per K-row segment (swizzle span)
   constexpr int kWBox = 128 * kRow;         // one 128-row weight box
   constexpr int kXBox = 64 * kRow;          // one 64-row activation box
-  // runtime stage layout: W bytes + X bytes per stage
   const bool wide = (T <= 256 && a.tile_rows == 256);
   const int w_bytes = wide ? 2 * kWBox : kWBox;
   const int x_rows = wide ? ((T + 63) & ~63) : min((T + 63) & ~63, 512);
@@ -113,24 +191,17 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   int stages = stage_bytes > 0 ? kGemmPipeBytes / stage_bytes : 1;
   stages = stages > kGemmMaxStages ? kGemmMaxStages : (stages < 1 ? 1 : stages);
   if (a.max_stages > 0 && stages > a.max_stages) stages = a.max_stages;
+  // TMEM accumulator buffers: two whenever a job needs <= 256 columns
+  const int t_pad_all = (T + 15) & ~15;
+  const int nbuf = ((wide && t_pad_all <= 128) || (!wide && t_pad_all <= 256)) ? 2 : 1;
+  const int half_stride = (wide && t_pad_all <= 128) ? 128 : 256;   // wide: 2nd accumulator
 
   uint8_t* pipe = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kGemmPipeBytes);
   uint64_t* empty = full + kGemmMaxStages;
-  uint64_t* tmem_full = empty + kGemmMaxStages;
-  uint64_t* tmem_empty = tmem_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-  float* scratch = reinterpret_cast<float*>(smem + kGemmPipeBytes + 1024);
-
-  const int n_tiles = (a.N + a.tile_rows - 1) / a.tile_rows;
-  const int tile = blockIdx.x % n_tiles;
-  const int split = blockIdx.x / n_tiles;
-  const int n0 = tile * a.tile_rows;
-  const int k_iters_total = a.K / BK;
-  const int it_begin = (int)((long long)k_iters_total * split / a.splits);
-  const int it_end = (int)((long long)k_iters_total * (split + 1) / a.splits);
-  const int n_iters = it_end - it_begin;
-  const int n_phases = gemm_n_phases(T, a.tile_rows);
+  uint64_t* tmem_full = empty + kGemmMaxStages;    // [2]
+  uint64_t* tmem_empty = tmem_full + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_w);
@@ -139,8 +210,10 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 256);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 256);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -154,183 +227,290 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     pdl_wait();
     pdl_trigger();
   }
-  if (T == 0 || n_iters <= 0) {
+  GemmSched sched;
+  sched.init(a, T, BK);
+  if (a.dbg && threadIdx.x == 64) a.dbg[blockIdx.x * 8 + 0] = gtimer();
+  const bool no_work = (T == 0);
+
+  if (no_work) {
     if (producer) {
       pdl_wait();
       pdl_trigger();
-    }
-    if (kEpi == kPartial && warp >= 2) {  // K < splits: this split contributes zeros
-      for (int r = threadIdx.x - 64; r < a.tile_rows; r += 256) {
-        const int n = n0 + r;
-        if (n < a.N)
-          for (int t = 0; t < T; ++t) a.part[((size_t)split * a.rows_cap + t) * a.N + n] = 0.0f;
-      }
     }
   } else if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();   // weights stream through once
       const uint64_t pol_x = policy_evict_last();    // activations are re-read by every tile
+      GemmJob j;
+      bool have = sched.next(j);
       // Weights never change: the first stages' weight tiles are requested
       // before waiting on the previous kernel (its tail overlaps our fill).
-      const GemmPhase ph0 = gemm_phase(T, a.tile_rows, 0);
-      const int pre = n_iters < stages ? n_iters : stages;
-      {
-        const int x_boxes = (ph0.nt + 63) >> 6;
-        const uint32_t tx = (uint32_t)ph0.boxes * kWBox + (uint32_t)x_boxes * kXBox;
+      int pre = 0;
+      if (have) {
+        const int x_boxes = (j.nt + 63) >> 6;
+        const uint32_t tx = (uint32_t)j.boxes * kWBox + (uint32_t)x_boxes * kXBox;
+        pre = min(j.k1 - j.k0, stages);
         for (int i = 0; i < pre; ++i) {
           mbar_arrive_expect_tx(&full[i], tx);
-          const int kc = (it_begin + i) * BK;
-          for (int b = 0; b < ph0.boxes; ++b)
-            tma_load_2d(pipe + i * stage_bytes + b * kWBox, &tmap_w, &full[i], kc,
-                        n0 + ph0.row_off + b * 128, pol_w);
+          for (int b = 0; b < j.boxes; ++b)
+            tma_load_2d(pipe + i * stage_bytes + b * kWBox, &tmap_w, &full[i], (j.k0 + i) * BK,
+                        j.tile * a.tile_rows + j.row_off + b * 128, pol_w);
         }
       }
       pdl_wait();
       pdl_trigger();
       int g = 0;
-      for (int p = 0; p < n_phases; ++p) {
-        const GemmPhase ph = gemm_phase(T, a.tile_rows, p);
-        const int x_boxes = (ph.nt + 63) >> 6;
-        const uint32_t tx = (uint32_t)ph.boxes * kWBox + (uint32_t)x_boxes * kXBox;
-        for (int i = 0; i < n_iters; ++i, ++g) {
+      for (; have; have = sched.next(j)) {
+        const int x_boxes = (j.nt + 63) >> 6;
+        const uint32_t tx = (uint32_t)j.boxes * kWBox + (uint32_t)x_boxes * kXBox;
+        const int n0 = j.tile * a.tile_rows + j.row_off;
+        for (int k = j.k0; k < j.k1; ++k, ++g) {
           const int s = g % stages;
           uint8_t* st = pipe + s * stage_bytes;
-          const int kc = (it_begin + i) * BK;
           if (g >= pre) {
-            const uint32_t par = (uint32_t)(g / stages) & 1u;
-            mbar_wait(&empty[s], par ^ 1u);
+            if (g >= stages) mbar_wait(&empty[s], ((uint32_t)(g / stages) & 1u) ^ 1u);
             mbar_arrive_expect_tx(&full[s], tx);
-            for (int b = 0; b < ph.boxes; ++b)
-              tma_load_2d(st + b * kWBox, &tmap_w, &full[s], kc, n0 + ph.row_off + b * 128,
-                          pol_w);
+            for (int b = 0; b < j.boxes; ++b)
+              tma_load_2d(st + b * kWBox, &tmap_w, &full[s], k * BK, n0 + b * 128, pol_w);
           }
           for (int b = 0; b < x_boxes; ++b)
-            tma_load_2d(st + w_bytes + b * kXBox, &tmap_x, &full[s], kc, ph.t0 + b * 64, pol_x);
+            tma_load_2d(st + w_bytes + b * kXBox, &tmap_x, &full[s], k * BK, j.t0 + b * 64, pol_x);
         }
       }
     } else {
       pdl_wait();
       pdl_trigger();
     }
+    __syncwarp();   // reconverge the producer lane before the CTA-wide barrier
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread)
-    int g = 0;
-    for (int p = 0; p < n_phases; ++p) {
-      const GemmPhase ph = gemm_phase(T, a.tile_rows, p);
-      const int t_pad = (ph.nt + 15) & ~15;
+    int g = 0, jn = 0;
+    GemmJob j;
+    while (sched.next(j)) {
+      const int t_pad = (j.nt + 15) & ~15;
       const int nc0 = t_pad < 256 ? t_pad : 256;
       const int nc1 = t_pad - nc0;
       const uint32_t id0 = idesc_bf16_f32(128, (uint32_t)nc0);
       const uint32_t id1 = idesc_bf16_f32(128, (uint32_t)(nc1 > 0 ? nc1 : 16));
-      if (p > 0) {
-        mbar_wait(tmem_empty, (uint32_t)(p - 1) & 1u);
+      const int buf = jn % nbuf;
+      const uint32_t acc = tmem_base + (uint32_t)(buf * 256);
+      if (jn >= nbuf) {
+        mbar_wait(&tmem_empty[buf], (uint32_t)((jn / nbuf) - 1) & 1u);
         tc_fence_after();
       }
-      for (int i = 0; i < n_iters; ++i, ++g) {
+      for (int k = j.k0; k < j.k1; ++k, ++g) {
         const int s = g % stages;
-        const uint32_t par = (uint32_t)(g / stages) & 1u;
-        mbar_wait(&full[s], par);
+        mbar_wait(&full[s], (uint32_t)(g / stages) & 1u);
         tc_fence_after();
-        if (lane == 0) {
+        if (lane == 0 && !(a.diag & 1)) {
           const uint32_t sa = smem_u32(pipe + s * stage_bytes);
           const uint32_t xa = sa + (uint32_t)w_bytes;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+            const uint32_t accf = (k > j.k0 || kk > 0) ? 1u : 0u;
             const uint64_t bd = umma_desc_kmajor<kRow>(xa + kk * 32);
-            if (ph.boxes == 2) {
-              mma_bf16_ss(tmem_base, umma_desc_kmajor<kRow>(sa + kk * 32), bd, id0, acc);
-              mma_bf16_ss(tmem_base + 256, umma_desc_kmajor<kRow>(sa + kWBox + kk * 32), bd, id0,
-                          acc);
+            if (j.boxes == 2) {
+              mma_bf16_ss(acc, umma_desc_kmajor<kRow>(sa + kk * 32), bd, id0, accf);
+              mma_bf16_ss(acc + (uint32_t)half_stride,
+                          umma_desc_kmajor<kRow>(sa + kWBox + kk * 32), bd, id0, accf);
             } else {
               const uint64_t ad = umma_desc_kmajor<kRow>(sa + kk * 32);
-              mma_bf16_ss(tmem_base, ad, bd, id0, acc);
+              mma_bf16_ss(acc, ad, bd, id0, accf);
               if (nc1 > 0)
-                mma_bf16_ss(tmem_base + 256, ad, umma_desc_kmajor<kRow>(xa + 256 * kRow + kk * 32),
-                            id1, acc);
+                mma_bf16_ss(acc + 256, ad, umma_desc_kmajor<kRow>(xa + 256 * kRow + kk * 32),
+                            id1, accf);
             }
           }
+          mma_commit(&empty[s]);
+        } else if (lane == 0) {
           mma_commit(&empty[s]);
         }
         __syncwarp();
       }
-      if (lane == 0) mma_commit(tmem_full);
+      if (lane == 0) mma_commit(&tmem_full[buf]);
       __syncwarp();
+      ++jn;
     }
   } else {
     // ---------------- epilogue warps 2..9: lane quarter q = warp % 4, group = (warp-2)/4
+    // Each thread owns one weight row (TMEM lane) and walks 32-column chunks
+    // (tokens); one tcgen05.wait per chunk.
     const int q = warp & 3;
     const int grp = (warp - 2) >> 2;
-    const int gtid = threadIdx.x - 64 - grp * 128;       // 0..127 within the group
-    const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16);
-    float* up = scratch + grp * (64 * 17);
-    for (int p = 0; p < n_phases; ++p) {
-      const GemmPhase ph = gemm_phase(T, a.tile_rows, p);
-      mbar_wait(tmem_full, (uint32_t)p & 1u);
+    const int etid = threadIdx.x - 64;                   // 0..255
+    const int ewarp = etid >> 5;                         // 0..7
+    int jn = 0;
+    int amax_jobs = 0;   // jobs that wrote argmax slots (contributor segments do not)
+    GemmJob j;
+    while (sched.next(j)) {
+      const int buf = jn % nbuf;
+      mbar_wait(&tmem_full[buf], (uint32_t)(jn / nbuf) & 1u);
       tc_fence_after();
-      const int t_pad = (ph.nt + 15) & ~15;
-      // 2 boxes: group g reads accumulator g (all columns);
-      // 1 box:   both groups read accumulator 0, alternating 16-column chunks
-      const int box = ph.boxes == 2 ? grp : 0;
-      const int col_base = ph.boxes == 2 ? 256 * grp : 0;
-      const int chunk_step = ph.boxes == 2 ? 16 : 32;
-      const int chunk0 = ph.boxes == 2 ? 0 : 16 * grp;
-      const int row = ph.row_off + box * 128 + q * 32 + lane;  // row within the tile
-      const int n = n0 + row;
-      for (int cc = chunk0; cc < t_pad; cc += chunk_step) {
-        float v[16];
-        tmem_ld16(tq + (uint32_t)(col_base + cc), v);
-        const int c0 = ph.t0 + cc;
+      if (a.dbg && etid == 0 && jn == 0) a.dbg[blockIdx.x * 8 + 7] = gtimer();
+      const int t_pad = (j.nt + 15) & ~15;
+      // wide: group g reads accumulator g (all columns);
+      // 1 box: both groups read accumulator 0, alternating 32-column chunks
+      const int box = j.boxes == 2 ? grp : 0;
+      const int col_base = buf * 256 + (j.boxes == 2 ? half_stride * grp : 0);
+      const int chunk_step = j.boxes == 2 ? 32 : 64;
+      const int chunk0 = j.boxes == 2 ? 0 : 32 * grp;
+      const int trow = j.row_off + box * 128 + q * 32 + lane;   // row within the tile
+      const int n = j.tile * a.tile_rows + trow;
+      const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16);
+      // stream-K head owner: the CTAs whose first segment continues this tile
+      // (at most kSkMaxSeg - 1 of them: the plan only enables stream-K when
+      // every CTA owns at least a quarter of a tile's iterations)
+      constexpr int kSkMaxSeg = 8;
+      int cl[kSkMaxSeg - 1];
+      int ncl = 0;
+      if (j.role == 1) {
+        const int total = sched.n_tiles * sched.KI;
+        const int tile_end = (j.tile + 1) * sched.KI;
+        for (int cc = sched.c + 1;
+             cc < sched.G && GemmSched::iter_lo(cc, sched.G, total) < tile_end; ++cc)
+          if (sched.has_iters(cc) && ncl < kSkMaxSeg - 1) cl[ncl++] = cc;
+        if (etid == 0) {   // one poller per owner (no polling storm on the flag lines)
+          for (int i = 0; i < ncl; ++i)
+            while (atomicAdd(a.sk_flag + cl[i], 0) == 0) __nanosleep(128);
+          __threadfence();
+        }
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+      }
+      for (int cc = chunk0; cc < t_pad && !(a.diag & 2); cc += chunk_step) {
+        float v[32];
+        tmem_ld32(tq + (uint32_t)(col_base + cc), v);   // columns past t_pad: unused
+        if (j.k1 <= j.k0) {   // empty k-range (K < splits): this split contributes zeros
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) v[jj] = 0.f;
+        }
+        const int c0 = j.t0 + cc;
+        const int nvalid = min(32, j.nt - cc);           // live token columns of this chunk
+        if (j.role == 2) {   // contributor: publish the raw segment sum
+          float* dst = a.sk_part + (size_t)sched.c * (256 * 256) + trow + (size_t)c0 * 256;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            if (jj < nvalid) dst[jj * 256] = v[jj];
+          continue;
+        }
+        if (j.role == 1) {   // owner: add later segments in k order
+          for (int i = 0; i < ncl; ++i) {
+            const float* src = a.sk_part + (size_t)cl[i] * (256 * 256) + trow + (size_t)c0 * 256;
+            float add[32];
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) add[jj] = jj < nvalid ? __ldcg(src + jj * 256) : 0.f;
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) v[jj] += add[jj];
+          }
+        }
         if (kEpi == kPartial) {
           if (n < a.N) {
-            float* dst = a.part + ((size_t)split * a.rows_cap) * a.N + n;
+            float* dst = a.part + ((size_t)j.split * a.rows_cap + c0) * a.N + n;
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (cc + j < ph.nt) dst[(size_t)(c0 + j) * a.N] = v[j];
+            for (int jj = 0; jj < 32; ++jj)
+              if (jj < nvalid) dst[(size_t)jj * a.N] = v[jj];
           }
         } else if (kEpi == kArgmax) {
-          const int blk = n >> 5;  // 32-row block of this warp
-          const bool warp_live = (n - lane) < a.N;
+          // (max, lowest index) over this warp's 32 rows for each of the 32
+          // token columns: transpose-reduce butterfly (31 pair exchanges
+          // instead of 32 x 5); afterwards lane l holds column l.
+          float bv[32];
+          int bi[32];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float best = (n < a.N) ? v[j] : -INFINITY;
-            int bi = n;
+          for (int jj = 0; jj < 32; ++jj) {
+            bv[jj] = (n < a.N) ? v[jj] : -INFINITY;
+            bi[jj] = n;
+          }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-              const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-              if (ov > best || (ov == best && oi < bi)) {
-                best = ov;
-                bi = oi;
+          for (int w = 16; w >= 1; w >>= 1) {
+            const bool upper = (lane & w) != 0;
+#pragma unroll
+            for (int jj = 0; jj < w; ++jj) {
+              // keep half [jj] (lower lanes) or [jj + w] (upper lanes); send the other
+              const float send_v = upper ? bv[jj] : bv[jj + w];
+              const int send_i = upper ? bi[jj] : bi[jj + w];
+              const float keep_v = upper ? bv[jj + w] : bv[jj];
+              const int keep_i = upper ? bi[jj + w] : bi[jj];
+              const float ov = __shfl_xor_sync(0xffffffffu, send_v, w);
+              const int oi = __shfl_xor_sync(0xffffffffu, send_i, w);
+              const bool take = ov > keep_v || (ov == keep_v && oi < keep_i);
+              bv[jj] = take ? ov : keep_v;
+              bi[jj] = take ? oi : keep_i;
+            }
+          }
+          // lane l now holds column c = bit-reverse-free index: lane bits select halves
+          // high-to-low, so the surviving slot 0 of lane l is column l
+          if (lane < nvalid) {
+            const size_t slot = ((size_t)blockIdx.x * 8 + ewarp) * a.rows_cap + c0 + lane;
+            float ov = bv[0];
+            int oi = bi[0];
+            // first coverage of a token by this warp: the CTA's first unit,
+            // first row pass; later jobs merge with what the warp wrote
+            if (!(amax_jobs < sched.n_phases && j.row_off == 0)) {
+              const float pv = a.amax_val[slot];
+              const int pi = a.amax_idx[slot];
+              if (pv > ov || (pv == ov && pi < oi)) {
+                ov = pv;
+                oi = pi;
               }
             }
-            if (warp_live && lane == j && cc + j < ph.nt) {
-              a.amax_val[(size_t)blk * a.rows_cap + c0 + j] = best;
-              a.amax_idx[(size_t)blk * a.rows_cap + c0 + j] = bi;
+            a.amax_val[slot] = ov;
+            a.amax_idx[slot] = oi;
+          }
+        } else {
+          // kSwiGLU: weight rows interleaved per row pair [gate_i, up_i]: lane
+          // 2i holds gate_i, lane 2i+1 up_i.  Even lanes finish tokens 0..15 of
+          // the chunk, odd lanes tokens 16..31.
+          const bool odd = lane & 1;
+          float out[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            // even lane needs up[jj] from its partner; odd lane needs gate[jj+16]
+            const float send = odd ? v[jj] : v[jj + 16];
+            const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+            const float g = odd ? recv : v[jj];
+            const float u = odd ? v[jj + 16] : recv;
+            out[jj] = silu_f(g) * u;
+          }
+          const int f = (j.tile * a.tile_rows + trow) >> 1;   // feature of this row pair
+          if (n < a.N) {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int tc = (odd ? 16 : 0) + jj;
+              if (tc < nvalid)
+                a.act[(size_t)(c0 + tc) * a.ld_act + f] = __float2bfloat16_rn(out[jj]);
             }
           }
-        } else {  // kSwiGLU: lanes [0,64) gate, [64,128) up of the box's 64 features
-          const int r = q * 32 + lane;
-          if (r >= 64) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) up[(r - 64) * 17 + j] = v[j];
-          }
-          asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
-          if (r < 64) {
-            const int f = (n0 + ph.row_off + box * 128) / 2 + r;
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (cc + j < ph.nt)
-                a.act[(size_t)(c0 + j) * a.ld_act + f] =
-                    __float2bfloat16_rn(silu_f(v[j]) * up[r * 17 + j]);
-          }
-          asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
         }
       }
-      (void)gtid;
+      if (a.dbg && etid == 0 && jn < 5) a.dbg[blockIdx.x * 8 + 1 + jn] = gtimer() | ((unsigned long long)j.role << 62);
       tc_fence_before();
-      mbar_arrive(tmem_empty);
+      mbar_arrive(&tmem_empty[buf]);
+      if (j.role == 2) {
+        // make the segment partial visible, then flag it (one thread, after all 256)
+        __threadfence();
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (etid == 0) atomicExch(a.sk_flag + sched.c, 1);
+      } else if (j.role == 1) {
+        asm volatile("bar.sync 3, 256;" ::: "memory");   // every owner thread read them
+        if (etid == 0)
+          for (int i = 0; i < ncl; ++i) a.sk_flag[cl[i]] = 0;   // self-reset
+      }
+      if (j.role != 2) ++amax_jobs;
+      ++jn;
+    }
+    if (kEpi == kArgmax && !(a.diag & 2)) {
+      // every (CTA, warp) slot of every live token is defined: fill the tokens
+      // this warp never covered (no job, or the other group's chunks of a
+      // one-box pass) with the identity
+      for (int t = lane; t < T; t += 32) {
+        const bool covered = amax_jobs > 0 && (sched.wide || (((t % 512) >> 5) & 1) == grp);
+        if (!covered) {
+          const size_t slot = ((size_t)blockIdx.x * 8 + ewarp) * a.rows_cap + t;
+          a.amax_val[slot] = -INFINITY;
+          a.amax_idx[slot] = 0x7fffffff;
+        }
+      }
     }
   }
   tc_fence_before();

@@ -55,19 +55,20 @@ __global__ void __launch_bounds__(256) k_embed_rmsnorm(const int* __restrict__ t
   pdl_wait();
   pdl_trigger();
   __shared__ float sh[16];
-  const int t = blockIdx.x;
-  if (t >= *t_dev) return;
-  const __nv_bfloat16* e = E + (size_t)tok[t] * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += 256) {
-    const float v = __bfloat162float(e[i]);
-    h[(size_t)t * d + i] = v;
-    ss += v * v;
+  const int T = *t_dev;
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {   // grid-stride over the live rows
+    const __nv_bfloat16* e = E + (size_t)tok[t] * d;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d; i += 256) {
+      const float v = __bfloat162float(e[i]);
+      h[(size_t)t * d + i] = v;
+      ss += v * v;
+    }
+    ss = block_sum_256(ss, sh);
+    const float r = rsqrtf(ss / (float)d + eps);
+    for (int i = threadIdx.x; i < d; i += 256)
+      x[(size_t)t * d + i] = __float2bfloat16_rn(h[(size_t)t * d + i] * r * w[i]);
   }
-  ss = block_sum_256(ss, sh);
-  const float r = rsqrtf(ss / (float)d + eps);
-  for (int i = threadIdx.x; i < d; i += 256)
-    x[(size_t)t * d + i] = __float2bfloat16_rn(h[(size_t)t * d + i] * r * w[i]);
 }
 
 // ---------------------------------------------- residual add (+split-K sum)
@@ -87,8 +88,8 @@ __global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restr
   pdl_wait();
   pdl_trigger();
   __shared__ float sh[40];
-  const int t = blockIdx.x;
-  if (t >= *t_dev) return;
+  const int T = *t_dev;
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {   // grid-stride over the live rows
   const int nv = d >> 2;
   float4 v[kVec];
   const float4* h4 = reinterpret_cast<const float4*>(h + (size_t)t * d);
@@ -146,6 +147,8 @@ __global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restr
       xo[2 * i + 1] = __floats2bfloat162_rn(v[j].z * r * ww.z, v[j].w * r * ww.w);
     }
   }
+  __syncthreads();   // sh reused by the next row
+  }
 }
 
 // ------------------------------------------- qkv epilogue: RoPE + KV write
@@ -163,12 +166,14 @@ __global__ void __launch_bounds__(128) k_qkv_rope_kv(const float* __restrict__ p
                                                      int n_kv, int hd, int ctx_cap) {
   pdl_wait();
   pdl_trigger();
-  const int t = blockIdx.x;
-  if (t >= *t_dev) return;
+  const int T = *t_dev;
   const int half = hd / 2;
-  const int c = blockIdx.y * 128 + threadIdx.x;
   const int n_pairs = (n_q + 2 * n_kv) * half;
-  if (c >= n_pairs) return;
+  const int per_tok = (n_pairs + 127) / 128;
+  for (int wi = blockIdx.x; wi < T * per_tok; wi += gridDim.x) {   // (token, pair block)
+  const int t = wi / per_tok;
+  const int c = (wi % per_tok) * 128 + threadIdx.x;
+  if (c >= n_pairs) continue;
   const int head = c / half, i = c % half;
   const int N = (n_q + 2 * n_kv) * hd;
   const float* p0 = part + (size_t)t * N + head * hd + i;
@@ -207,6 +212,7 @@ __global__ void __launch_bounds__(128) k_qkv_rope_kv(const float* __restrict__ p
     vc[off + i] = __float2bfloat16_rn(a);
     vc[off + i + half] = __float2bfloat16_rn(b);
   }
+  }
 }
 
 // ------------------------------------------------------------ argmax reduce
@@ -219,8 +225,8 @@ __global__ void __launch_bounds__(256) k_argmax_reduce(const float* __restrict__
                                                        float* __restrict__ out_val) {
   pdl_wait();
   pdl_trigger();
-  const int t = blockIdx.x;
-  if (t >= *t_dev) return;
+  const int T = *t_dev;
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {   // grid-stride over the live rows
   float best = -INFINITY;
   int bi = 0x7fffffff;
   for (int i = threadIdx.x; i < n_tiles; i += 256) {
@@ -256,6 +262,8 @@ __global__ void __launch_bounds__(256) k_argmax_reduce(const float* __restrict__
     out_tok[t] = bi;
     if (out_val) out_val[t] = best;
   }
+  __syncthreads();   // sv / si reused by the next row
+  }
 }
 
 // RoPE table: rope[p][i] = (cos(p * theta^(-2i/hd)), sin(...)), double precision.
@@ -272,9 +280,12 @@ __global__ void k_rope_table(float2* rope, int ctx_cap, int hd, double theta) {
 }
 
 // ------------------------------------------------------------------ launchers
+// Row kernels are grid-stride loops over the device-side row count: a fixed
+// grid of a few CTAs per SM instead of one CTA per row of capacity.
+constexpr int kSms = 148;
 int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void* E,
                          const float* w, float* h, void* x, int d, float eps, cudaStream_t s) {
-  SPECTRE_LAUNCH_PDL("k_embed_rmsnorm", k_embed_rmsnorm, dim3(t_cap), dim3(256), 0, s, tok, t_dev,
+  SPECTRE_LAUNCH_PDL("k_embed_rmsnorm", k_embed_rmsnorm, dim3(std::min(t_cap, 2 * kSms)), dim3(256), 0, s, tok, t_dev,
                      reinterpret_cast<const __nv_bfloat16*>(E), w, h,
                      reinterpret_cast<__nv_bfloat16*>(x), d, eps);
   return SPECTRE_OK;
@@ -288,14 +299,15 @@ int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const i
   const int threads = nv < 512 ? ((nv + 31) / 32) * 32 : 512;
   const int vec = (nv + threads - 1) / threads;
   auto* xb = reinterpret_cast<__nv_bfloat16*>(x);
+  const dim3 grid(std::min(t_cap, 2 * kSms));
   if (vec <= 1)
-    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<1>, dim3(t_cap), dim3(threads),
+    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<1>, grid, dim3(threads),
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
   else if (vec <= 2)
-    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<2>, dim3(t_cap), dim3(threads),
+    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<2>, grid, dim3(threads),
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
   else if (vec <= 4)
-    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<4>, dim3(t_cap), dim3(threads),
+    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<4>, grid, dim3(threads),
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
   else
     return arg_fail("residual_rmsnorm: d > 8192");
@@ -308,7 +320,8 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
                        cudaStream_t s) {
   if (splits > kMaxSplits) return arg_fail("qkv_rope_kv: splits");
   const int pairs = (n_q + 2 * n_kv) * hd / 2;
-  SPECTRE_LAUNCH_PDL("k_qkv_rope_kv", k_qkv_rope_kv, dim3(t_cap, (pairs + 127) / 128), dim3(128),
+  SPECTRE_LAUNCH_PDL("k_qkv_rope_kv", k_qkv_rope_kv,
+                     dim3(std::min(t_cap * ((pairs + 127) / 128), 8 * kSms)), dim3(128),
                      0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
                      reinterpret_cast<const float2*>(rope), reinterpret_cast<__nv_bfloat16*>(q),
                      reinterpret_cast<__nv_bfloat16*>(kc), reinterpret_cast<__nv_bfloat16*>(vc),
@@ -319,7 +332,7 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
 int launch_argmax_reduce(const float* val, const int* idx, int n_tiles, int rows_cap,
                          const int* t_dev, int t_cap, int* out_tok, float* out_val,
                          cudaStream_t s) {
-  SPECTRE_LAUNCH_PDL("k_argmax_reduce", k_argmax_reduce, dim3(t_cap), dim3(256), 0, s, val, idx,
+  SPECTRE_LAUNCH_PDL("k_argmax_reduce", k_argmax_reduce, dim3(std::min(t_cap, 2 * kSms)), dim3(256), 0, s, val, idx,
                      n_tiles, rows_cap, t_dev, out_tok, out_val);
   return SPECTRE_OK;
 }

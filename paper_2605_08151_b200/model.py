@@ -92,7 +92,7 @@ class ModelWeights:
         self.wqkv = torch.empty(L, spec.qkv_rows, d, dtype=bf, device=device)
         self.wo = torch.empty(L, d, qd, dtype=bf, device=device)
         self.mlp_norm = torch.ones(L, d, dtype=torch.float32, device=device)
-        self.wgu = torch.empty(L, 2 * F, d, dtype=bf, device=device)   # 64-row gate/up interleave
+        self.wgu = torch.empty(L, 2 * F, d, dtype=bf, device=device)   # rows [g0, u0, g1, u1, ..]
         self.wd = torch.empty(L, d, F, dtype=bf, device=device)
         self.final_norm = torch.ones(d, dtype=torch.float32, device=device)
         self.lm_head = torch.empty(V, d, dtype=bf, device=device)
@@ -113,8 +113,8 @@ class ModelWeights:
     def gate_up(self, layer: int):
         """De-interleaved (gate [F][d], up [F][d]) views for reference code."""
         F, d = self.spec.ffn, self.spec.d_model
-        w = self.wgu[layer].view(F // 64, 2, 64, d)
-        return w[:, 0].reshape(F, d), w[:, 1].reshape(F, d)
+        w = self.wgu[layer].view(F, 2, d)
+        return w[:, 0], w[:, 1]
 
     def struct(self) -> _native.ModelWeights:
         p = lambda t: t.data_ptr()

@@ -22,7 +22,8 @@ for name, N, K, epi, splits, T in SHAPES:
     av = torch.empty((N + 31) // 32, 512, device="cuda")
     ai = torch.empty((N + 31) // 32, 512, dtype=torch.int32, device="cuda")
     act = torch.empty(512, N // 2, dtype=torch.bfloat16, device="cuda")
-    for bk, ms in (("256rows", 0), ("128rows", 1000)):
+    variants = (("sk", 0), ("nosk", 2000)) if epi != 0 else (("256rows", 0),)
+    for bk, ms in variants:
         ts = []
         for it in range(30):
             W = Ws[it % copies]

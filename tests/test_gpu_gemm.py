@@ -34,7 +34,7 @@ def _run(env, X, W, T, rows_cap, splits=1, epi=PARTIAL, t_dev=None, max_stages=0
     N, K = W.shape
     dev = X.device
     part = torch.zeros(splits, rows_cap, N, dtype=torch.float32, device=dev)
-    n_blocks = (N + 31) // 32
+    n_blocks = _native.lib().spectre_gemm_argmax_blocks(N, W.shape[1])
     av = torch.zeros(n_blocks, rows_cap, dtype=torch.float32, device=dev)
     ai = torch.zeros(n_blocks, rows_cap, dtype=torch.int32, device=dev)
     act = torch.zeros(rows_cap, max(N // 2, 1), dtype=torch.bfloat16, device=dev)
@@ -129,8 +129,8 @@ def test_multipass_argmax_and_swiglu(env):
     clear = (top2[:, 0] - top2[:, 1]) > 1e-2
     assert torch.equal(idx[clear], logits.argmax(1)[clear])
     _, _, _, act = _run(env, X, W, T, 1024, 1, SWIGLU)
-    g = _ref(torch, X, W.view(8, 2, 64, 512)[:, 0].reshape(512, 512), T)
-    u = _ref(torch, X, W.view(8, 2, 64, 512)[:, 1].reshape(512, 512), T)
+    g = _ref(torch, X, W.view(512, 2, 512)[:, 0], T)   # rows [g0, u0, g1, u1, ...]
+    u = _ref(torch, X, W.view(512, 2, 512)[:, 1], T)
     assert torch.allclose(act[:T].float(), torch.nn.functional.silu(g) * u, atol=3e-2, rtol=2e-2)
 
 
@@ -140,12 +140,68 @@ def test_swiglu_epilogue(env):
     X = torch.randn(64, K, device="cuda").bfloat16()
     Wg = (torch.randn(F, K, device="cuda") * 0.05).bfloat16()
     Wu = (torch.randn(F, K, device="cuda") * 0.05).bfloat16()
-    # interleave per 64 rows: [g0..g63, u0..u63, g64..g127, u64..u127, ...]
-    W = torch.stack([Wg.view(F // 64, 64, K), Wu.view(F // 64, 64, K)], 1).reshape(2 * F, K)
-    _, _, _, act = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU)
+    # interleave per row pair: [g0, u0, g1, u1, ...]
+    W = torch.stack([Wg, Wu], 1).reshape(2 * F, K)
+    _, _, _, act = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU)          # stream-K
+    _, _, _, act256 = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU, max_stages=2000)
     _, _, _, act128 = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU, max_stages=1000)
-    assert torch.equal(act, act128)
+    assert torch.equal(act256, act128)   # same full-K order, different tiling
+    assert torch.allclose(act.float(), act256.float(), atol=1e-2, rtol=1e-2)
     g = _ref(torch, X, Wg, T)
     u = _ref(torch, X, Wu, T)
     want = torch.nn.functional.silu(g) * u
     assert torch.allclose(act[:T, :F].float(), want, atol=3e-2, rtol=2e-2)
+
+
+@pytest.mark.parametrize("epi", [ARGMAX, SWIGLU])
+@pytest.mark.parametrize("N,K", [(28672 // 4, 4096), (128256 // 8 - 4, 2048), (1024, 1024)])
+def test_stream_k_batch_invariance_bitwise(env, epi, N, K):
+    if epi == SWIGLU and N % 128:
+        N -= N % 128
+    """Stream-K cut points depend on (N, K, grid) only: a token's result is
+    bit-identical for any token count, and matches the fp32 reference."""
+    torch = env[0]
+    g = torch.Generator(device="cuda").manual_seed(N + K + epi)
+    X = torch.randn(256, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.03).bfloat16()
+    outs = {}
+    for T in (1, 7, 64, 130, 256):
+        _, av, ai, act = _run(env, X, W, T, 256, 1, epi)
+        outs[T] = (av[:, :T].clone(), ai[:, :T].clone()) if epi == ARGMAX else act[:T].clone()
+    for T in (1, 7, 64, 130):
+        if epi == ARGMAX:
+            assert torch.equal(outs[T][0], outs[256][0][:, :T])
+            assert torch.equal(outs[T][1], outs[256][1][:, :T])
+        else:
+            assert torch.equal(outs[T], outs[256][:T])
+    logits = _ref(torch, X, W, 256)
+    if epi == ARGMAX:
+        av, ai = outs[256]
+        idx = ai.gather(0, av.argmax(0)[None]).squeeze(0).long()
+        top2 = logits.topk(2, dim=1).values
+        clear = (top2[:, 0] - top2[:, 1]) > 1e-2
+        assert torch.equal(idx[clear], logits.argmax(1)[clear])
+    else:
+        Wv = W.view(N // 2, 2, K)
+        gt = _ref(torch, X, Wv[:, 0], 256)
+        ut = _ref(torch, X, Wv[:, 1], 256)
+        want = torch.nn.functional.silu(gt) * ut
+        assert torch.allclose(outs[256].float()[:, :N // 2], want, atol=3e-2, rtol=2e-2)
+
+
+def test_argmax_no_stale_partials(env):
+    """Back-to-back launches with different inputs (stream-K contributor CTAs
+    write no argmax slot of their own): every result must be fresh."""
+    torch = env[0]
+    V, K = 32000, 1024
+    W = (torch.randn(V, K, device="cuda") * 0.03).bfloat16()
+    for seed in range(3):
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        X = torch.randn(64, K, device="cuda", generator=g).bfloat16()
+        for T in (32, 5, 64):
+            _, av, ai, _ = _run(env, X, W, T, 64, 1, ARGMAX)
+            idx = ai[:, :T].gather(0, av[:, :T].argmax(0)[None]).squeeze(0).long()
+            logits = _ref(torch, X, W, T)
+            top2 = logits.topk(2, dim=1).values
+            clear = (top2[:, 0] - top2[:, 1]) > 1e-2
+            assert torch.equal(idx[clear], logits.argmax(1)[clear]), (seed, T)
