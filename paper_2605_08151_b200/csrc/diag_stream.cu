@@ -116,3 +116,43 @@ extern "C" int spectre_diag_stream(const void* buf, int64_t bytes_per_cta, int32
   cudaEventDestroy(e1);
   return SPECTRE_OK;
 }
+
+// TMEM load latency/throughput: 8 warps x `iters` x tcgen05.ld.32x32b.x32 (+ wait each).
+namespace spectre {
+__global__ void __launch_bounds__(320, 1) k_diag_tmem(int iters, int shape, unsigned long long* out) {
+  using namespace ptx;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 1) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t base = slot;
+  unsigned long long t0 = clock64();
+  float acc = 0.f;
+  if (warp >= 2) {
+    const uint32_t tq = base + ((uint32_t)((warp & 3) * 32) << 16);
+    for (int i = 0; i < iters; ++i) {
+      float v[32];
+      tmem_ld32(tq + (uint32_t)((i * 32) & 511), v);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc += v[k];
+    }
+  }
+  unsigned long long t1 = clock64();
+  if ((threadIdx.x & 31) == 0 && warp >= 2) out[blockIdx.x * 8 + warp - 2] = t1 - t0;
+  if (acc == 1234.5f) out[0] = 0;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(base);
+  }
+}
+}  // namespace spectre
+
+extern "C" int spectre_diag_tmem(int32_t iters, unsigned long long* out_dev, void* stream) {
+  k_diag_tmem<<<1, 320, 0, as_stream(stream)>>>(iters, 0, out_dev);
+  SPECTRE_LAUNCH_CHECK("k_diag_tmem");
+  return SPECTRE_OK;
+}

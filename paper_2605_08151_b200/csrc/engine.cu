@@ -152,14 +152,16 @@ struct ModelRT {
                     kPartial, sp_qkv, 0, 0, tile_rows));
       TRY(gemm_plan(&po[l], bf(w.wo) + (size_t)l * d * qd, d, qd, attn, rows_cap, kPartial,
                     sp_o, 0, 0, tile_rows));
-      // SwiGLU needs full K per tile: stream-K over every SM
+      // SwiGLU needs full K per tile: 128-row tiles when they fit one wave
+      // (draft), else 256-row tiles (two accumulators share every X stage)
+      const bool gu128 = (2 * F) / 128 <= gemm_sk_grid();
       TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
-                    1, 0, 0, 256, sk_part, sk_flag));
+                    1, 0, 0, gu128 ? 128 : 256));
       TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
                     0, 0, tile_rows));
-      for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) p->args.part = part;
-      pgu[l].args.act = act;
-      pgu[l].args.ld_act = F;
+      for (GemmPlan* p : {&pq[l], &po[l], &pd[l]})
+        TRY(gemm_set_outputs(p, part, nullptr, nullptr, nullptr, 0));
+      TRY(gemm_set_outputs(&pgu[l], nullptr, nullptr, nullptr, act, F));
       for (GemmPlan* p : {&pq[l], &po[l], &pgu[l], &pd[l]}) p->args.t_dev = bt.t_dev;
     }
     TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, 256, sk_part,
@@ -167,8 +169,7 @@ struct ModelRT {
     const uint64_t kv_rows = (uint64_t)L * n_req * dm.n_kv_heads * ctx_cap;
     TRY(make_tmap_bf16(&tm_k, w.k_cache, dm.head_dim, kv_rows, 64, 64));
     TRY(make_tmap_bf16(&tm_v, w.v_cache, dm.head_dim, kv_rows, 64, 64));
-    plm.args.amax_val = amax_v;
-    plm.args.amax_idx = amax_i;
+    TRY(gemm_set_outputs(&plm, nullptr, amax_v, amax_i, nullptr, 0));
     plm.args.t_dev = bt.t_dev;
     return SPECTRE_OK;
   }

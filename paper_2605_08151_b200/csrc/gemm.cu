@@ -55,6 +55,55 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t out
   return SPECTRE_OK;
 }
 
+static int num_sms_pub();
+
+// 2-D fp32 / bf16 map for TMA stores: [outer][inner], box {box_inner, box_outer}, no swizzle.
+static int make_tmap_store(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esize,
+                           uint64_t inner, uint64_t outer, uint32_t box_inner,
+                           uint32_t box_outer) {
+  if (int e = get_encoder()) return e;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * esize};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled(store) failed: " + std::to_string((int)r));
+    return SPECTRE_ECUDA;
+  }
+  return SPECTRE_OK;
+}
+
+int gemm_set_outputs(GemmPlan* p, float* part, float* amax_val, int* amax_idx, void* act,
+                     int ld_act) {
+  p->args.part = part;
+  p->args.amax_val = amax_val;
+  p->args.amax_idx = amax_idx;
+  p->args.act = reinterpret_cast<__nv_bfloat16*>(act);
+  p->args.ld_act = ld_act;
+  if (p->epi == kPartial && part) {
+    if ((p->args.N * 4) % 16) return arg_fail("gemm: partial rows must be 16-byte aligned");
+    if (int e = make_tmap_store(&p->tmap_out, part, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                                (uint64_t)p->args.N,
+                                (uint64_t)p->args.splits * p->args.rows_cap, 128, 16))
+      return e;
+  }
+  if (p->epi == kSwiGLU && act) {
+    if ((ld_act * 2) % 16) return arg_fail("gemm: act rows must be 16-byte aligned");
+    if (int e = make_tmap_store(&p->tmap_out, act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                (uint64_t)ld_act, (uint64_t)p->args.rows_cap, 64, 32))
+      return e;
+  }
+  if (p->args.stream_k && p->args.sk_part) {
+    if (int e = make_tmap_store(&p->tmap_sk, p->args.sk_part, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                                256, (uint64_t)num_sms_pub() * 256, 128, 16))
+      return e;
+  }
+  return SPECTRE_OK;
+}
+
 template <int kEpi, int BK>
 static int launch_one(const GemmPlan& p, cudaStream_t s) {
   auto kern = gemm_bf16_swapab<kEpi, BK>;
@@ -65,7 +114,7 @@ static int launch_one(const GemmPlan& p, cudaStream_t s) {
     configured = true;
   }
   SPECTRE_LAUNCH_PDL("gemm_bf16_swapab", kern, dim3(p.grid), dim3(kGemmThreads), kGemmSmemBytes,
-                     s, p.tmap_w, p.tmap_x, p.args);
+                     s, p.tmap_w, p.tmap_x, p.tmap_out, p.tmap_sk, p.args);
   return SPECTRE_OK;
 }
 
@@ -88,6 +137,7 @@ static int num_sms() {
 }
 
 size_t gemm_sk_part_floats() { return (size_t)num_sms() * 256 * 256; }
+static int num_sms_pub() { return num_sms(); }
 int gemm_sk_grid() { return num_sms(); }
 
 int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_cap, int epi,
@@ -191,11 +241,7 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
     return e;
   p.args.t_dev = t_dev;
   p.args.t_static = t_static;
-  p.args.part = partial;
-  p.args.amax_val = amax_val;
-  p.args.amax_idx = amax_idx;
-  p.args.act = reinterpret_cast<__nv_bfloat16*>(act);
-  p.args.ld_act = ld_act;
+  if (int e = gemm_set_outputs(&p, partial, amax_val, amax_idx, act, ld_act)) return e;
   if (const char* dg = getenv("SPECTRE_GEMM_DIAG")) p.args.diag = atoi(dg);
   static unsigned long long* dbg = nullptr;
   if (getenv("SPECTRE_GEMM_DBG")) {

@@ -11,6 +11,8 @@ namespace spectre {
 struct GemmPlan {
   CUtensorMap tmap_w;
   CUtensorMap tmap_x;
+  CUtensorMap tmap_out;   // kPartial: part fp32 [splits*rows_cap][N]; kSwiGLU: act bf16
+  CUtensorMap tmap_sk;    // stream-K partials fp32 [grid*256][256]
   GemmArgs args;
   int grid = 0;
   int epi = 0;
@@ -29,6 +31,9 @@ int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_
               float* sk_part = nullptr, int* sk_flag = nullptr);
 size_t gemm_sk_part_floats();
 int gemm_sk_grid();
+// Output buffers (call after gemm_plan): builds the TMA store maps.
+int gemm_set_outputs(GemmPlan* p, float* part, float* amax_val, int* amax_idx, void* act,
+                     int ld_act);
 int gemm_run(const GemmPlan& p, cudaStream_t s);
 
 }  // namespace spectre

@@ -53,7 +53,8 @@ constexpr int kGemmTileN = 256;        // weight rows per CTA tile
 constexpr int kGemmMaxStages = 8;
 constexpr int kGemmSmemBytes = 232448; // dynamic smem requested at launch
 constexpr int kGemmScratch = 1024;
-constexpr int kGemmPipeBytes = kGemmSmemBytes - 1024 - 1024 - kGemmScratch;
+constexpr int kGemmStageOut = 2 * 16384;   // per epilogue group: [32 tokens][128 rows] fp32
+constexpr int kGemmPipeBytes = kGemmSmemBytes - 1024 - 1024 - kGemmScratch - kGemmStageOut;
 
 struct GemmArgs {
   int N, K;                 // weight rows, reduction length
@@ -64,10 +65,10 @@ struct GemmArgs {
   int max_stages;           // cap on pipeline depth (tests / tuning)
   int tile_rows;            // weight rows per tile: 256 (two accumulators) or 128
   int stream_k;             // full-K epilogues: equal iteration ranges per CTA
-  float* part;              // kPartial: [splits][rows_cap][N]
+  float* part;              // kPartial: [splits][rows_cap][N] (written through tmap_out)
   float* amax_val;          // kArgmax: [grid * 8][rows_cap]
   int* amax_idx;
-  __nv_bfloat16* act;       // kSwiGLU: [rows_cap][ld_act]
+  __nv_bfloat16* act;       // kSwiGLU: [rows_cap][ld_act] (written through tmap_out)
   int ld_act;
   float* sk_part;           // stream-K: [grid][256 tokens][256 rows] fp32 segment partials
   int* sk_flag;             // stream-K: [grid] segment-ready flags (self-resetting)
@@ -170,7 +171,10 @@ struct GemmSched {
 template <int kEpi, int BK>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
-                 const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
+                 const __grid_constant__ CUtensorMap tmap_x,
+                 const __grid_constant__ CUtensorMap tmap_out,   // part fp32 / act bf16
+                 const __grid_constant__ CUtensorMap tmap_sk,    // stream-K partials fp32
+                 GemmArgs a) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -197,7 +201,8 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   const int half_stride = (wide && t_pad_all <= 128) ? 128 : 256;   // wide: 2nd accumulator
 
   uint8_t* pipe = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kGemmPipeBytes);
+  uint8_t* stage_out = smem + kGemmPipeBytes;   // 1024-aligned: kGemmPipeBytes % 1024 == 0
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kGemmPipeBytes + kGemmStageOut);
   uint64_t* empty = full + kGemmMaxStages;
   uint64_t* tmem_full = empty + kGemmMaxStages;    // [2]
   uint64_t* tmem_empty = tmem_full + 2;            // [2]
@@ -340,6 +345,24 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     const int grp = (warp - 2) >> 2;
     const int etid = threadIdx.x - 64;                   // 0..255
     const int ewarp = etid >> 5;                         // 0..7
+    // Outputs leave through TMA bulk-tensor stores staged in shared memory
+    // (per group [32 tokens][128 rows]): plain per-thread stores are bounded
+    // by outstanding-store slots (~20 GB/s per SM), bulk stores are not.
+    const bool issuer = (warp == 2 + 4 * grp) && lane == 0;
+    const int srow = q * 32 + lane;                      // row within the group's 128
+    const int gbar = 1 + grp;
+    int sbuf = 0;   // double-buffered staging: 2 x 8 KB per group
+    uint8_t* stg = stage_out + grp * 16384;
+    auto stage_begin = [&]() {   // the store issued two steps ago has read its buffer
+      stg = stage_out + grp * 16384 + sbuf * 8192;
+      sbuf ^= 1;
+      if (issuer) bulk_wait_read<1>();
+      asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");
+    };
+    auto stage_end = [&]() {     // staged tile visible to the async proxy
+      fence_proxy_async_smem();
+      asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");
+    };
     int jn = 0;
     int amax_jobs = 0;   // jobs that wrote argmax slots (contributor segments do not)
     GemmJob j;
@@ -386,11 +409,24 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
         }
         const int c0 = j.t0 + cc;
         const int nvalid = min(32, j.nt - cc);           // live token columns of this chunk
-        if (j.role == 2) {   // contributor: publish the raw segment sum
-          float* dst = a.sk_part + (size_t)sched.c * (256 * 256) + trow + (size_t)c0 * 256;
+        if (a.diag & 4) {   // diagnostics: TMEM loads only
+          if (v[0] == 12345.f) a.part[0] = v[1];
+          if (a.dbg && etid == 0 && cc == chunk0) a.dbg[blockIdx.x * 8 + 6] = gtimer();
+          continue;
+        }
+        if (j.role == 2) {   // contributor: publish the raw segment sum ([col][256 rows])
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj)
-            if (jj < nvalid) dst[jj * 256] = v[jj];
+          for (int h = 0; h < 2; ++h) {   // two 16-token halves
+            stage_begin();
+            float* st = reinterpret_cast<float*>(stg);
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) st[jj * 128 + srow] = v[h * 16 + jj];
+            stage_end();
+            if (issuer) {
+              tma_store_2d(&tmap_sk, stg, box * 128, sched.c * 256 + c0 + 16 * h);
+              bulk_commit();
+            }
+          }
           continue;
         }
         if (j.role == 1) {   // owner: add later segments in k order
@@ -404,11 +440,21 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
           }
         }
         if (kEpi == kPartial) {
-          if (n < a.N) {
-            float* dst = a.part + ((size_t)j.split * a.rows_cap + c0) * a.N + n;
+          // [split][t][n]: rows t >= T of the 32-token box land in unread
+          // padding; columns past N are clipped by the tensor map
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-              if (jj < nvalid) dst[(size_t)jj * a.N] = v[jj];
+          for (int h = 0; h < 2; ++h) {   // two 16-token halves
+            if (h * 16 >= nvalid) break;
+            stage_begin();
+            float* st = reinterpret_cast<float*>(stg);
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) st[jj * 128 + srow] = v[h * 16 + jj];
+            stage_end();
+            if (issuer) {
+              tma_store_2d(&tmap_out, stg, j.tile * a.tile_rows + j.row_off + box * 128,
+                           j.split * a.rows_cap + c0 + 16 * h);
+              bulk_commit();
+            }
           }
         } else if (kEpi == kArgmax) {
           // (max, lowest index) over this warp's 32 rows for each of the 32
@@ -472,14 +518,17 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
             const float u = odd ? v[jj + 16] : recv;
             out[jj] = silu_f(g) * u;
           }
-          const int f = (j.tile * a.tile_rows + trow) >> 1;   // feature of this row pair
-          if (n < a.N) {
+          // stage [32 tokens][64 features] bf16, store the box at (f0, c0)
+          stage_begin();
+          __nv_bfloat16* st = reinterpret_cast<__nv_bfloat16*>(stg);
+          const int fi = srow >> 1;
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-              const int tc = (odd ? 16 : 0) + jj;
-              if (tc < nvalid)
-                a.act[(size_t)(c0 + tc) * a.ld_act + f] = __float2bfloat16_rn(out[jj]);
-            }
+          for (int jj = 0; jj < 16; ++jj)
+            st[((odd ? 16 : 0) + jj) * 64 + fi] = __float2bfloat16_rn(out[jj]);
+          stage_end();
+          if (issuer) {
+            tma_store_2d(&tmap_out, stg, (j.tile * a.tile_rows + j.row_off + box * 128) >> 1, c0);
+            bulk_commit();
           }
         }
       }
@@ -488,6 +537,10 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       mbar_arrive(&tmem_empty[buf]);
       if (j.role == 2) {
         // make the segment partial visible, then flag it (one thread, after all 256)
+        if (issuer) {
+          bulk_wait_all();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         __threadfence();
         asm volatile("bar.sync 3, 256;" ::: "memory");
         if (etid == 0) atomicExch(a.sk_flag + sched.c, 1);
@@ -499,6 +552,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       if (j.role != 2) ++amax_jobs;
       ++jn;
     }
+    if (issuer) bulk_wait_all();   // outputs complete before the grid does
     if (kEpi == kArgmax && !(a.diag & 2)) {
       // every (CTA, warp) slot of every live token is defined: fill the tokens
       // this warp never covered (no job, or the other group's chunks of a

@@ -110,5 +110,41 @@ def main():
                                               kernels=out), indent=1))
 
 
+
+
+def timeline(argv=None):
+    """Print the kernel sequence (start/end, us) of one eager ordinary round."""
+    import argparse as _a
+    ap = _a.ArgumentParser()
+    ap.add_argument("--warm-rounds", type=int, default=160)
+    ap.add_argument("--first", type=int, default=0)
+    ap.add_argument("--count", type=int, default=40)
+    args = ap.parse_args(argv)
+    spec = M.DecodeSpec(n_req=64, gamma=4, output_len=1024, prompt_len=128, seed=0)
+    pair = M.build_pair(M.LLAMA_31_8B, M.LLAMA_32_1B, n_req=64, ctx_cap=spec.ctx_cap(), seed=0,
+                        target_branch=0.004, draft_branch=0.004)
+    eng = M.SpectreEngine(pair, spec, "ordinary")
+    eng.prefill(M.synthetic_prompts(64, 128, M.LLAMA_31_8B.vocab))
+    eng.run(max_rounds=args.warm_rounds, use_graph=False)
+    torch.cuda.synchronize()
+    from torch.profiler import profile, ProfilerActivity
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        eng.run(max_rounds=1, use_graph=False)
+        torch.cuda.synchronize()
+    evs = sorted(((e.time_range.start, e.time_range.end, short(e.name)) for e in prof.events()
+                  if e.device_type.name == "CUDA" and "Memcpy" not in e.name
+                  and "Memset" not in e.name), key=lambda x: x[0])
+    t0 = evs[0][0]
+    prev = None
+    for i, (a, b, n) in enumerate(evs[args.first:args.first + args.count]):
+        gap = (a - prev) if prev is not None else 0.0
+        print(f"{i + args.first:4d} start {a - t0:9.2f} end {b - t0:9.2f} dur {b - a:7.2f} "
+              f"gap_after_prev_end {gap:7.2f}  {n}")
+        prev = b
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "timeline":
+        timeline(sys.argv[2:])
+    else:
+        main()

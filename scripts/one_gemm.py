@@ -7,6 +7,7 @@ from paper_2605_08151_b200 import _native
 L = _native.lib()
 N, K, epi, T = (int(v) for v in sys.argv[1:5])
 flags = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+splits = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 W = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
 X = torch.randn(512, K, device="cuda").bfloat16()
 part = torch.empty(12, 512, N, device="cuda") if epi == 0 else torch.empty(1, device="cuda")
@@ -14,7 +15,7 @@ av = torch.empty((N + 31) // 32, 512, device="cuda")
 ai = torch.empty((N + 31) // 32, 512, dtype=torch.int32, device="cuda")
 act = torch.empty(512, N // 2, dtype=torch.bfloat16, device="cuda")
 for _ in range(3):
-    _native.check(L.spectre_gemm_bf16(X.data_ptr(), W.data_ptr(), None, T, 512, N, K, 1, epi,
+    _native.check(L.spectre_gemm_bf16(X.data_ptr(), W.data_ptr(), None, T, 512, N, K, splits, epi,
                                       part.data_ptr(), av.data_ptr(), ai.data_ptr(), act.data_ptr(),
                                       N // 2, flags, _native.stream_ptr()), "gemm")
 torch.cuda.synchronize()

@@ -145,8 +145,9 @@ def test_swiglu_epilogue(env):
     _, _, _, act = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU)          # stream-K
     _, _, _, act256 = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU, max_stages=2000)
     _, _, _, act128 = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU, max_stages=1000)
-    assert torch.equal(act256, act128)   # same full-K order, different tiling
-    assert torch.allclose(act.float(), act256.float(), atol=1e-2, rtol=1e-2)
+    # rows >= T are unread padding (the 32-token store boxes may write them)
+    assert torch.equal(act256[:T], act128[:T])   # same full-K order, different tiling
+    assert torch.allclose(act[:T].float(), act256[:T].float(), atol=1e-2, rtol=1e-2)
     g = _ref(torch, X, Wg, T)
     u = _ref(torch, X, Wu, T)
     want = torch.nn.functional.silu(g) * u
