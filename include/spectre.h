@@ -219,6 +219,8 @@ typedef struct SpectreDecodeConfig {
   double t_draft;
   double ema_decay;
   double fixed_threshold_l;
+  double temperature;       /* 0: greedy verification; > 0: speculative rejection
+                               sampling at this temperature (config 3) */
 } SpectreDecodeConfig;
 
 size_t spectre_engine_workspace_bytes(const SpectreModelDims* target,

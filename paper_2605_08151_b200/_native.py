@@ -106,7 +106,7 @@ class DecodeConfig(C.Structure):
                 ("controller", C.c_int32), ("r_kind", C.c_int32), ("max_rounds", C.c_int32),
                 ("ctx_cap", C.c_int32), ("has_fixed_l", C.c_int32), ("alpha", C.c_double),
                 ("t_target", C.c_double), ("t_draft", C.c_double), ("ema_decay", C.c_double),
-                ("fixed_threshold_l", C.c_double)]
+                ("fixed_threshold_l", C.c_double), ("temperature", C.c_double)]
 
 
 TRACE_FIELDS = ("mode", "participants", "delta", "n_roll", "content_sum", "content_n",

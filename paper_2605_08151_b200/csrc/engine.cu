@@ -91,6 +91,11 @@ struct ModelRT {
   float *part = nullptr, *att_o = nullptr, *att_ml = nullptr, *amax_v = nullptr;
   float* sk_part = nullptr;   // stream-K segment partials (SwiGLU / lm_head GEMMs)
   int* sk_flag = nullptr;
+  int sampling = 0;           // temperature > 0: lm_head writes fp32 logits
+  float inv_t = 1.f;
+  uint64_t seed = 0;
+  float* logits = nullptr;    // [rows_cap][vocab] (sampling)
+  float2* lstat = nullptr;    // [rows_cap] (max, sum exp) of logits / T
   int* att_cnt = nullptr;
   int* amax_i = nullptr;
   float2* rope = nullptr;
@@ -124,6 +129,10 @@ struct ModelRT {
     att_ml = b.take<float>(att_rows * 2);
     att_cnt = b.take<int>((size_t)n_req * dm.n_kv_heads * rb_cap);
     const int n_blocks = gemm_sk_grid() * 8;   // argmax partials: one per CTA epilogue warp
+    if (sampling) {
+      logits = b.take<float>((size_t)R * dm.vocab);
+      lstat = b.take<float2>(R);
+    }
     amax_v = b.take<float>((size_t)n_blocks * R);
     amax_i = b.take<int>((size_t)n_blocks * R);
     rope = b.take<float2>((size_t)ctx_cap * dm.head_dim / 2);
@@ -164,19 +173,26 @@ struct ModelRT {
       TRY(gemm_set_outputs(&pgu[l], nullptr, nullptr, nullptr, act, F));
       for (GemmPlan* p : {&pq[l], &po[l], &pgu[l], &pd[l]}) p->args.t_dev = bt.t_dev;
     }
-    TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, 256, sk_part,
-                  sk_flag));
+    if (sampling) {   // materialise fp32 logits (one split) for the samplers
+      TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kPartial, 1, 0, 0, 256));
+      TRY(gemm_set_outputs(&plm, logits, nullptr, nullptr, nullptr, 0));
+    } else {
+      TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, 256, sk_part,
+                    sk_flag));
+      TRY(gemm_set_outputs(&plm, nullptr, amax_v, amax_i, nullptr, 0));
+    }
     const uint64_t kv_rows = (uint64_t)L * n_req * dm.n_kv_heads * ctx_cap;
     TRY(make_tmap_bf16(&tm_k, w.k_cache, dm.head_dim, kv_rows, 64, 64));
     TRY(make_tmap_bf16(&tm_v, w.v_cache, dm.head_dim, kv_rows, 64, 64));
-    TRY(gemm_set_outputs(&plm, nullptr, amax_v, amax_i, nullptr, 0));
     plm.args.t_dev = bt.t_dev;
     return SPECTRE_OK;
   }
 
   // One forward pass over the packed batch in `bt`; `new_per_req` bounds
   // n_new[b] (sizes the attention row blocks).
-  int forward(int new_per_req, cudaStream_t s, void* out_x = nullptr) {
+  // sample_rows: in sampling mode also draw a token for every row (target
+  // verify / prefill); the draft's decode steps sample per request instead.
+  int forward(int new_per_req, cudaStream_t s, void* out_x = nullptr, bool sample_rows = true) {
     const int d = dm.d_model, L = dm.n_layers, hd = dm.head_dim;
     const float eps = dm.rms_eps;
     const int rows = new_per_req * group();
@@ -221,8 +237,14 @@ struct ModelRT {
                                   s));
     }
     TRY(gemm_run(plm, s));
-    TRY(launch_argmax_reduce(amax_v, amax_i, plm.n_amax_blocks, rows_cap, bt.t_dev, rows_cap,
-                             bt.out_tok, nullptr, s));
+    if (sampling) {
+      if (sample_rows)
+        TRY(launch_sample_rows(logits, dm.vocab, bt.t_dev, rows_cap, bt.pos, bt.slot, inv_t, seed,
+                               lstat, bt.out_tok, s));
+    } else {
+      TRY(launch_argmax_reduce(amax_v, amax_i, plm.n_amax_blocks, rows_cap, bt.t_dev, rows_cap,
+                               bt.out_tok, nullptr, s));
+    }
     if (out_x)
       SPECTRE_CUDA_TRY(cudaMemcpyAsync(out_x, x, (size_t)rows_cap * d * 2,
                                        cudaMemcpyDeviceToDevice, s));
@@ -244,6 +266,10 @@ struct Engine {
   int graph_failed = 0;
   int* mode_host = nullptr;  // pinned
   int warmed = 0;
+  // rejection sampling (temperature > 0): draft q-store by output position
+  int qwin = 0;               // slots per request (positions mod qwin)
+  float* qstore = nullptr;    // [n_req][qwin][vocab] draft logits
+  float2* qstat = nullptr;    // [n_req][qwin] (max, sum exp)
 
   ~Engine() {
     if (exec_loop) cudaGraphExecDestroy(exec_loop);
@@ -304,6 +330,12 @@ struct Engine {
     st.trace.r_hat_ema = b.take<double>(R);
     st.trace.accepted_len_ema = b.take<double>(R);
     st.trace.r_star = b.take<double>(R);
+    if (st.sampling) {
+      st.samp_a = b.take<int>(n);
+      st.samp_bonus = b.take<int>(n);
+      qstore = b.take<float>((size_t)n * qwin * drf.dm.vocab);
+      qstat = b.take<float2>((size_t)n * qwin);
+    }
   }
 
   void configure(const SpectreModelDims& t, const SpectreModelWeights& tw,
@@ -344,6 +376,13 @@ struct Engine {
     st.ema_decay = c.ema_decay;
     st.fixed_l = c.fixed_threshold_l;
     st.use_handles = 0;
+    st.sampling = c.temperature > 0.0 ? 1 : 0;
+    qwin = 4 * c.gamma + 4;   // > every candidate-to-speculation position gap
+    for (ModelRT* m : {&tgt, &drf}) {
+      m->sampling = st.sampling;
+      m->inv_t = st.sampling ? (float)(1.0 / c.temperature) : 1.f;
+      m->seed = c.seed;
+    }
   }
 
   // ---- round pieces
@@ -351,7 +390,10 @@ struct Engine {
     TRY(launch_draft_prep(st, drf.bt, which, s));
     const int steps = which == 'O' ? cfg.gamma - 1 : cfg.gamma;
     for (int i = 0; i < steps; ++i) {
-      TRY(drf.forward(i == 0 ? draft_new_max : 1, s));
+      TRY(drf.forward(i == 0 ? draft_new_max : 1, s, nullptr, false));
+      if (st.sampling)
+        TRY(launch_draft_sample(st, drf.bt, drf.logits, drf.dm.vocab, drf.inv_t, qstore, qstat,
+                                qwin, s));
       TRY(launch_draft_append(st, drf.bt, which, i == steps - 1, s));
     }
     return SPECTRE_OK;
@@ -379,8 +421,15 @@ struct Engine {
     }
     TRY(verify_phase(s));
     if (mode == 'P') SPECTRE_CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
-    TRY(launch_accept(st, tgt.bt, s));
+    TRY(accept(s));
     return SPECTRE_OK;
+  }
+
+  int accept(cudaStream_t s) {
+    if (st.sampling)
+      TRY(launch_accept_sample(st, tgt.bt, tgt.logits, tgt.dm.vocab, tgt.inv_t, tgt.lstat, qstore,
+                               qstat, qwin, st.samp_a, st.samp_bonus, s));
+    return launch_accept(st, tgt.bt, s);
   }
 
   // Capture a conditional IF node at the current capture point of `s`, with
@@ -466,7 +515,7 @@ struct Engine {
         fail(e, "cudaStreamUpdateCaptureDependencies");
         break;
       }
-      if ((r = launch_accept(st, tgt.bt, s))) break;
+      if ((r = accept(s))) break;
     } while (0);
     if (capturing) {
       cudaGraph_t captured;

@@ -86,6 +86,9 @@ struct DecodeStateDev {
   RoundTraceDev trace;
   cudaGraphConditionalHandle h_ord, h_par, h_loop;
   int use_handles;
+  int sampling;          // 1: accept from samp_a / samp_bonus (rejection sampling)
+  int* samp_a;           // [n_req] accepted candidates
+  int* samp_bonus;       // [n_req] bonus / resampled token
 };
 
 // launchers (model_protocol.cu)
@@ -99,5 +102,15 @@ int launch_draft_append(const DecodeStateDev& st, const BatchDev& bt, int which,
                         cudaStream_t s);
 int launch_verify_prep(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);
 int launch_accept(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);
+// sampling.cu
+int launch_sample_rows(const float* logits, int V, const int* t_dev, int t_cap,
+                       const int* tok_pos, const int* tok_slot, float inv_t, uint64_t seed,
+                       float2* stats, int* out_tok, cudaStream_t s);
+int launch_draft_sample(const DecodeStateDev& st, const BatchDev& bt, const float* logits, int V,
+                        float inv_t, float* qstore, float2* qstat, int W, cudaStream_t s);
+int launch_accept_sample(const DecodeStateDev& st, const BatchDev& bt, const float* logits, int V,
+                         float inv_t, const float2* tstat, const float* qstore,
+                         const float2* qstat, int W, int* out_a, int* out_bonus,
+                         cudaStream_t s);
 
 }  // namespace spectre

@@ -384,8 +384,14 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
     uint64_t* com = s.committed + (size_t)b * s.out_len;
     int pos = s.pos[b];
     int a = 0;
-    while (a < m && cand[a] == (uint64_t)bt.out_tok[row0 + a]) ++a;
-    const uint64_t bonus = (uint64_t)bt.out_tok[row0 + a];
+    uint64_t bonus;
+    if (s.sampling) {   // rejection sampling outcome (sampling.cu:k_accept_sample)
+      a = s.samp_a[b];
+      bonus = (uint64_t)s.samp_bonus[b];
+    } else {            // greedy exact-prefix verification (oracle.py:99-107)
+      while (a < m && cand[a] == (uint64_t)bt.out_tok[row0 + a]) ++a;
+      bonus = (uint64_t)bt.out_tok[row0 + a];
+    }
     const int accepted_count = a + (kind == kCached ? 0 : 1);
     const int real = kind == kRepaired ? s.gamma : (kind == kCached ? m : 1);
     // this round's prepared segment (parallel mode): the draft's speculation

@@ -181,6 +181,7 @@ class DecodeSpec:
     ema_decay: float = 0.9
     fixed_threshold_l: float | None = None
     max_rounds: int | None = None
+    temperature: float = 0.0        # 0: greedy; > 0: speculative rejection sampling (config 3)
 
     def ctx_cap(self) -> int:
         need = self.prompt_len + self.output_len + 4 * self.gamma + 16
@@ -212,7 +213,8 @@ class SpectreEngine:
             max_rounds=self.max_rounds, ctx_cap=pair.ctx_cap,
             has_fixed_l=int(spec.fixed_threshold_l is not None), alpha=spec.alpha,
             t_target=spec.t_target, t_draft=spec.t_draft, ema_decay=spec.ema_decay,
-            fixed_threshold_l=float(spec.fixed_threshold_l or 0.0))
+            fixed_threshold_l=float(spec.fixed_threshold_l or 0.0),
+            temperature=float(spec.temperature))
         self._tdims = pair.target.spec.dims()
         self._ddims = pair.draft.spec.dims()
         self._tw = pair.target.struct()
