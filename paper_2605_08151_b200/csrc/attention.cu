@@ -548,7 +548,7 @@ static int launch_attn_t(const CUtensorMap& tk, const CUtensorMap& tv, AttnArgs 
   }();
   a.rb_max = (a.rb_max + MT - 1) / MT * MT;   // whole row blocks of MT m-tiles
   const int items = a.n_req * a.n_kv * (a.rb_max / MT) * a.split_max;
-  const int grid = std::min(items, per_sm * num_sms());
+  const int grid = cap_grid(std::min(items, per_sm * num_sms()));
   SPECTRE_LAUNCH_PDL("k_attn", k_attn<HD, MT, NG, NS>, dim3(grid), dim3(C::kThreads), C::kSmem,
                      s, tk, tv, a);
   return SPECTRE_OK;

@@ -4,11 +4,13 @@
 // (no host round trip per round), looped by a device-side WHILE node.
 //
 // Round DAG (one WHILE iteration):
-//   round_begin (controller) ──► IF(ordinary){ draft repair: prep, (γ-1)×[fwd, append] }
-//        └────────────────────────┬──────────────────────────────────────────────┘
-//                                 ├──► IF(parallel){ draft speculation: prep, γ×[fwd, append] }  (2nd branch)
-//                                 └──► verify_prep ─► target forward ─┐
-//                                                       accept ◄──────┘◄── (join)
+//   round_begin (controller) ─┬─► IF(ordinary){ draft repair (γ-1 steps) ─► verify }
+//                             ├─► IF(parallel){ fork: draft speculation (γ steps) ∥ verify; join }
+//                             └─► IF(ar){ verify }
+//                                        ─► accept (rejection-sampling pre-pass when T > 0)
+// In parallel rounds the draft and the target run with disjoint CTA budgets
+// (par_draft_ctas + par_target_ctas <= SMs) so their persistent kernels
+// co-reside on different SMs instead of time-slicing the GPU.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -177,8 +179,8 @@ struct ModelRT {
       TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kPartial, 1, 0, 0, 256));
       TRY(gemm_set_outputs(&plm, logits, nullptr, nullptr, nullptr, 0));
     } else {
-      TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, 256, sk_part,
-                    sk_flag));
+      // whole tiles per CTA (no stream-K): logits independent of the CTA budget
+      TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, 256));
       TRY(gemm_set_outputs(&plm, nullptr, amax_v, amax_i, nullptr, 0));
     }
     const uint64_t kv_rows = (uint64_t)L * n_req * dm.n_kv_heads * ctx_cap;
@@ -242,7 +244,7 @@ struct ModelRT {
         TRY(launch_sample_rows(logits, dm.vocab, bt.t_dev, rows_cap, bt.pos, bt.slot, inv_t, seed,
                                lstat, bt.out_tok, s));
     } else {
-      TRY(launch_argmax_reduce(amax_v, amax_i, plm.n_amax_blocks, rows_cap, bt.t_dev, rows_cap,
+      TRY(launch_argmax_reduce(amax_v, amax_i, cap_grid(plm.grid) * 8, rows_cap, bt.t_dev, rows_cap,
                                bt.out_tok, nullptr, s));
     }
     if (out_x)
@@ -266,6 +268,8 @@ struct Engine {
   int graph_failed = 0;
   int* mode_host = nullptr;  // pinned
   int warmed = 0;
+  int par_draft_ctas = 0, par_target_ctas = 0;   // parallel-round CTA budgets (0: whole GPU)
+  cudaStream_t s_cap2 = nullptr;
   // rejection sampling (temperature > 0): draft q-store by output position
   int qwin = 0;               // slots per request (positions mod qwin)
   float* qstore = nullptr;    // [n_req][qwin][vocab] draft logits
@@ -276,6 +280,7 @@ struct Engine {
     if (graph_loop) cudaGraphDestroy(graph_loop);
     if (s_draft) cudaStreamDestroy(s_draft);
     if (s_cap) cudaStreamDestroy(s_cap);
+    if (s_cap2) cudaStreamDestroy(s_cap2);
     if (s_main) cudaStreamDestroy(s_main);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
@@ -377,6 +382,8 @@ struct Engine {
     st.fixed_l = c.fixed_threshold_l;
     st.use_handles = 0;
     st.sampling = c.temperature > 0.0 ? 1 : 0;
+    if (const char* v = getenv("SPECTRE_PAR_DRAFT_CTAS")) par_draft_ctas = atoi(v);
+    if (const char* v = getenv("SPECTRE_PAR_TARGET_CTAS")) par_target_ctas = atoi(v);
     qwin = 4 * c.gamma + 4;   // > every candidate-to-speculation position gap
     for (ModelRT* m : {&tgt, &drf}) {
       m->sampling = st.sampling;
@@ -414,14 +421,28 @@ struct Engine {
     if (mode == 0) return SPECTRE_OK;
     if (mode == 'O') TRY(draft_phase('O', s));
     if (mode == 'P') {
-      SPECTRE_CUDA_TRY(cudaEventRecord(ev_fork, s));
-      SPECTRE_CUDA_TRY(cudaStreamWaitEvent(s_draft, ev_fork, 0));
-      TRY(draft_phase('P', s_draft));
-      SPECTRE_CUDA_TRY(cudaEventRecord(ev_join, s_draft));
+      TRY(parallel_phase(s, s_draft));
+    } else {
+      TRY(verify_phase(s));
     }
-    TRY(verify_phase(s));
-    if (mode == 'P') SPECTRE_CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
     TRY(accept(s));
+    return SPECTRE_OK;
+  }
+
+  // draft speculation on `sd` concurrent with the verify on `s`, disjoint CTA budgets
+  int parallel_phase(cudaStream_t s, cudaStream_t sd) {
+    SPECTRE_CUDA_TRY(cudaEventRecord(ev_fork, s));
+    SPECTRE_CUDA_TRY(cudaStreamWaitEvent(sd, ev_fork, 0));
+    {
+      CtaCapGuard g(par_draft_ctas);
+      TRY(draft_phase('P', sd));
+    }
+    SPECTRE_CUDA_TRY(cudaEventRecord(ev_join, sd));
+    {
+      CtaCapGuard g(par_target_ctas);
+      TRY(verify_phase(s));
+    }
+    SPECTRE_CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
     return SPECTRE_OK;
   }
 
@@ -475,10 +496,11 @@ struct Engine {
     do {
       cudaError_t e = cudaGraphCreate(&g, 0);
       if (e != cudaSuccess) { fail(e, "cudaGraphCreate"); break; }
-      cudaGraphConditionalHandle h_loop, h_ord, h_par;
+      cudaGraphConditionalHandle h_loop, h_ord, h_par, h_ar;
       if ((e = cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault)) ||
           (e = cudaGraphConditionalHandleCreate(&h_ord, g, 0, cudaGraphCondAssignDefault)) ||
-          (e = cudaGraphConditionalHandleCreate(&h_par, g, 0, cudaGraphCondAssignDefault))) {
+          (e = cudaGraphConditionalHandleCreate(&h_par, g, 0, cudaGraphCondAssignDefault)) ||
+          (e = cudaGraphConditionalHandleCreate(&h_ar, g, 0, cudaGraphCondAssignDefault))) {
         fail(e, "cudaGraphConditionalHandleCreate");
         break;
       }
@@ -493,6 +515,7 @@ struct Engine {
       st.h_loop = h_loop;
       st.h_ord = h_ord;
       st.h_par = h_par;
+      st.h_ar = h_ar;
       st.use_handles = 1;
       if ((e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
                                              cudaStreamCaptureModeRelaxed))) {
@@ -501,17 +524,21 @@ struct Engine {
       }
       capturing = true;
       if ((r = launch_round_begin(st, s))) break;
-      cudaGraphNode_t n_ord, n_par;
-      if ((r = add_if_node(s, h_ord, [&](cudaStream_t cs) { return draft_phase('O', cs); }, true,
-                           &n_ord)))
+      cudaGraphNode_t n_if[3];
+      // the three mode bodies hang off round_begin; exactly one runs
+      if ((r = add_if_node(s, h_ord, [&](cudaStream_t cs) {
+             if (int q = draft_phase('O', cs)) return q;
+             return verify_phase(cs);
+           }, false, &n_if[0])))
         break;
-      // the parallel branch hangs off the same point; the stream keeps going
-      if ((r = add_if_node(s, h_par, [&](cudaStream_t cs) { return draft_phase('P', cs); },
-                           false, &n_par)))
+      if ((r = add_if_node(s, h_par, [&](cudaStream_t cs) { return parallel_phase(cs, s_cap2); },
+                           false, &n_if[1])))
         break;
-      if ((r = verify_phase(s))) break;
-      if ((e = cudaStreamUpdateCaptureDependencies(s, &n_par, 1,
-                                                   cudaStreamAddCaptureDependencies))) {
+      if ((r = add_if_node(s, h_ar, [&](cudaStream_t cs) { return verify_phase(cs); }, false,
+                           &n_if[2])))
+        break;
+      if ((e = cudaStreamUpdateCaptureDependencies(s, n_if, 3,
+                                                   cudaStreamSetCaptureDependencies))) {
         fail(e, "cudaStreamUpdateCaptureDependencies");
         break;
       }
@@ -590,6 +617,7 @@ extern "C" void* spectre_engine_create(const SpectreModelDims* target,
       cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&e->ev_out, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithFlags(&e->s_cap, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&e->s_cap2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaMallocHost(&e->mode_host, sizeof(int)) != cudaSuccess) {

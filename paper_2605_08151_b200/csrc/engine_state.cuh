@@ -84,7 +84,7 @@ struct DecodeStateDev {
   uint64_t* cand_tok;    // [n_req][gamma + 1]
   CtrlDev* ctrl;
   RoundTraceDev trace;
-  cudaGraphConditionalHandle h_ord, h_par, h_loop;
+  cudaGraphConditionalHandle h_ord, h_par, h_ar, h_loop;
   int use_handles;
   int sampling;          // 1: accept from samp_a / samp_bonus (rejection sampling)
   int* samp_a;           // [n_req] accepted candidates

@@ -113,7 +113,9 @@ static int launch_one(const GemmPlan& p, cudaStream_t s) {
                                           kGemmSmemBytes));
     configured = true;
   }
-  SPECTRE_LAUNCH_PDL("gemm_bf16_swapab", kern, dim3(p.grid), dim3(kGemmThreads), kGemmSmemBytes,
+  if (p.args.stream_k && cap_grid(p.grid) != p.grid)
+    return arg_fail("gemm: stream-K plans need the whole grid");
+  SPECTRE_LAUNCH_PDL("gemm_bf16_swapab", kern, dim3(cap_grid(p.grid)), dim3(kGemmThreads), kGemmSmemBytes,
                      s, p.tmap_w, p.tmap_x, p.tmap_out, p.tmap_sk, p.args);
   return SPECTRE_OK;
 }

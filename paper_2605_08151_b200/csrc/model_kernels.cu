@@ -285,7 +285,7 @@ __global__ void k_rope_table(float2* rope, int ctx_cap, int hd, double theta) {
 constexpr int kSms = 148;
 int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void* E,
                          const float* w, float* h, void* x, int d, float eps, cudaStream_t s) {
-  SPECTRE_LAUNCH_PDL("k_embed_rmsnorm", k_embed_rmsnorm, dim3(std::min(t_cap, 2 * kSms)), dim3(256), 0, s, tok, t_dev,
+  SPECTRE_LAUNCH_PDL("k_embed_rmsnorm", k_embed_rmsnorm, dim3(cap_grid(std::min(t_cap, 2 * kSms))), dim3(256), 0, s, tok, t_dev,
                      reinterpret_cast<const __nv_bfloat16*>(E), w, h,
                      reinterpret_cast<__nv_bfloat16*>(x), d, eps);
   return SPECTRE_OK;
@@ -299,7 +299,7 @@ int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const i
   const int threads = nv < 512 ? ((nv + 31) / 32) * 32 : 512;
   const int vec = (nv + threads - 1) / threads;
   auto* xb = reinterpret_cast<__nv_bfloat16*>(x);
-  const dim3 grid(std::min(t_cap, 2 * kSms));
+  const dim3 grid(cap_grid(std::min(t_cap, 2 * kSms)));
   if (vec <= 1)
     SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<1>, grid, dim3(threads),
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
@@ -321,7 +321,7 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
   if (splits > kMaxSplits) return arg_fail("qkv_rope_kv: splits");
   const int pairs = (n_q + 2 * n_kv) * hd / 2;
   SPECTRE_LAUNCH_PDL("k_qkv_rope_kv", k_qkv_rope_kv,
-                     dim3(std::min(t_cap * ((pairs + 127) / 128), 8 * kSms)), dim3(128),
+                     dim3(cap_grid(std::min(t_cap * ((pairs + 127) / 128), 8 * kSms))), dim3(128),
                      0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
                      reinterpret_cast<const float2*>(rope), reinterpret_cast<__nv_bfloat16*>(q),
                      reinterpret_cast<__nv_bfloat16*>(kc), reinterpret_cast<__nv_bfloat16*>(vc),
@@ -332,7 +332,7 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
 int launch_argmax_reduce(const float* val, const int* idx, int n_tiles, int rows_cap,
                          const int* t_dev, int t_cap, int* out_tok, float* out_val,
                          cudaStream_t s) {
-  SPECTRE_LAUNCH_PDL("k_argmax_reduce", k_argmax_reduce, dim3(std::min(t_cap, 2 * kSms)), dim3(256), 0, s, val, idx,
+  SPECTRE_LAUNCH_PDL("k_argmax_reduce", k_argmax_reduce, dim3(cap_grid(std::min(t_cap, 2 * kSms))), dim3(256), 0, s, val, idx,
                      n_tiles, rows_cap, t_dev, out_tok, out_val);
   return SPECTRE_OK;
 }

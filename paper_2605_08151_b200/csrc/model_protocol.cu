@@ -169,6 +169,7 @@ __global__ void k_round_begin(DecodeStateDev s) {
   if (s.use_handles) {
     cudaGraphSetConditional(s.h_ord, mode == 'O' ? 1u : 0u);
     cudaGraphSetConditional(s.h_par, mode == 'P' ? 1u : 0u);
+    cudaGraphSetConditional(s.h_ar, mode == 'F' ? 1u : 0u);
   }
 }
 
@@ -461,7 +462,9 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
       if (!c.has_tD) { c.tD = td; c.has_tD = 1; } else { c.tD = ema_step(d, c.tD, td); }
     }
     // per-committed-token cost of each mode, normalised to the round shape
-    if (mode == 'P') {
+    // an all-PADDED parallel round is the one-off switch-over from ordinary
+    // (sim.py:455-458): its short verify is not the steady parallel round time
+    if (mode == 'P' && npad < P) {
       if (!c.has_tpar) { c.tpar = tr; c.has_tpar = 1; } else { c.tpar = ema_step(d, c.tpar, tr); }
     } else if (mode == 'O') {
       if (!c.has_tord) { c.tord = tr; c.has_tord = 1; } else { c.tord = ema_step(d, c.tord, tr); }

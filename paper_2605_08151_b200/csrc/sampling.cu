@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kSampThreads) k_accept_sample(
 int launch_sample_rows(const float* logits, int V, const int* t_dev, int t_cap,
                        const int* tok_pos, const int* tok_slot, float inv_t, uint64_t seed,
                        float2* stats, int* out_tok, cudaStream_t s) {
-  SPECTRE_LAUNCH_PDL("k_sample_rows", k_sample_rows, dim3(t_cap < 296 ? t_cap : 296),
+  SPECTRE_LAUNCH_PDL("k_sample_rows", k_sample_rows, dim3(cap_grid(t_cap < 296 ? t_cap : 296)),
                      dim3(kSampThreads), 0, s, logits, V, t_dev, tok_pos, tok_slot, inv_t, seed,
                      stats, out_tok);
   return SPECTRE_OK;
