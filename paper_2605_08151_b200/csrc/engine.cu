@@ -72,8 +72,16 @@ static int attn_chunk_default() {
   return (c >= 64 && c % 64 == 0 && c <= 8192) ? c : 1024;
 }
 
+static int jobs_per_cta() {
+  const char* v = getenv("SPECTRE_JOBS_PER_CTA");
+  const int j = v ? atoi(v) : 1;
+  return j < 1 ? 1 : (j > 4 ? 4 : j);
+}
+
 static int pick_splits(int n_tiles, int k_iters) {
-  int s = 148 / n_tiles;  // one wave of CTAs (1 CTA per SM: 512 TMEM columns)
+  // one wave of CTAs (1 CTA per SM) x jobs per CTA: with two or more jobs a
+  // CTA's epilogue overlaps its next job's mainloop (double-buffered TMEM)
+  int s = 148 * jobs_per_cta() / n_tiles;
   if (s > 12) s = 12;     // partial traffic grows with s (consumers unroll <= 12)
   if (s < 1) s = 1;
   while (s > 1 && k_iters / s < 3) --s;
@@ -87,6 +95,7 @@ struct ModelRT {
   int n_req = 0, rows_cap = 0, ctx_cap = 0, max_new = 1, split_max = 1, rb_cap = 1;
   int sp_qkv = 1, sp_o = 1, sp_d = 1;
   int tile_rows = 256;   // weight rows per GEMM CTA (128 for small-T models)
+  long long pf_cap = 0;   // L2 prefetch of the next GEMM's weights (bytes; measured: off)
   int attn_chunk = 128;
   float* h = nullptr;
   __nv_bfloat16 *x = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
@@ -182,6 +191,22 @@ struct ModelRT {
       // whole tiles per CTA (no stream-K): logits independent of the CTA budget
       TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, 256));
       TRY(gemm_set_outputs(&plm, nullptr, amax_v, amax_i, nullptr, 0));
+    }
+    // each GEMM prefetches the next GEMM's weights into L2 (capped: the
+    // next kernel's working set must not push them out before use)
+    if (const char* v = getenv("SPECTRE_L2_PREFETCH_MB")) pf_cap = (long long)atoi(v) << 20;
+    auto link = [&](GemmPlan& p, const void* w, long long bytes) {
+      p.args.pf_ptr = pf_cap > 0 ? w : nullptr;
+      p.args.pf_bytes = std::min(bytes, pf_cap) & ~15ll;
+    };
+    for (int l = 0; l < L; ++l) {
+      link(pq[l], bf(w.wo) + (size_t)l * d * qd, (long long)d * qd * 2);
+      link(po[l], bf(w.wgu) + (size_t)l * 2 * F * d, (long long)2 * F * d * 2);
+      link(pgu[l], bf(w.wd) + (size_t)l * d * F, (long long)d * F * 2);
+      if (l + 1 < L)
+        link(pd[l], bf(w.wqkv) + (size_t)(l + 1) * nqkv() * d, (long long)nqkv() * d * 2);
+      else
+        link(pd[l], w.lm_head, (long long)dm.vocab * d * 2);
     }
     const uint64_t kv_rows = (uint64_t)L * n_req * dm.n_kv_heads * ctx_cap;
     TRY(make_tmap_bf16(&tm_k, w.k_cache, dm.head_dim, kv_rows, 64, 64));

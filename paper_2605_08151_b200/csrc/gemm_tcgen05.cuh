@@ -74,6 +74,8 @@ struct GemmArgs {
   int* sk_flag;             // stream-K: [grid] segment-ready flags (self-resetting)
   unsigned long long* dbg;  // diagnostics: per-CTA [8] globaltimer stamps (nullptr: off)
   int diag;                 // diagnostics (timing only): 1 skip MMAs, 2 skip epilogue math
+  const void* pf_ptr;       // next GEMM's weights: prefetched into L2 while this one runs
+  long long pf_bytes;       //   (static data, so issued before griddepcontrol.wait)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -228,6 +230,16 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   const uint32_t tmem_base = *tmem_slot;
 
   const bool producer = (warp == 0 && lane == 0);
+  if (a.pf_ptr && a.pf_bytes > 0 && warp >= 2) {
+    // this CTA's share of the next GEMM's weights, one bulk prefetch per thread
+    const long long share = (a.pf_bytes / gridDim.x + 4095) & ~4095ll;
+    const long long c0 = share * blockIdx.x;
+    const long long per = (share / 256 + 15) & ~15ll;
+    const long long b0 = c0 + per * (threadIdx.x - 64);
+    const long long b1 = min(min(b0 + per, c0 + share), a.pf_bytes);
+    if (b1 > b0)
+      prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(a.pf_ptr) + b0, (uint32_t)(b1 - b0));
+  }
   if (!producer) {  // everyone but the TMA lane waits for the previous kernel now
     pdl_wait();
     pdl_trigger();
