@@ -60,6 +60,16 @@ inline int cap_grid(int g) {
   const int c = cta_cap_ref();
   return (c > 0 && g > c) ? c : g;
 }
+// Set while capturing/launching work that runs CONCURRENTLY with another
+// stream's kernels (parallel rounds): kernels with an in-kernel grid barrier
+// (fused split-K reductions) would deadlock if two of them each held part of
+// the GPU, so they fall back to separate reduction kernels.
+bool& no_grid_sync_ref();
+struct NoGridSyncGuard {
+  bool prev;
+  NoGridSyncGuard() : prev(no_grid_sync_ref()) { no_grid_sync_ref() = true; }
+  ~NoGridSyncGuard() { no_grid_sync_ref() = prev; }
+};
 struct CtaCapGuard {
   int prev;
   explicit CtaCapGuard(int c) : prev(cta_cap_ref()) { cta_cap_ref() = c; }

@@ -100,6 +100,8 @@ struct ModelRT {
   float* h = nullptr;
   __nv_bfloat16 *x = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
   float *part = nullptr, *att_o = nullptr, *att_ml = nullptr, *amax_v = nullptr;
+  int* gbar = nullptr;        // [2] grid barrier of this model's fused-post GEMMs
+  bool fuse_post = false;     // split-K reductions fused into the GEMMs (gemm_post.cuh; measured slower)
   float* sk_part = nullptr;   // stream-K segment partials (SwiGLU / lm_head GEMMs)
   int* sk_flag = nullptr;
   int sampling = 0;           // temperature > 0: lm_head writes fp32 logits
@@ -148,6 +150,7 @@ struct ModelRT {
     amax_i = b.take<int>((size_t)n_blocks * R);
     rope = b.take<float2>((size_t)ctx_cap * dm.head_dim / 2);
     sk_part = b.take<float>(gemm_sk_part_floats());
+    gbar = b.take<int>(2);
     sk_flag = b.take<int>(gemm_sk_grid());
     bt.tok = b.take<int>(R);
     bt.pos = b.take<int>(R);
@@ -199,6 +202,37 @@ struct ModelRT {
       p.args.pf_ptr = pf_cap > 0 ? w : nullptr;
       p.args.pf_bytes = std::min(bytes, pf_cap) & ~15ll;
     };
+    if (const char* v = getenv("SPECTRE_FUSE_POST")) fuse_post = atoi(v) != 0;
+    if (fuse_post) {
+      const size_t kv_layer = (size_t)n_req * dm.n_kv_heads * ctx_cap * dm.head_dim;
+      auto* kc = reinterpret_cast<__nv_bfloat16*>(w.k_cache);
+      auto* vc = reinterpret_cast<__nv_bfloat16*>(w.v_cache);
+      for (int l = 0; l < L; ++l) {
+        GemmPost& r = pq[l].args.post;
+        r.kind = kPostRope;
+        r.gbar = gbar;
+        r.tok_pos = bt.pos;
+        r.tok_slot = bt.slot;
+        r.rope = rope;
+        r.q = q;
+        r.kc = kc + l * kv_layer;
+        r.vc = vc + l * kv_layer;
+        r.n_q = dm.n_q_heads;
+        r.n_kv = dm.n_kv_heads;
+        r.hd = dm.head_dim;
+        r.ctx_cap = ctx_cap;
+        for (int which = 0; which < 2; ++which) {
+          GemmPost& z = which == 0 ? po[l].args.post : pd[l].args.post;
+          z.kind = kPostResid;
+          z.gbar = gbar;
+          z.h = h;
+          z.x = x;
+          z.eps = dm.rms_eps;
+          z.w = which == 0 ? w.mlp_norm + (size_t)l * d
+                           : (l + 1 < L ? w.attn_norm + (size_t)(l + 1) * d : w.final_norm);
+        }
+      }
+    }
     for (int l = 0; l < L; ++l) {
       link(pq[l], bf(w.wo) + (size_t)l * d * qd, (long long)d * qd * 2);
       link(po[l], bf(w.wgu) + (size_t)l * 2 * F * d, (long long)2 * F * d * 2);
@@ -249,19 +283,23 @@ struct ModelRT {
     TRY(launch_embed_rmsnorm(bt.tok, bt.t_dev, rows_cap, w.embed, w.attn_norm, h, x, d, eps, s));
     for (int l = 0; l < L; ++l) {
       TRY(gemm_run(pq[l], s));
-      TRY(launch_qkv_rope_kv(part, sp_qkv, rows_cap, bt.t_dev, rows_cap, bt.pos, bt.slot, rope,
-                             q, kc + l * kv_layer, vc + l * kv_layer, dm.n_q_heads,
-                             dm.n_kv_heads, hd, ctx_cap, s));
+      const bool fused = fuse_post && !no_grid_sync_ref();
+      if (!fused)
+        TRY(launch_qkv_rope_kv(part, sp_qkv, rows_cap, bt.t_dev, rows_cap, bt.pos, bt.slot,
+                               rope, q, kc + l * kv_layer, vc + l * kv_layer, dm.n_q_heads,
+                               dm.n_kv_heads, hd, ctx_cap, s));
       a.layer_row0 = l * n_req * dm.n_kv_heads * ctx_cap;
       TRY(launch_attention(tm_k, tm_v, a, hd, rows, s));
       TRY(gemm_run(po[l], s));
-      TRY(launch_residual_rmsnorm(part, sp_o, rows_cap, bt.t_dev, rows_cap,
-                                  w.mlp_norm + (size_t)l * d, h, x, d, eps, s));
+      if (!fused)
+        TRY(launch_residual_rmsnorm(part, sp_o, rows_cap, bt.t_dev, rows_cap,
+                                    w.mlp_norm + (size_t)l * d, h, x, d, eps, s));
       TRY(gemm_run(pgu[l], s));
       TRY(gemm_run(pd[l], s));
       const float* next = (l + 1 < L) ? w.attn_norm + (size_t)(l + 1) * d : w.final_norm;
-      TRY(launch_residual_rmsnorm(part, sp_d, rows_cap, bt.t_dev, rows_cap, next, h, x, d, eps,
-                                  s));
+      if (!fused)
+        TRY(launch_residual_rmsnorm(part, sp_d, rows_cap, bt.t_dev, rows_cap, next, h, x, d, eps,
+                                    s));
     }
     TRY(gemm_run(plm, s));
     if (sampling) {
@@ -456,6 +494,7 @@ struct Engine {
 
   // draft speculation on `sd` concurrent with the verify on `s`, disjoint CTA budgets
   int parallel_phase(cudaStream_t s, cudaStream_t sd) {
+    NoGridSyncGuard concurrent;   // draft and target kernels overlap on two streams
     SPECTRE_CUDA_TRY(cudaEventRecord(ev_fork, s));
     SPECTRE_CUDA_TRY(cudaStreamWaitEvent(sd, ev_fork, 0));
     {

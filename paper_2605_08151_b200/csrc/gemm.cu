@@ -178,7 +178,15 @@ int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_
   return SPECTRE_OK;
 }
 
-int gemm_run(const GemmPlan& p, cudaStream_t s) {
+int gemm_run(const GemmPlan& p0, cudaStream_t s) {
+  GemmPlan stripped;
+  const GemmPlan* pp = &p0;
+  if (p0.args.post.kind != kPostNone && no_grid_sync_ref()) {   // concurrent: no grid barrier
+    stripped = p0;
+    stripped.args.post.kind = kPostNone;
+    pp = &stripped;
+  }
+  const GemmPlan& p = *pp;
   if (p.bk == 64) {
     switch (p.epi) {
       case kPartial: return launch_one<kPartial, 64>(p, s);

@@ -42,6 +42,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "gemm_post.cuh"
 #include "ptx.cuh"
 
 namespace spectre {
@@ -76,6 +77,7 @@ struct GemmArgs {
   int diag;                 // diagnostics (timing only): 1 skip MMAs, 2 skip epilogue math
   const void* pf_ptr;       // next GEMM's weights: prefetched into L2 while this one runs
   long long pf_bytes;       //   (static data, so issued before griddepcontrol.wait)
+  GemmPost post;            // fused split-K reduction phase (gemm_post.cuh)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -564,7 +566,10 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       if (j.role != 2) ++amax_jobs;
       ++jn;
     }
-    if (issuer) bulk_wait_all();   // outputs complete before the grid does
+    if (issuer) {   // outputs complete (and visible to generic loads) before the grid does
+      bulk_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     if (kEpi == kArgmax && !(a.diag & 2)) {
       // every (CTA, warp) slot of every live token is defined: fill the tokens
       // this warp never covered (no job, or the other group's chunks of a
@@ -581,6 +586,14 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   }
   tc_fence_before();
   __syncthreads();
+  if (kEpi == kPartial && a.post.kind != kPostNone) {
+    // every CTA's partials are in global memory: reduce them in this grid
+    // 40 floats in the (dynamic) barrier area, past the mbarriers and the TMEM slot
+    float* post_sh = reinterpret_cast<float*>(smem + kGemmPipeBytes + kGemmStageOut + 512);
+    post_grid_sync(a.post.gbar);
+    if (a.post.kind == kPostRope) post_rope(a.post, a.part, a.splits, a.rows_cap, T);
+    else post_resid(a.post, a.part, a.splits, a.rows_cap, T, a.N, post_sh);
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);
