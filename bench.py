@@ -151,7 +151,8 @@ def run_ours(args):
     dev_index = local
     B, g = args.batch, args.gamma
     spec_kw = dict(n_req=B, gamma=g, output_len=args.out_len, prompt_len=args.prompt_len,
-                   alpha=args.alpha, seed=args.seed + rank, controller=args.controller)
+                   alpha=args.alpha, seed=args.seed + rank, controller=args.controller,
+                   temperature=args.temperature)
     base = M.DecodeSpec(**spec_kw)
     pair = M.build_pair(M.LLAMA_31_8B, M.LLAMA_32_1B, n_req=B, ctx_cap=base.ctx_cap(),
                         seed=args.seed, target_branch=args.branch, draft_branch=args.branch)
@@ -258,8 +259,13 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic prompts (TokenStreamOracle prompt stream mod V), random-init "
                     "coupled weights",
-            "config": {"workload": "C2: llama-3.1-8b-shape target / llama-3.2-1b-shape draft, "
-                                   "B=64/GPU, gamma=4, prompt 128, output 1024, greedy",
+            "config": {"workload": (f"C2: llama-3.1-8b-shape target / llama-3.2-1b-shape draft, "
+                                    f"B={B}/GPU, gamma={g}, prompt {args.prompt_len}, output "
+                                    f"{args.out_len}, greedy" if args.temperature <= 0 else
+                                    f"C3: llama-3.1-8b-shape target / llama-3.2-1b-shape draft, "
+                                    f"B={B}/GPU, gamma={g}, prompt {args.prompt_len}, output "
+                                    f"{args.out_len}, T={args.temperature} rejection sampling"),
+                       "temperature": args.temperature,
                        "variant": args.variant, "batch_per_gpu": B, "gamma": g,
                        "output_len": args.out_len, "prompt_len": args.prompt_len,
                        "draft_alpha": args.alpha, "branch_scale": args.branch,
@@ -416,6 +422,8 @@ def main():
                     help="reference arm: agreement rate of the synthetic pair")
     ap.add_argument("--branch", type=float, default=0.004)
     ap.add_argument("--controller", default="round")
+    ap.add_argument("--temperature", type=float, default=0.0,
+                    help="0: greedy (C2); > 0: speculative rejection sampling (C3)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
