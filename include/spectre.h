@@ -221,7 +221,13 @@ typedef struct SpectreDecodeConfig {
   double fixed_threshold_l;
   double temperature;       /* 0: greedy verification; > 0: speculative rejection
                                sampling at this temperature (config 3) */
+  int32_t role;             /* SPECTRE_ROLE_*: both models, or one side of a
+                               disaggregated pair (config 5) */
 } SpectreDecodeConfig;
+
+#define SPECTRE_ROLE_BOTH 0
+#define SPECTRE_ROLE_TARGET 1   /* verify side: controller, assembly, verify, accept */
+#define SPECTRE_ROLE_DRAFT 2    /* draft server: sync / rollback, speculation */
 
 size_t spectre_engine_workspace_bytes(const SpectreModelDims* target,
                                       const SpectreModelDims* draft,
@@ -232,6 +238,27 @@ void* spectre_engine_create(const SpectreModelDims* target, const SpectreModelWe
                             const SpectreDecodeConfig* cfg, void* workspace,
                             size_t workspace_bytes);
 int spectre_engine_destroy(void* engine);
+
+/* Disaggregated rounds (config 5: draft on its own GPU, target replicas on
+ * others; the reference's draft server / target endpoints, draft_engine.py /
+ * target_engine.py, joined by sim.py's channels).  The host drives one
+ * round as BEGIN (target: controller, returns the mode) -> exchange
+ * target->draft -> DRAFT (draft server) ∥ VERIFY (target) -> exchange
+ * draft->target -> ACCEPT (target).  Returns the mode for BEGIN. */
+#define SPECTRE_STEP_BEGIN 0
+#define SPECTRE_STEP_DRAFT 1
+#define SPECTRE_STEP_VERIFY 2
+#define SPECTRE_STEP_ACCEPT 3
+int spectre_engine_step(void* engine, int32_t step, int32_t mode, void* stream);
+/* Copy the per-request state one side needs from the other for requests
+ * [src_req0, src_req0+n) of `src` into [dst_req0, ...) of `dst` (peer copies
+ * when the engines live on different GPUs).  direction 0: target -> draft
+ * (mode, committed tokens, positions, cache flags); 1: draft -> target
+ * (draft history window, generation counters, draft timing). */
+int spectre_engine_exchange(void* src, void* dst, int32_t direction, int32_t src_req0,
+                            int32_t dst_req0, int32_t n, void* stream);
+/* Enable direct peer access between two GPUs (both directions; idempotent). */
+int spectre_enable_peer_access(int32_t dev_a, int32_t dev_b);
 /* Prefill both models with prompts [n_req][prompt_len] (device int32) and
  * commit output token 0 (target greedy) — admission (target_engine.py:105-126). */
 int spectre_engine_prefill(void* engine, const int32_t* prompts, void* stream);

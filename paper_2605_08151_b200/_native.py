@@ -106,7 +106,8 @@ class DecodeConfig(C.Structure):
                 ("controller", C.c_int32), ("r_kind", C.c_int32), ("max_rounds", C.c_int32),
                 ("ctx_cap", C.c_int32), ("has_fixed_l", C.c_int32), ("alpha", C.c_double),
                 ("t_target", C.c_double), ("t_draft", C.c_double), ("ema_decay", C.c_double),
-                ("fixed_threshold_l", C.c_double), ("temperature", C.c_double)]
+                ("fixed_threshold_l", C.c_double), ("temperature", C.c_double),
+                ("role", C.c_int32)]
 
 
 TRACE_FIELDS = ("mode", "participants", "delta", "n_roll", "content_sum", "content_n",
@@ -123,6 +124,9 @@ def _bind_model(L) -> None:
     _sig(L, "spectre_gemm_bf16", C.c_int,
          [_P, _P, _P, i32, i32, i32, i32, i32, i32, _P, _P, _P, _P, i32, i32, _P])
     _sig(L, "spectre_gemm_argmax_blocks", i32, [i32, i32])
+    _sig(L, "spectre_engine_step", C.c_int, [_P, i32, i32, _P])
+    _sig(L, "spectre_engine_exchange", C.c_int, [_P, _P, i32, i32, i32, i32, _P])
+    _sig(L, "spectre_enable_peer_access", C.c_int, [i32, i32])
     _sig(L, "spectre_engine_workspace_bytes", C.c_size_t,
          [C.POINTER(ModelDims), C.POINTER(ModelDims), C.POINTER(DecodeConfig)])
     _sig(L, "spectre_engine_create", C.c_void_p,

@@ -332,6 +332,7 @@ struct Engine {
   int* mode_host = nullptr;  // pinned
   int warmed = 0;
   int par_draft_ctas = 0, par_target_ctas = 0;   // parallel-round CTA budgets (0: whole GPU)
+  int device = 0;
   cudaStream_t s_cap2 = nullptr;
   // rejection sampling (temperature > 0): draft q-store by output position
   int qwin = 0;               // slots per request (positions mod qwin)
@@ -660,6 +661,10 @@ extern "C" void* spectre_engine_create(const SpectreModelDims* target,
     arg_fail("spectre_engine_create: dims / pointers");
     return nullptr;
   }
+  if (cfg->role < SPECTRE_ROLE_BOTH || cfg->role > SPECTRE_ROLE_DRAFT) {
+    arg_fail("spectre_engine_create: role");
+    return nullptr;
+  }
   if (cfg->n_req < 1 || cfg->n_req > 1024 || cfg->gamma < 1 || cfg->gamma > 16 ||
       cfg->output_len < 2 || cfg->prompt_len < 1 || cfg->max_rounds < 1 ||
       cfg->ctx_cap < cfg->prompt_len + cfg->output_len + 4 * cfg->gamma + 16 ||
@@ -675,7 +680,10 @@ extern "C" void* spectre_engine_create(const SpectreModelDims* target,
     arg_fail("spectre_engine_create: workspace too small");
     return nullptr;
   }
-  if (e->tgt.plan() || e->drf.plan()) return nullptr;
+  if ((cfg->role != SPECTRE_ROLE_DRAFT && e->tgt.plan()) ||
+      (cfg->role != SPECTRE_ROLE_TARGET && e->drf.plan()))
+    return nullptr;
+  cudaGetDevice(&e->device);
   if (cudaStreamCreateWithFlags(&e->s_draft, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&e->s_main, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming) != cudaSuccess ||
@@ -710,6 +718,9 @@ extern "C" int spectre_engine_prefill(void* engine, const int32_t* prompts, void
   cudaStream_t s = as_stream(stream);
   const int P = e->cfg.prompt_len, cs = e->prefill_cs;
   for (ModelRT* m : {&e->drf, &e->tgt}) {
+    if ((m == &e->drf && e->cfg.role == SPECTRE_ROLE_TARGET) ||
+        (m == &e->tgt && e->cfg.role == SPECTRE_ROLE_DRAFT))
+      continue;   // disaggregated: this side holds only one model
     for (int c0 = 0; c0 < P; c0 += cs) {
       TRY(launch_prefill_batch(prompts, P, e->cfg.n_req, c0, cs, m->bt, s));
       TRY(m->forward(cs, s));
@@ -858,5 +869,97 @@ extern "C" int spectre_engine_forward(void* engine, int32_t which, const int32_t
   TRY(m.forward(max_new, s, out_x));
   if (T > 0) SPECTRE_CUDA_TRY(d2d(out_tok, m.bt.out_tok, (size_t)T * 4));
   SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
+  return SPECTRE_OK;
+}
+
+extern "C" int spectre_engine_step(void* engine, int32_t step, int32_t mode, void* stream) {
+  auto* e = reinterpret_cast<Engine*>(engine);
+  if (!e) return arg_fail("spectre_engine_step");
+  cudaStream_t s = as_stream(stream);
+  switch (step) {
+    case SPECTRE_STEP_BEGIN: {
+      TRY(launch_round_begin(e->st, s));
+      SPECTRE_CUDA_TRY(cudaMemcpyAsync(e->mode_host, &e->st.ctrl->mode, sizeof(int),
+                                       cudaMemcpyDeviceToHost, s));
+      SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
+      return *e->mode_host;
+    }
+    case SPECTRE_STEP_DRAFT:
+      if (mode == 'O' || mode == 'P') TRY(e->draft_phase(mode, s));
+      return SPECTRE_OK;
+    case SPECTRE_STEP_VERIFY:
+      TRY(e->verify_phase(s));
+      return SPECTRE_OK;
+    case SPECTRE_STEP_ACCEPT:
+      TRY(e->accept(s));
+      return SPECTRE_OK;
+    default:
+      return arg_fail("spectre_engine_step: step");
+  }
+}
+
+extern "C" int spectre_engine_exchange(void* src, void* dst, int32_t direction,
+                                       int32_t src_req0, int32_t dst_req0, int32_t n,
+                                       void* stream) {
+  auto* a = reinterpret_cast<Engine*>(src);
+  auto* b = reinterpret_cast<Engine*>(dst);
+  if (!a || !b || n < 0 || src_req0 < 0 || dst_req0 < 0 || src_req0 + n > a->cfg.n_req ||
+      dst_req0 + n > b->cfg.n_req || a->cfg.output_len != b->cfg.output_len ||
+      a->st.hist_cap != b->st.hist_cap || a->cfg.gamma != b->cfg.gamma)
+    return arg_fail("spectre_engine_exchange");
+  cudaStream_t s = as_stream(stream);
+  // cudaMemcpyDefault: unified addressing routes peer copies over NVLink
+  auto cp = [&](void* d, const void* sp, size_t bytes) {
+    return cudaMemcpyAsync(d, sp, bytes, cudaMemcpyDefault, s);
+  };
+  auto ints = [&](int* d, const int* sp) {
+    return cp(d + dst_req0, sp + src_req0, (size_t)n * sizeof(int));
+  };
+  if (direction == 0) {   // target -> draft: what the draft server's sync needs
+    SPECTRE_CUDA_TRY(cp(&b->st.ctrl->mode, &a->st.ctrl->mode, sizeof(int)));
+    SPECTRE_CUDA_TRY(ints(b->st.pos, a->st.pos));
+    SPECTRE_CUDA_TRY(ints(b->st.done, a->st.done));
+    SPECTRE_CUDA_TRY(ints(b->st.cached_len, a->st.cached_len));
+    SPECTRE_CUDA_TRY(ints(b->st.in_rollback, a->st.in_rollback));
+    SPECTRE_CUDA_TRY(cp(b->st.committed + (size_t)dst_req0 * b->cfg.output_len,
+                        a->st.committed + (size_t)src_req0 * a->cfg.output_len,
+                        (size_t)n * a->cfg.output_len * sizeof(uint64_t)));
+  } else if (direction == 1) {   // draft -> target: speculation + draft timing
+    SPECTRE_CUDA_TRY(cp(b->st.hist + (size_t)dst_req0 * b->st.hist_cap,
+                        a->st.hist + (size_t)src_req0 * a->st.hist_cap,
+                        (size_t)n * a->st.hist_cap * sizeof(uint64_t)));
+    SPECTRE_CUDA_TRY(ints(b->st.hist_len, a->st.hist_len));
+    SPECTRE_CUDA_TRY(ints(b->st.gen_count, a->st.gen_count));
+    SPECTRE_CUDA_TRY(ints(b->st.gen_done, a->st.gen_done));
+    SPECTRE_CUDA_TRY(ints(b->st.gen_start, a->st.gen_start));
+    // draft phase timing only: the target's own clock fields stay untouched
+    SPECTRE_CUDA_TRY(cp(&b->st.ctrl->t_draft_begin, &a->st.ctrl->t_draft_begin,
+                        2 * sizeof(long long)));
+    SPECTRE_CUDA_TRY(cp(&b->st.ctrl->draft_steps, &a->st.ctrl->draft_steps, sizeof(int)));
+  } else {
+    return arg_fail("spectre_engine_exchange: direction");
+  }
+  return SPECTRE_OK;
+}
+
+// Direct NVLink access between the GPUs of a disaggregated pair (idempotent).
+extern "C" int spectre_enable_peer_access(int32_t dev_a, int32_t dev_b) {
+  if (dev_a == dev_b) return SPECTRE_OK;
+  int can_ab = 0, can_ba = 0;
+  SPECTRE_CUDA_TRY(cudaDeviceCanAccessPeer(&can_ab, dev_a, dev_b));
+  SPECTRE_CUDA_TRY(cudaDeviceCanAccessPeer(&can_ba, dev_b, dev_a));
+  if (!can_ab || !can_ba) return arg_fail("spectre_enable_peer_access: no peer path");
+  int cur = 0;
+  SPECTRE_CUDA_TRY(cudaGetDevice(&cur));
+  for (int k = 0; k < 2; ++k) {
+    SPECTRE_CUDA_TRY(cudaSetDevice(k == 0 ? dev_a : dev_b));
+    cudaError_t e = cudaDeviceEnablePeerAccess(k == 0 ? dev_b : dev_a, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else if (e != cudaSuccess) {
+      cudaSetDevice(cur);
+      return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    }
+  }
+  SPECTRE_CUDA_TRY(cudaSetDevice(cur));
   return SPECTRE_OK;
 }

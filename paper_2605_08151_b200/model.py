@@ -192,10 +192,15 @@ _VAR = {PolicyVariant.AR: 0, PolicyVariant.ORDINARY: 1, PolicyVariant.PARALLEL: 
         PolicyVariant.HYBRID: 3}
 
 
-class SpectreEngine:
-    """Owns the libspectre engine handle and its workspace."""
+ROLES = {"both": 0, "target": 1, "draft": 2}
 
-    def __init__(self, pair: ModelPair, spec: DecodeSpec, variant: PolicyVariant | str):
+
+class SpectreEngine:
+    """Owns the libspectre engine handle and its workspace.  role "target" /
+    "draft" builds one side of a disaggregated pair (config 5, see disagg.py)."""
+
+    def __init__(self, pair: ModelPair, spec: DecodeSpec, variant: PolicyVariant | str,
+                 role: str = "both"):
         torch = _native.require_cuda()
         L = _native.lib()
         if isinstance(variant, str):
@@ -214,7 +219,8 @@ class SpectreEngine:
             has_fixed_l=int(spec.fixed_threshold_l is not None), alpha=spec.alpha,
             t_target=spec.t_target, t_draft=spec.t_draft, ema_decay=spec.ema_decay,
             fixed_threshold_l=float(spec.fixed_threshold_l or 0.0),
-            temperature=float(spec.temperature))
+            temperature=float(spec.temperature), role=ROLES[role])
+        self.role = role
         self._tdims = pair.target.spec.dims()
         self._ddims = pair.draft.spec.dims()
         self._tw = pair.target.struct()
@@ -256,6 +262,13 @@ class SpectreEngine:
             int(use_graph), C.byref(n) if sync else None, _native.stream_ptr(stream)),
             "spectre_engine_run")
         return n.value if sync else None
+
+    def step(self, step: int, mode: int = 0, stream=None) -> int:
+        """One piece of a host-driven round (disaggregated pairs); BEGIN returns the mode."""
+        r = _native.lib().spectre_engine_step(self.handle, step, mode, _native.stream_ptr(stream))
+        if r < 0:
+            _native.check(r, "spectre_engine_step")
+        return r
 
     def graph_status(self) -> int:
         return _native.lib().spectre_engine_graph_status(self.handle)
