@@ -40,18 +40,27 @@ struct GemmPost {
 
 constexpr int kPostMaxSplits = 12;
 
-// All CTAs of the grid: arrival counter + generation flip (one thread per CTA).
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// All CTAs of the grid: arrival counter + generation flip (one thread per
+// CTA).  Waiters poll with plain acquire loads — read-modify-write polling
+// serialises 148 CTAs on one L2 slice.
 __device__ __forceinline__ void post_grid_sync(int* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int gen = atomicAdd(bar + 1, 0);
+    const int gen = ld_acquire_gpu(bar + 1);
     __threadfence();
     if (atomicAdd(bar, 1) == (int)gridDim.x - 1) {
       atomicExch(bar, 0);
       __threadfence();
       atomicAdd(bar + 1, 1);
     } else {
-      while (atomicAdd(bar + 1, 0) == gen) __nanosleep(64);
+      while (ld_acquire_gpu(bar + 1) == gen) {
+      }
     }
     __threadfence();
   }

@@ -409,7 +409,8 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
           if (sched.has_iters(cc) && ncl < kSkMaxSeg - 1) cl[ncl++] = cc;
         if (etid == 0) {   // one poller per owner (no polling storm on the flag lines)
           for (int i = 0; i < ncl; ++i)
-            while (atomicAdd(a.sk_flag + cl[i], 0) == 0) __nanosleep(128);
+            while (ld_acquire_gpu(a.sk_flag + cl[i]) == 0) {
+            }
           __threadfence();
         }
         asm volatile("bar.sync 3, 256;" ::: "memory");
