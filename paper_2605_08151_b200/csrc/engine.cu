@@ -27,6 +27,8 @@ namespace spectre {
 
 int launch_attention(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, int hd,
                      int rows_per_req, cudaStream_t s);
+int launch_attention_w(const CUtensorMap& tk32, const CUtensorMap& tv32, const AttnArgs& a,
+                       int hd, int rows_per_req, cudaStream_t s);
 int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void* E,
                          const float* w, float* h, void* x, int d, float eps, cudaStream_t s);
 int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const int* t_dev,
@@ -113,6 +115,8 @@ struct ModelRT {
   int* amax_i = nullptr;
   float2* rope = nullptr;
   CUtensorMap tm_k{}, tm_v{};   // whole K / V cache as [L*slots*n_kv*ctx_cap][hd] rows
+  CUtensorMap tm_k32{}, tm_v32{};   // same, 32-key boxes (warp-per-item attention)
+  bool attn_warp = true;            // warp-per-item attention (SPECTRE_ATTN_WARP=0: CTA items)
   BatchDev bt{};
   std::vector<GemmPlan> pq, po, pgu, pd;
   GemmPlan plm{};
@@ -245,6 +249,9 @@ struct ModelRT {
     const uint64_t kv_rows = (uint64_t)L * n_req * dm.n_kv_heads * ctx_cap;
     TRY(make_tmap_bf16(&tm_k, w.k_cache, dm.head_dim, kv_rows, 64, 64));
     TRY(make_tmap_bf16(&tm_v, w.v_cache, dm.head_dim, kv_rows, 64, 64));
+    TRY(make_tmap_bf16(&tm_k32, w.k_cache, dm.head_dim, kv_rows, 32, 64));
+    TRY(make_tmap_bf16(&tm_v32, w.v_cache, dm.head_dim, kv_rows, 32, 64));
+    if (const char* v = getenv("SPECTRE_ATTN_WARP")) attn_warp = atoi(v) != 0;
     plm.args.t_dev = bt.t_dev;
     return SPECTRE_OK;
   }
@@ -289,7 +296,8 @@ struct ModelRT {
                                rope, q, kc + l * kv_layer, vc + l * kv_layer, dm.n_q_heads,
                                dm.n_kv_heads, hd, ctx_cap, s));
       a.layer_row0 = l * n_req * dm.n_kv_heads * ctx_cap;
-      TRY(launch_attention(tm_k, tm_v, a, hd, rows, s));
+      if (attn_warp) TRY(launch_attention_w(tm_k32, tm_v32, a, hd, rows, s));
+      else TRY(launch_attention(tm_k, tm_v, a, hd, rows, s));
       TRY(gemm_run(po[l], s));
       if (!fused)
         TRY(launch_residual_rmsnorm(part, sp_o, rows_cap, bt.t_dev, rows_cap,
