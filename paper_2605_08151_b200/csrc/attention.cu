@@ -545,11 +545,14 @@ __device__ __forceinline__ uint32_t swz32(int key, int col) {   // 32-row boxes
   return (uint32_t)((col >> 6) * (32 * 128) + key * 128 + ((((col & 63) >> 3) ^ (key & 7)) << 4));
 }
 
-template <int HD, int NWARP, int NS>
+template <int HD, int NWARP, int NS, int NP>
 __global__ void __launch_bounds__(NWARP * 32, 1)
 k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
          AttnArgs a) {
+  // NP warps per item: warp `sub` of the group takes the stages whose
+  // absolute index is sub mod NP (batch invariant), merged at the end.
   using C = AttnWCfg<HD, NWARP, NS>;
+  static_assert(NWARP % NP == 0, "warp groups");
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -572,12 +575,13 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
   const int n_rblk = a.rb_max;                 // 16-row m-tiles per request
   const int n_pairs = a.n_req * a.n_kv;
   const int n_items = n_pairs * a.split_max * n_rblk;
-  const int slots = gridDim.x * NWARP;
+  const int slots = gridDim.x * (NWARP / NP);
   const int g8 = lane >> 2, tq = lane & 3;
+  const int pw = warp / NP, sub = warp % NP;
   int g = 0;                                    // this warp's stage counter
   bool waited = false;
 
-  for (int item = warp * gridDim.x + blockIdx.x; item < n_items; item += slots) {
+  for (int item = pw * gridDim.x + blockIdx.x; item < n_items; item += slots) {
     // (row block, split, request, kv head), row block slowest
     const int rblk = item / (n_pairs * a.split_max);
     int r = item % (n_pairs * a.split_max);
@@ -596,14 +600,15 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
     const int c1 = min(c0 + a.chunk, kv_len);
     const int p_max = p0 + (min(rows_total, row_lo + 16) - 1) / group;
     const int c_end = min(c1, p_max + 1);        // keys past every row's position are no-ops
-    const int n_stages = (c_end - c0 + C::kKeys - 1) / C::kKeys;
+    const int n_all = (c_end - c0 + C::kKeys - 1) / C::kKeys;   // stages of the item
+    const int n_stages = (n_all - sub + NP - 1) / NP;             // this warp's share
     const int row0 = a.layer_row0 + (a.slot[b] * a.n_kv + kvh) * a.ctx_cap;
     const int g_item = g;
-    auto issue = [&](int st) {   // stage st of this item -> slot (g_item + st) % NS
+    auto issue = [&](int st) {   // local stage st (item stage st*NP+sub) -> slot (g_item+st)%NS
       const int gg = g_item + st;
       const int sl = gg % NS;
       uint8_t* dst = ring + sl * C::kStageBytes;
-      const int k0 = c0 + st * C::kKeys;
+      const int k0 = c0 + (st * NP + sub) * C::kKeys;
       mbar_arrive_expect_tx(&full[sl], C::kStageBytes);
 #pragma unroll
       for (int bx = 0; bx < C::kBoxes; ++bx) {
@@ -616,7 +621,7 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
     if (!waited) {
       // keys below pos0 were written by earlier rounds: stream them before
       // the QKV epilogue kernel (which writes the new keys and Q) finishes
-      while (pre < NS && pre < n_stages && c0 + (pre + 1) * C::kKeys <= p0) ++pre;
+      while (pre < NS && pre < n_stages && c0 + (pre * NP + sub + 1) * C::kKeys <= p0) ++pre;
       if (lane == 0)
         for (int st = 0; st < pre; ++st) issue(st);
       pdl_wait();
@@ -665,7 +670,7 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
       mbar_wait(&full[sl], (uint32_t)(g / NS) & 1u);
       const uint32_t sK = smem_u32(ring + sl * C::kStageBytes);
       const uint32_t sV = sK + C::kBoxes * C::kBoxBytes;
-      const int kb = c0 + st * C::kKeys;
+      const int kb = c0 + (st * NP + sub) * C::kKeys;
 #pragma unroll
       for (int half16 = 0; half16 < 2; ++half16) {   // two 16-key steps per stage
         const int kofs = half16 * 16;
@@ -739,6 +744,43 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
       if (lane == 0 && st + NS < n_stages) issue(st + NS);
     }
     g = g_item + n_stages;
+    if (NP == 2) {
+      // fold warp 1's state into warp 0's (same lane layout) through warp 1's
+      // now idle ring, fixed order (stages of parity 0, then parity 1)
+      float* xch = reinterpret_cast<float*>(smem + (pw * NP + 1) * C::kWarpRing);
+      if (sub == 1) {
+#pragma unroll
+        for (int n = 0; n < HD / 8; ++n)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) xch[(n * 4 + e) * 32 + lane] = o[n][e];
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+          xch[(HD / 2 + hr * 2) * 32 + lane] = mrow[hr];
+          xch[(HD / 2 + hr * 2 + 1) * 32 + lane] = lrow[hr];
+        }
+      }
+      bar_named(1 + pw, 64);
+      if (sub == 0) {
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+          const float m1 = xch[(HD / 2 + hr * 2) * 32 + lane];
+          const float l1 = xch[(HD / 2 + hr * 2 + 1) * 32 + lane];
+          const float M = fmaxf(mrow[hr], m1);
+          const float f0 = (mrow[hr] == -INFINITY) ? 0.f : exp2f(mrow[hr] - M);
+          const float f1 = (m1 == -INFINITY) ? 0.f : exp2f(m1 - M);
+#pragma unroll
+          for (int n = 0; n < HD / 8; ++n) {
+            o[n][hr * 2] = o[n][hr * 2] * f0 + xch[(n * 4 + hr * 2) * 32 + lane] * f1;
+            o[n][hr * 2 + 1] = o[n][hr * 2 + 1] * f0 + xch[(n * 4 + hr * 2 + 1) * 32 + lane] * f1;
+          }
+          lrow[hr] = lrow[hr] * f0 + l1 * f1;
+          mrow[hr] = M;
+        }
+      }
+      bar_named(1 + pw, 64);   // warp 1's ring is free again
+      fence_proxy_async_smem();
+      if (sub == 1) continue;
+    }
     // ---- output: this warp holds the whole split of its 16 rows
     const int n_split = (kv_len + a.chunk - 1) / a.chunk;
     const int qoff = a.q_off[b];
@@ -871,19 +913,19 @@ static int attn_mtiles_cfg() {
   return v;
 }
 
-template <int HD, int NWARP, int NS>
+template <int HD, int NWARP, int NS, int NP>
 static int launch_attn_w_t(const CUtensorMap& tk, const CUtensorMap& tv, AttnArgs a,
                            int rows_per_req, cudaStream_t s) {
   using C = AttnWCfg<HD, NWARP, NS>;
   static_assert(C::kSmem <= 232448, "attention smem");
   static bool cfg = false;
   if (!cfg) {
-    SPECTRE_CUDA_TRY(cudaFuncSetAttribute(k_attn_w<HD, NWARP, NS>,
+    SPECTRE_CUDA_TRY(cudaFuncSetAttribute(k_attn_w<HD, NWARP, NS, NP>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     cfg = true;
   }
   a.rb_max = (rows_per_req + 15) / 16;
-  SPECTRE_LAUNCH_PDL("k_attn_w", k_attn_w<HD, NWARP, NS>, dim3(cap_grid(num_sms())),
+  SPECTRE_LAUNCH_PDL("k_attn_w", k_attn_w<HD, NWARP, NS, NP>, dim3(cap_grid(num_sms())),
                      dim3(NWARP * 32), C::kSmem, s, tk, tv, a);
   return SPECTRE_OK;
 }
@@ -892,15 +934,14 @@ static int launch_attn_w_t(const CUtensorMap& tk, const CUtensorMap& tv, AttnArg
 int launch_attention_w(const CUtensorMap& tk32, const CUtensorMap& tv32, const AttnArgs& a,
                        int hd, int rows_per_req, cudaStream_t s) {
   if (a.chunk % 64 || a.chunk <= 0) return arg_fail("attention: chunk must be a multiple of 64");
-  if (hd == 128) return launch_attn_w_t<128, 4, 3>(tk32, tv32, a, rows_per_req, s);
+  static const int v = [] {
+    const char* e = getenv("SPECTRE_ATTN_WPAIR");   // warps per item (1 or 2)
+    return e ? atoi(e) : 2;
+  }();
+  if (hd == 128) return launch_attn_w_t<128, 4, 3, 1>(tk32, tv32, a, rows_per_req, s);
   if (hd == 64) {
-    static const int v = [] {
-      const char* e = getenv("SPECTRE_ATTN_W64");
-      return e ? atoi(e) : 0;
-    }();
-    if (v == 1) return launch_attn_w_t<64, 6, 4>(tk32, tv32, a, rows_per_req, s);
-    if (v == 2) return launch_attn_w_t<64, 4, 6>(tk32, tv32, a, rows_per_req, s);
-    return launch_attn_w_t<64, 8, 3>(tk32, tv32, a, rows_per_req, s);
+    if (v == 1) return launch_attn_w_t<64, 8, 3, 1>(tk32, tv32, a, rows_per_req, s);
+    return launch_attn_w_t<64, 8, 3, 2>(tk32, tv32, a, rows_per_req, s);
   }
   return arg_fail("attention: head_dim must be 64 or 128");
 }
