@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "model_kernels.cuh"
@@ -283,6 +284,20 @@ __global__ void k_rope_table(float2* rope, int ctx_cap, int hd, double theta) {
 // Row kernels are grid-stride loops over the device-side row count: a fixed
 // grid of a few CTAs per SM instead of one CTA per row of capacity.
 constexpr int kSms = 148;
+static int rope_ctas_per_sm() {
+  static const int v = [] {
+    const char* e = getenv("SPECTRE_ROPE_CTAS");   // measured: 24 per SM hides the load chains
+    return e ? atoi(e) : 24;
+  }();
+  return v;
+}
+static int resid_ctas_per_sm() {
+  static const int v = [] {
+    const char* e = getenv("SPECTRE_RESID_CTAS");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
 int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void* E,
                          const float* w, float* h, void* x, int d, float eps, cudaStream_t s) {
   SPECTRE_LAUNCH_PDL("k_embed_rmsnorm", k_embed_rmsnorm, dim3(cap_grid(std::min(t_cap, 2 * kSms))), dim3(256), 0, s, tok, t_dev,
@@ -299,7 +314,7 @@ int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const i
   const int threads = nv < 512 ? ((nv + 31) / 32) * 32 : 512;
   const int vec = (nv + threads - 1) / threads;
   auto* xb = reinterpret_cast<__nv_bfloat16*>(x);
-  const dim3 grid(cap_grid(std::min(t_cap, 2 * kSms)));
+  const dim3 grid(cap_grid(std::min(t_cap, resid_ctas_per_sm() * kSms)));
   if (vec <= 1)
     SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<1>, grid, dim3(threads),
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
@@ -321,7 +336,7 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
   if (splits > kMaxSplits) return arg_fail("qkv_rope_kv: splits");
   const int pairs = (n_q + 2 * n_kv) * hd / 2;
   SPECTRE_LAUNCH_PDL("k_qkv_rope_kv", k_qkv_rope_kv,
-                     dim3(cap_grid(std::min(t_cap * ((pairs + 127) / 128), 8 * kSms))), dim3(128),
+                     dim3(cap_grid(std::min(t_cap * ((pairs + 127) / 128), rope_ctas_per_sm() * kSms))), dim3(128),
                      0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
                      reinterpret_cast<const float2*>(rope), reinterpret_cast<__nv_bfloat16*>(q),
                      reinterpret_cast<__nv_bfloat16*>(kc), reinterpret_cast<__nv_bfloat16*>(vc),
