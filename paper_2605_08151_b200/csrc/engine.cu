@@ -80,10 +80,10 @@ static int jobs_per_cta() {
   return j < 1 ? 1 : (j > 4 ? 4 : j);
 }
 
-static int pick_splits(int n_tiles, int k_iters) {
-  // one wave of CTAs (1 CTA per SM) x jobs per CTA: with two or more jobs a
-  // CTA's epilogue overlaps its next job's mainloop (double-buffered TMEM)
-  int s = 148 * jobs_per_cta() / n_tiles;
+static int pick_splits(int n_tiles, int k_iters, int ctas = 148) {
+  // one wave of CTAs x jobs per CTA: with two or more jobs a CTA's epilogue
+  // overlaps its next job's mainloop (double-buffered TMEM)
+  int s = ctas * jobs_per_cta() / n_tiles;
   if (s > 12) s = 12;     // partial traffic grows with s (consumers unroll <= 12)
   if (s < 1) s = 1;
   while (s > 1 && k_iters / s < 3) --s;
@@ -98,6 +98,7 @@ struct ModelRT {
   int sp_qkv = 1, sp_o = 1, sp_d = 1;
   int tile_rows = 256;   // weight rows per GEMM CTA (128 for small-T models)
   long long pf_cap = 0;   // L2 prefetch of the next GEMM's weights (bytes; measured: off)
+  bool half_gemm = false; // decode GEMMs in the half-SM config (2 CTAs per SM, 128-row tiles)
   int attn_chunk = 128;
   float* h = nullptr;
   __nv_bfloat16 *x = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
@@ -127,9 +128,10 @@ struct ModelRT {
   void layout(Bump& b) {
     const int d = dm.d_model, R = rows_cap;
     const int qd = dm.n_q_heads * dm.head_dim;
-    sp_qkv = pick_splits((nqkv() + tile_rows - 1) / tile_rows, d / 64);
-    sp_o = pick_splits((d + tile_rows - 1) / tile_rows, qd / 64);
-    sp_d = pick_splits((d + tile_rows - 1) / tile_rows, dm.ffn / 64);
+    const int tr = half_gemm ? 128 : tile_rows, ctas = half_gemm ? 296 : 148;
+    sp_qkv = pick_splits((nqkv() + tr - 1) / tr, d / 64, ctas);
+    sp_o = pick_splits((d + tr - 1) / tr, qd / 64, ctas);
+    sp_d = pick_splits((d + tr - 1) / tr, dm.ffn / 64, ctas);
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
     attn_chunk = attn_chunk_default();
     split_max = (ctx_cap + attn_chunk - 1) / attn_chunk;
@@ -174,18 +176,23 @@ struct ModelRT {
     po.resize(L);
     pgu.resize(L);
     pd.resize(L);
+    const int tr = half_gemm ? 128 : tile_rows;
     for (int l = 0; l < L; ++l) {
       TRY(gemm_plan(&pq[l], bf(w.wqkv) + (size_t)l * nqkv() * d, nqkv(), d, x, rows_cap,
-                    kPartial, sp_qkv, 0, 0, tile_rows));
+                    kPartial, sp_qkv, 0, 0, tr));
       TRY(gemm_plan(&po[l], bf(w.wo) + (size_t)l * d * qd, d, qd, attn, rows_cap, kPartial,
-                    sp_o, 0, 0, tile_rows));
+                    sp_o, 0, 0, tr));
       // SwiGLU needs full K per tile: 128-row tiles when they fit one wave
       // (draft), else 256-row tiles (two accumulators share every X stage)
       const bool gu128 = (2 * F) / 128 <= gemm_sk_grid();
       TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
                     1, 0, 0, gu128 ? 128 : 256));
       TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
-                    0, 0, tile_rows));
+                    0, 0, tr));
+      if (half_gemm) {
+        // partial GEMMs only: the SwiGLU GEMM measured faster in the full config
+        for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) TRY(gemm_set_half(p));
+      }
       for (GemmPlan* p : {&pq[l], &po[l], &pd[l]})
         TRY(gemm_set_outputs(p, part, nullptr, nullptr, nullptr, 0));
       TRY(gemm_set_outputs(&pgu[l], nullptr, nullptr, nullptr, act, F));
@@ -434,6 +441,10 @@ struct Engine {
     drf.ctx_cap = c.ctx_cap;
     drf.max_new = std::max(draft_new_max, prefill_cs);
     drf.tile_rows = tile_rows_default(256);
+    drf.half_gemm = [] {
+      const char* v = getenv("SPECTRE_DRAFT_HALF");
+      return v ? atoi(v) != 0 : true;
+    }();
     tgt.tile_rows = tile_rows_default(256);
     st.n_req = c.n_req;
     st.gamma = c.gamma;

@@ -104,19 +104,20 @@ int gemm_set_outputs(GemmPlan* p, float* part, float* amax_val, int* amax_idx, v
   return SPECTRE_OK;
 }
 
-template <int kEpi, int BK>
+template <int kEpi, int BK, int kHalf>
 static int launch_one(const GemmPlan& p, cudaStream_t s) {
-  auto kern = gemm_bf16_swapab<kEpi, BK>;
+  using Cfg = GemmCfg<kHalf>;
+  auto kern = gemm_bf16_swapab<kEpi, BK, kHalf>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     SPECTRE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kGemmSmemBytes));
+                                          Cfg::kSmem));
     configured = true;
   }
   if (p.args.stream_k && cap_grid(p.grid) != p.grid)
     return arg_fail("gemm: stream-K plans need the whole grid");
-  SPECTRE_LAUNCH_PDL("gemm_bf16_swapab", kern, dim3(cap_grid(p.grid)), dim3(kGemmThreads), kGemmSmemBytes,
-                     s, p.tmap_w, p.tmap_x, p.tmap_out, p.tmap_sk, p.args);
+  SPECTRE_LAUNCH_PDL("gemm_bf16_swapab", kern, dim3(cap_grid(p.grid)), dim3(Cfg::kThreads),
+                     Cfg::kSmem, s, p.tmap_w, p.tmap_x, p.tmap_out, p.tmap_sk, p.args);
   return SPECTRE_OK;
 }
 
@@ -187,18 +188,31 @@ int gemm_run(const GemmPlan& p0, cudaStream_t s) {
     pp = &stripped;
   }
   const GemmPlan& p = *pp;
+  if (p.half) {
+    if (p.bk != 64 || p.epi == kArgmax) return arg_fail("gemm: half config needs BK 64, no argmax");
+    if (p.epi == kPartial) return launch_one<kPartial, 64, 1>(p, s);
+    return launch_one<kSwiGLU, 64, 1>(p, s);
+  }
   if (p.bk == 64) {
     switch (p.epi) {
-      case kPartial: return launch_one<kPartial, 64>(p, s);
-      case kArgmax: return launch_one<kArgmax, 64>(p, s);
-      default: return launch_one<kSwiGLU, 64>(p, s);
+      case kPartial: return launch_one<kPartial, 64, 0>(p, s);
+      case kArgmax: return launch_one<kArgmax, 64, 0>(p, s);
+      default: return launch_one<kSwiGLU, 64, 0>(p, s);
     }
   }
   switch (p.epi) {
-    case kPartial: return launch_one<kPartial, 32>(p, s);
-    case kArgmax: return launch_one<kArgmax, 32>(p, s);
-    default: return launch_one<kSwiGLU, 32>(p, s);
+    case kPartial: return launch_one<kPartial, 32, 0>(p, s);
+    case kArgmax: return launch_one<kArgmax, 32, 0>(p, s);
+    default: return launch_one<kSwiGLU, 32, 0>(p, s);
   }
+}
+
+int gemm_set_half(GemmPlan* p) {
+  if (p->args.tile_rows != 128 || p->epi == kArgmax || p->args.stream_k || p->bk != 64)
+    return arg_fail("gemm_set_half: 128-row tiles, BK 64, partial / SwiGLU epilogue");
+  p->half = 1;
+  p->grid = std::min(p->n_tiles * p->args.splits, 2 * num_sms());
+  return SPECTRE_OK;
 }
 
 }  // namespace spectre
@@ -235,11 +249,17 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
   // test knobs: max_stages < 0 forces 32-wide K blocks; >= 2000 disables stream-K;
   // >= 1000 selects 128-row tiles
   bool sk = true;
+  bool half = false;
+  if (max_stages >= 3000) {
+    half = true;
+    sk = false;
+    max_stages -= 3000;
+  }
   if (max_stages >= 2000) {
     sk = false;
     max_stages -= 2000;
   }
-  const int tile_rows = max_stages >= 1000 ? 128 : 256;
+  const int tile_rows = (half || max_stages >= 1000) ? 128 : 256;
   if (max_stages >= 1000) max_stages -= 1000;
   const int bk = max_stages < 0 ? 32 : 64;
   float* skp = nullptr;
@@ -251,6 +271,8 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
     return e;
   p.args.t_dev = t_dev;
   p.args.t_static = t_static;
+  if (half)
+    if (int e = gemm_set_half(&p)) return e;
   if (int e = gemm_set_outputs(&p, partial, amax_val, amax_idx, act, ld_act)) return e;
   if (const char* dg = getenv("SPECTRE_GEMM_DIAG")) p.args.diag = atoi(dg);
   static unsigned long long* dbg = nullptr;

@@ -19,6 +19,7 @@ struct GemmPlan {
   int n_tiles = 0;        // weight tiles (args.tile_rows rows each)
   int n_amax_blocks = 0;  // argmax partial rows (grid * 8 epilogue warps)
   int bk = 32;            // K per pipeline stage (32: 64B swizzle, 64: 128B swizzle)
+  int half = 0;           // half-SM launch config (two CTAs per SM, GemmCfg<1>)
 };
 
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
@@ -35,5 +36,7 @@ int gemm_sk_grid();
 int gemm_set_outputs(GemmPlan* p, float* part, float* amax_val, int* amax_idx, void* act,
                      int ld_act);
 int gemm_run(const GemmPlan& p, cudaStream_t s);
+// Switch a 128-row-tile partial / SwiGLU plan to the half-SM configuration.
+int gemm_set_half(GemmPlan* p);
 
 }  // namespace spectre

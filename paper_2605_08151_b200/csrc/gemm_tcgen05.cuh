@@ -49,13 +49,30 @@ namespace spectre {
 
 enum GemmEpilogue : int { kPartial = 0, kArgmax = 1, kSwiGLU = 2 };
 
-constexpr int kGemmThreads = 320;      // 2 control warps + 8 epilogue warps
+constexpr int kGemmThreads = 320;      // full config: 2 control warps + 8 epilogue warps
 constexpr int kGemmTileN = 256;        // weight rows per CTA tile
 constexpr int kGemmMaxStages = 8;
 constexpr int kGemmSmemBytes = 232448; // dynamic smem requested at launch
 constexpr int kGemmScratch = 1024;
 constexpr int kGemmStageOut = 2 * 16384;   // per epilogue group: [32 tokens][128 rows] fp32
 constexpr int kGemmPipeBytes = kGemmSmemBytes - 1024 - 1024 - kGemmScratch - kGemmStageOut;
+
+// Launch configurations.  Full: one CTA per SM (all 512 TMEM columns, ~227 KB
+// shared memory).  Half (T <= 128 decode GEMMs): 128-row tiles, 4 epilogue
+// warps, 256 TMEM columns, ~113 KB — two CTAs per SM, so the next kernel's
+// CTAs become resident (and prefetch their weights under PDL) while this
+// kernel's last CTAs drain.
+template <int kHalf>
+struct GemmCfg {
+  static constexpr int kEpiWarps = kHalf ? 4 : 8;
+  static constexpr int kThreads = 64 + 32 * kEpiWarps;
+  static constexpr int kTmemCols = kHalf ? 256 : 512;
+  static constexpr int kSmem = kHalf ? 115712 : kGemmSmemBytes;
+  static constexpr int kStageOut = (kEpiWarps / 4) * 16384;
+  static constexpr int kPipe = kSmem - 1024 - 1024 - kGemmScratch - kStageOut;
+  static constexpr int kPass = kHalf ? 256 : 512;   // tokens per one-box pass
+  static constexpr int kMinBlocks = kHalf ? 2 : 1;
+};
 
 struct GemmArgs {
   int N, K;                 // weight rows, reduction length
@@ -100,7 +117,7 @@ struct GemmJob {
 
 // The static schedule, computed identically by the three warp roles.
 struct GemmSched {
-  int n_tiles, KI, G, c, T, tile_rows, splits, n_phases;
+  int n_tiles, KI, G, c, T, tile_rows, splits, n_phases, pass;
   bool sk, wide;
   int it, hi, unit, phase;
 
@@ -113,8 +130,9 @@ struct GemmSched {
     return iter_lo(cc + 1, G, total) > iter_lo(cc, G, total);
   }
 
-  __device__ __forceinline__ void init(const GemmArgs& a, int T_, int BK) {
+  __device__ __forceinline__ void init(const GemmArgs& a, int T_, int BK, int pass_ = 512) {
     T = T_;
+    pass = pass_;
     tile_rows = a.tile_rows;
     n_tiles = (a.N + tile_rows - 1) / tile_rows;
     KI = a.K / BK;
@@ -123,7 +141,7 @@ struct GemmSched {
     wide = (T <= 256 && tile_rows == 256);
     sk = a.stream_k && wide;
     splits = sk ? 1 : a.splits;
-    n_phases = wide ? 1 : (tile_rows / 128) * ((T + 511) / 512);
+    n_phases = wide ? 1 : (tile_rows / 128) * ((T + pass - 1) / pass);
     const int total = n_tiles * KI;
     it = sk ? iter_lo(c, G, total) : 0;
     hi = sk ? iter_lo(c + 1, G, total) : 0;
@@ -158,11 +176,11 @@ struct GemmSched {
       j.t0 = 0;
       j.nt = T;
     } else {
-      const int per = (T + 511) / 512;
+      const int per = (T + pass - 1) / pass;
       j.row_off = (phase / per) * 128;
       j.boxes = 1;
-      j.t0 = (phase % per) * 512;
-      j.nt = min(512, T - j.t0);
+      j.t0 = (phase % per) * pass;
+      j.nt = min(pass, T - j.t0);
     }
     if (++phase >= n_phases) {
       phase = 0;
@@ -172,14 +190,18 @@ struct GemmSched {
   }
 };
 
-template <int kEpi, int BK>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+template <int kEpi, int BK, int kHalf>
+__global__ void __launch_bounds__(GemmCfg<kHalf>::kThreads, GemmCfg<kHalf>::kMinBlocks)
 gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
                  const __grid_constant__ CUtensorMap tmap_x,
                  const __grid_constant__ CUtensorMap tmap_out,   // part fp32 / act bf16
                  const __grid_constant__ CUtensorMap tmap_sk,    // stream-K partials fp32
                  GemmArgs a) {
   using namespace ptx;
+  using Cfg = GemmCfg<kHalf>;
+  constexpr int kPipeB = Cfg::kPipe;
+  constexpr int kStageOutB = Cfg::kStageOut;
+  constexpr int kEpiThreads = 32 * Cfg::kEpiWarps;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -194,19 +216,20 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   constexpr int kXBox = 64 * kRow;          // one 64-row activation box
   const bool wide = (T <= 256 && a.tile_rows == 256);
   const int w_bytes = wide ? 2 * kWBox : kWBox;
-  const int x_rows = wide ? ((T + 63) & ~63) : min((T + 63) & ~63, 512);
+  const int x_rows = wide ? ((T + 63) & ~63) : min((T + 63) & ~63, Cfg::kPass);
   const int stage_bytes = w_bytes + x_rows * kRow;
-  int stages = stage_bytes > 0 ? kGemmPipeBytes / stage_bytes : 1;
+  int stages = stage_bytes > 0 ? kPipeB / stage_bytes : 1;
   stages = stages > kGemmMaxStages ? kGemmMaxStages : (stages < 1 ? 1 : stages);
   if (a.max_stages > 0 && stages > a.max_stages) stages = a.max_stages;
-  // TMEM accumulator buffers: two whenever a job needs <= 256 columns
+  // TMEM accumulator buffers: two whenever a job needs <= half the columns
   const int t_pad_all = (T + 15) & ~15;
-  const int nbuf = ((wide && t_pad_all <= 128) || (!wide && t_pad_all <= 256)) ? 2 : 1;
+  constexpr int kBufCols = Cfg::kTmemCols / 2;
+  const int nbuf = ((wide && t_pad_all <= 128) || (!wide && t_pad_all <= kBufCols)) ? 2 : 1;
   const int half_stride = (wide && t_pad_all <= 128) ? 128 : 256;   // wide: 2nd accumulator
 
   uint8_t* pipe = smem;
-  uint8_t* stage_out = smem + kGemmPipeBytes;   // 1024-aligned: kGemmPipeBytes % 1024 == 0
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kGemmPipeBytes + kGemmStageOut);
+  uint8_t* stage_out = smem + kPipeB;   // 1024-aligned: kPipe % 1024 == 0
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPipeB + kStageOutB);
   uint64_t* empty = full + kGemmMaxStages;
   uint64_t* tmem_full = empty + kGemmMaxStages;    // [2]
   uint64_t* tmem_empty = tmem_full + 2;            // [2]
@@ -221,11 +244,11 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tmem_full[b], 1);
-      mbar_init(&tmem_empty[b], 256);
+      mbar_init(&tmem_empty[b], kEpiThreads);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -236,7 +259,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     // this CTA's share of the next GEMM's weights, one bulk prefetch per thread
     const long long share = (a.pf_bytes / gridDim.x + 4095) & ~4095ll;
     const long long c0 = share * blockIdx.x;
-    const long long per = (share / 256 + 15) & ~15ll;
+    const long long per = (share / kEpiThreads + 15) & ~15ll;
     const long long b0 = c0 + per * (threadIdx.x - 64);
     const long long b1 = min(min(b0 + per, c0 + share), a.pf_bytes);
     if (b1 > b0)
@@ -247,7 +270,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     pdl_trigger();
   }
   GemmSched sched;
-  sched.init(a, T, BK);
+  sched.init(a, T, BK, Cfg::kPass);
   if (a.dbg && threadIdx.x == 64) a.dbg[blockIdx.x * 8 + 0] = gtimer();
   const bool no_work = (T == 0);
 
@@ -313,7 +336,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       const uint32_t id0 = idesc_bf16_f32(128, (uint32_t)nc0);
       const uint32_t id1 = idesc_bf16_f32(128, (uint32_t)(nc1 > 0 ? nc1 : 16));
       const int buf = jn % nbuf;
-      const uint32_t acc = tmem_base + (uint32_t)(buf * 256);
+      const uint32_t acc = tmem_base + (uint32_t)(buf * kBufCols);
       if (jn >= nbuf) {
         mbar_wait(&tmem_empty[buf], (uint32_t)((jn / nbuf) - 1) & 1u);
         tc_fence_after();
@@ -389,8 +412,9 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       // wide: group g reads accumulator g (all columns);
       // 1 box: both groups read accumulator 0, alternating 32-column chunks
       const int box = j.boxes == 2 ? grp : 0;
-      const int col_base = buf * 256 + (j.boxes == 2 ? half_stride * grp : 0);
-      const int chunk_step = j.boxes == 2 ? 32 : 64;
+      const int col_base = buf * kBufCols + (j.boxes == 2 ? half_stride * grp : 0);
+      constexpr int kGroups = Cfg::kEpiWarps / 4;
+      const int chunk_step = j.boxes == 2 ? 32 : 32 * kGroups;
       const int chunk0 = j.boxes == 2 ? 0 : 32 * grp;
       const int trow = j.row_off + box * 128 + q * 32 + lane;   // row within the tile
       const int n = j.tile * a.tile_rows + trow;
@@ -413,7 +437,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
             }
           __threadfence();
         }
-        asm volatile("bar.sync 3, 256;" ::: "memory");
+        asm volatile("bar.sync 3, %0;" ::"r"(kEpiThreads) : "memory");
       }
       for (int cc = chunk0; cc < t_pad && !(a.diag & 2); cc += chunk_step) {
         float v[32];
@@ -557,10 +581,10 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         __threadfence();
-        asm volatile("bar.sync 3, 256;" ::: "memory");
+        asm volatile("bar.sync 3, %0;" ::"r"(kEpiThreads) : "memory");
         if (etid == 0) atomicExch(a.sk_flag + sched.c, 1);
       } else if (j.role == 1) {
-        asm volatile("bar.sync 3, 256;" ::: "memory");   // every owner thread read them
+        asm volatile("bar.sync 3, %0;" ::"r"(kEpiThreads) : "memory");   // every owner thread read them
         if (etid == 0)
           for (int i = 0; i < ncl; ++i) a.sk_flag[cl[i]] = 0;   // self-reset
       }
@@ -576,7 +600,8 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       // this warp never covered (no job, or the other group's chunks of a
       // one-box pass) with the identity
       for (int t = lane; t < T; t += 32) {
-        const bool covered = amax_jobs > 0 && (sched.wide || (((t % 512) >> 5) & 1) == grp);
+        const bool covered = amax_jobs > 0 &&
+                             (sched.wide || Cfg::kEpiWarps == 4 || (((t % 512) >> 5) & 1) == grp);
         if (!covered) {
           const size_t slot = ((size_t)blockIdx.x * 8 + ewarp) * a.rows_cap + t;
           a.amax_val[slot] = -INFINITY;
@@ -590,14 +615,14 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   if (kEpi == kPartial && a.post.kind != kPostNone) {
     // every CTA's partials are in global memory: reduce them in this grid
     // 40 floats in the (dynamic) barrier area, past the mbarriers and the TMEM slot
-    float* post_sh = reinterpret_cast<float*>(smem + kGemmPipeBytes + kGemmStageOut + 512);
+    float* post_sh = reinterpret_cast<float*>(smem + kPipeB + kStageOutB + 512);
     post_grid_sync(a.post.gbar);
     if (a.post.kind == kPostRope) post_rope(a.post, a.part, a.splits, a.rows_cap, T);
     else post_resid(a.post, a.part, a.splits, a.rows_cap, T, a.N, post_sh);
   }
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   }
 }
 

@@ -56,8 +56,9 @@ def _ref(torch, X, W, T):
     (320, 320, 1024, 4096, 4), (512, 512, 256, 256, 1), (130, 192, 768, 1024, 1),
     (700, 768, 384, 512, 2), (1280, 1280, 256, 1024, 1), (300, 320, 640, 2048, 3),
     (256, 256, 28672 // 8, 4096, 1), (77, 128, 1000, 640, 2)])
-# 0: defaults (BK=64, 256-row tiles); -8: BK=32 (64B swizzle); 1000: 128-row tiles
-@pytest.mark.parametrize("bk_flag", [0, -8, 1000])
+# 0: defaults (BK=64, 256-row tiles); -8: BK=32 (64B swizzle); 1000: 128-row tiles;
+# 3000: half-SM config (128-row tiles, 4 epilogue warps, 2 CTAs per SM)
+@pytest.mark.parametrize("bk_flag", [0, -8, 1000, 3000])
 def test_partial_matches_fp32(env, T, rows_cap, N, K, splits, bk_flag):
     torch = env[0]
     g = torch.Generator(device="cuda").manual_seed(T * 7 + N)
@@ -145,8 +146,10 @@ def test_swiglu_epilogue(env):
     _, _, _, act = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU)          # stream-K
     _, _, _, act256 = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU, max_stages=2000)
     _, _, _, act128 = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU, max_stages=1000)
+    _, _, _, acth = _run(env, X, W.contiguous(), T, 64, 1, SWIGLU, max_stages=3000)
     # rows >= T are unread padding (the 32-token store boxes may write them)
     assert torch.equal(act256[:T], act128[:T])   # same full-K order, different tiling
+    assert torch.equal(acth[:T], act128[:T])     # half-SM config: same arithmetic
     assert torch.allclose(act[:T].float(), act256[:T].float(), atol=1e-2, rtol=1e-2)
     g = _ref(torch, X, Wg, T)
     u = _ref(torch, X, Wu, T)
