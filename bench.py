@@ -129,15 +129,26 @@ def barrier(ws):
         dist.barrier()
 
 
-def kernels_per_round(mode: str, gamma: int, tL: int, dL: int) -> int:
-    fwd_t = 1 + 9 * tL + 2
-    fwd_d = 1 + 9 * dL + 2
-    n = 2  # round_begin + accept
+KERNELS_PER_LAYER = 8   # qkv GEMM, RoPE/KV write, attention, o GEMM, residual+norm,
+#                          gate/up GEMM (SwiGLU), down GEMM, residual+norm
+
+
+def forward_kernels(n_layers: int, sampling: bool) -> int:
+    """embed + layers + lm_head + (argmax reduce | row sampler)."""
+    return 1 + KERNELS_PER_LAYER * n_layers + 2
+
+
+def kernels_per_round(mode: str, gamma: int, tL: int, dL: int, sampling: bool = False) -> int:
+    """Our kernels launched by one device round (the graph body that runs)."""
+    fwd_t = forward_kernels(tL, sampling)
+    fwd_d = forward_kernels(dL, sampling) - (1 if sampling else 0)   # draft: per-request sampler
+    step_d = fwd_d + 1 + (1 if sampling else 0)                       # + append (+ draft sampler)
+    n = 2 + (1 if sampling else 0)  # round_begin + accept (+ accept sampler)
     n += 1 + fwd_t  # verify_prep + target forward
     if mode == "O":
-        n += 1 + (gamma - 1) * (fwd_d + 1)
+        n += 1 + (gamma - 1) * step_d
     elif mode == "P":
-        n += 1 + gamma * (fwd_d + 1)
+        n += 1 + gamma * step_d
     return n
 
 
@@ -198,11 +209,13 @@ def run_ours(args):
                                   args.seed, trace, tokens_per_step,
                                   float(trace["t_round_ns"].sum()) * 1e-9)
         modes = "".join(chr(int(m)) for m in trace["mode"])
-        launches = sum(kernels_per_round(m, g, M.LLAMA_31_8B.n_layers, M.LLAMA_32_1B.n_layers)
-                       for m in modes)
-        prefill_launches = 2 * ((args.prompt_len + 7) // 8) + 1  # batch kernels + admit
-        prefill_launches += ((args.prompt_len + 7) // 8) * (
-            (1 + 9 * 32 + 2) + (1 + 9 * 16 + 2))
+        samp = args.temperature > 0
+        launches = sum(kernels_per_round(m, g, M.LLAMA_31_8B.n_layers, M.LLAMA_32_1B.n_layers,
+                                         samp) for m in modes) + 1   # + set_round_limit
+        cs = max(1, min(8, 512 // B))          # engine prefill chunk (engine.cu:Engine::sizes)
+        chunks = (args.prompt_len + cs - 1) // cs
+        prefill_launches = 2 * chunks + 1  # batch kernels + admit
+        prefill_launches += chunks * (forward_kernels(32, samp) + forward_kernels(16, samp))
         results[v] = dict(
             ms_per_step=ms_max / args.steps, value=total_tokens / (ms_max / 1e3),
             rounds=len(modes), timeline=modes, clocks=clocks.summary(),
