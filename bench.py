@@ -342,8 +342,13 @@ def roofline_gate_up(pair, args):
     # bound = whichever roof is closer to binding at this intensity
     bound = "hbm" if bytes_ / (hbm * 1e9) >= flops / (tc * 1e12) else "tensor"
     ach, peak, unit = (gbs, hbm, "GB/s") if bound == "hbm" else (tfs, tc, "TFLOP/s")
+    kname = f"gemm_bf16_swapab<SwiGLU> target gate_up T={T} N={F2} K={K}"
+    traffic = None
+    tf = ROOT / "profiles" / "r01" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(kname)   # ncu capture of the same launch shape
     return {"bound": bound, "achieved": round(ach, 1), "peak": peak, "unit": unit,
-            "frac": round(ach / peak, 4), "traffic": None,
+            "frac": round(ach / peak, 4), "traffic": traffic,
             "kernel": f"gemm_bf16_swapab<SwiGLU> target gate_up T={T} N={F2} K={K}",
             "us_per_launch": round(t * 1e6, 2), "tflops": round(tfs, 1), "gbs": round(gbs, 1),
             "peak_source": src + " (MEASURED_PEAKS.json burst)"}
