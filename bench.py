@@ -320,18 +320,26 @@ def roofline_gate_up(pair, args):
     act = torch.empty(512, F2 // 2, dtype=torch.bfloat16, device="cuda")
     s = torch.cuda.Stream()
     times = []
+    n_layers = pair.target.spec.n_layers
+
+    def launch(layer):
+        _native.check(L.spectre_gemm_bf16(X.data_ptr(), pair.target.wgu[layer].data_ptr(), None, T,
+                                          512, F2, K, 1, 2, None, None, None, act.data_ptr(),
+                                          F2 // 2, 2000, int(s.cuda_stream)), "gemm")
+
+    # back-to-back launches over every layer's weights (> L2, PDL-chained as in
+    # the verify pass), CUDA events on the launching stream; repeated 4 times
     with torch.cuda.stream(s):
-        for it in range(25):
-            Wl = pair.target.wgu[it % pair.target.spec.n_layers]  # rotate layers: > L2
+        for layer in range(n_layers):   # warm
+            launch(layer)
+        for rep in range(4):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            _native.check(L.spectre_gemm_bf16(X.data_ptr(), Wl.data_ptr(), None, T, 512, F2, K, 1,
-                                              2, None, None, None, act.data_ptr(), F2 // 2, 0,
-                                              int(s.cuda_stream)), "gemm")
+            for layer in range(n_layers):
+                launch(layer)
             e1.record(s)
             e1.synchronize()
-            if it >= 5:
-                times.append(e0.elapsed_time(e1) * 1e-3)
+            times.append(e0.elapsed_time(e1) * 1e-3 / n_layers)
     t = statistics.median(times)
     bytes_ = F2 * K * 2 + T * K * 2 + T * (F2 // 2) * 2
     flops = 2.0 * T * F2 * K
