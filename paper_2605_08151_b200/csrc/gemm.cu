@@ -179,11 +179,24 @@ int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_
   return SPECTRE_OK;
 }
 
+static int l2_ahead_default() {
+  static const int v = [] {
+    const char* e = getenv("SPECTRE_GEMM_L2_AHEAD");   // k-steps; 0 = off
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 int gemm_run(const GemmPlan& p0, cudaStream_t s) {
   GemmPlan stripped;
   const GemmPlan* pp = &p0;
-  if (p0.args.post.kind != kPostNone && no_grid_sync_ref()) {   // concurrent: no grid barrier
+  if (l2_ahead_default() != p0.args.l2_ahead) {
     stripped = p0;
+    stripped.args.l2_ahead = l2_ahead_default();
+    pp = &stripped;
+  }
+  if (p0.args.post.kind != kPostNone && no_grid_sync_ref()) {   // concurrent: no grid barrier
+    if (pp != &stripped) stripped = p0;
     stripped.args.post.kind = kPostNone;
     pp = &stripped;
   }

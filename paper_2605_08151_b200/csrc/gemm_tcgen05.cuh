@@ -95,6 +95,7 @@ struct GemmArgs {
   const void* pf_ptr;       // next GEMM's weights: prefetched into L2 while this one runs
   long long pf_bytes;       //   (static data, so issued before griddepcontrol.wait)
   GemmPost post;            // fused split-K reduction phase (gemm_post.cuh)
+  int l2_ahead;             // producer L2-prefetches weight boxes this many k-steps ahead
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -310,6 +311,11 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
         for (int k = j.k0; k < j.k1; ++k, ++g) {
           const int s = g % stages;
           uint8_t* st = pipe + s * stage_bytes;
+          // L2 prefetch one ring ahead: the smem ring then refills from L2
+          // instead of waiting a full HBM round trip per slot
+          if (a.l2_ahead > 0 && k + a.l2_ahead < j.k1)
+            for (int b = 0; b < j.boxes; ++b)
+              tma_prefetch_2d(&tmap_w, (k + a.l2_ahead) * BK, n0 + b * 128);
           if (g >= pre) {
             if (g >= stages) mbar_wait(&empty[s], ((uint32_t)(g / stages) & 1u) ^ 1u);
             mbar_arrive_expect_tx(&full[s], tx);
