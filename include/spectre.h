@@ -223,6 +223,11 @@ typedef struct SpectreDecodeConfig {
                                sampling at this temperature (config 3) */
   int32_t role;             /* SPECTRE_ROLE_*: both models, or one side of a
                                disaggregated pair (config 5) */
+  int32_t breaker_threshold;  /* circuit breaker (target_engine.py:337-380): this
+                                 many consecutive speculative rounds with a
+                                 missing draft reply disable speculation ... */
+  int32_t breaker_cooldown;   /* ... for this many rounds.  <= 0: defaults 3 / 5
+                                 (core.py:93-94) */
 } SpectreDecodeConfig;
 
 #define SPECTRE_ROLE_BOTH 0
@@ -253,8 +258,15 @@ int spectre_engine_step(void* engine, int32_t step, int32_t mode, void* stream);
 /* Copy the per-request state one side needs from the other for requests
  * [src_req0, src_req0+n) of `src` into [dst_req0, ...) of `dst` (peer copies
  * when the engines live on different GPUs).  direction 0: target -> draft
- * (mode, committed tokens, positions, cache flags); 1: draft -> target
- * (draft history window, generation counters, draft timing). */
+ * (per-request mode and query tags, committed tokens, positions, cache
+ * flags); 1: draft -> target (draft history window, generation counters,
+ * reply tags, draft timing).  Every query carries a (round, serial) tag and
+ * the draft stamps its reply with it; the target uses a reply only when the
+ * tags match its outstanding query (target_engine.py:314-331), so a lost or
+ * superseded reply (an exchange that never ran) degrades that request to a
+ * FALLBACK / PADDED candidate and counts towards the circuit breaker.
+ * DRAFT with mode 'M' serves shards that chose different modes in one
+ * draft phase (per-request mode from the last direction-0 exchange). */
 int spectre_engine_exchange(void* src, void* dst, int32_t direction, int32_t src_req0,
                             int32_t dst_req0, int32_t n, void* stream);
 /* Enable direct peer access between two GPUs (both directions; idempotent). */
@@ -288,6 +300,8 @@ typedef struct SpectreRoundTrace {
   double* r_hat_ema;
   double* accepted_len_ema;
   double* r_star;
+  int32_t* n_stale;         /* queried requests whose reply was missing or
+                               superseded at commit (target_engine.py:314-331) */
 } SpectreRoundTrace;
 int spectre_engine_read(void* engine, int64_t* committed, int32_t* committed_pos,
                         const SpectreRoundTrace* trace, int32_t* n_rounds, void* stream);

@@ -107,12 +107,13 @@ class DecodeConfig(C.Structure):
                 ("ctx_cap", C.c_int32), ("has_fixed_l", C.c_int32), ("alpha", C.c_double),
                 ("t_target", C.c_double), ("t_draft", C.c_double), ("ema_decay", C.c_double),
                 ("fixed_threshold_l", C.c_double), ("temperature", C.c_double),
-                ("role", C.c_int32)]
+                ("role", C.c_int32), ("breaker_threshold", C.c_int32),
+                ("breaker_cooldown", C.c_int32)]
 
 
 TRACE_FIELDS = ("mode", "participants", "delta", "n_roll", "content_sum", "content_n",
                 "n_padded", "t_round_ns", "t_verify_ns", "t_draft_ns", "r_hat_ema",
-                "accepted_len_ema", "r_star")
+                "accepted_len_ema", "r_star", "n_stale")
 
 
 class RoundTraceBufs(C.Structure):

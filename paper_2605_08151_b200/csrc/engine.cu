@@ -395,6 +395,11 @@ struct Engine {
     st.vcand_n = b.take<int>(n);
     st.delta = b.take<int>(n);
     st.rolled = b.take<int>(n);
+    st.req_mode = b.take<int>(n);
+    st.q_round = b.take<int>(n);
+    st.q_serial = b.take<int>(n);
+    st.r_round = b.take<int>(n);
+    st.r_serial = b.take<int>(n);
     st.committed = b.take<uint64_t>((size_t)n * cfg.output_len);
     st.hist = b.take<uint64_t>((size_t)n * st.hist_cap);
     st.cached_tok = b.take<uint64_t>((size_t)n * G);
@@ -414,6 +419,7 @@ struct Engine {
     st.trace.r_hat_ema = b.take<double>(R);
     st.trace.accepted_len_ema = b.take<double>(R);
     st.trace.r_star = b.take<double>(R);
+    st.trace.n_stale = b.take<int>(R);
     if (st.sampling) {
       st.samp_a = b.take<int>(n);
       st.samp_bonus = b.take<int>(n);
@@ -465,6 +471,8 @@ struct Engine {
     st.fixed_l = c.fixed_threshold_l;
     st.use_handles = 0;
     st.sampling = c.temperature > 0.0 ? 1 : 0;
+    st.breaker_threshold = c.breaker_threshold > 0 ? c.breaker_threshold : 3;
+    st.breaker_cooldown = c.breaker_cooldown > 0 ? c.breaker_cooldown : 5;
     if (const char* v = getenv("SPECTRE_PAR_DRAFT_CTAS")) par_draft_ctas = atoi(v);
     if (const char* v = getenv("SPECTRE_PAR_TARGET_CTAS")) par_target_ctas = atoi(v);
     qwin = 4 * c.gamma + 4;   // > every candidate-to-speculation position gap
@@ -478,7 +486,7 @@ struct Engine {
   // ---- round pieces
   int draft_phase(int which, cudaStream_t s) {
     TRY(launch_draft_prep(st, drf.bt, which, s));
-    const int steps = which == 'O' ? cfg.gamma - 1 : cfg.gamma;
+    const int steps = which == 'O' ? cfg.gamma - 1 : cfg.gamma;   // 'M': the longest query
     for (int i = 0; i < steps; ++i) {
       TRY(drf.forward(i == 0 ? draft_new_max : 1, s, nullptr, false));
       if (st.sampling)
@@ -838,6 +846,7 @@ extern "C" int spectre_engine_read(void* engine, int64_t* committed, int32_t* co
     TRY(cp(trace->r_hat_ema, t.r_hat_ema, R * 8));
     TRY(cp(trace->accepted_len_ema, t.accepted_len_ema, R * 8));
     TRY(cp(trace->r_star, t.r_star, R * 8));
+    TRY(cp(trace->n_stale, t.n_stale, R * 4));
   }
   return SPECTRE_OK;
 }
@@ -904,7 +913,7 @@ extern "C" int spectre_engine_step(void* engine, int32_t step, int32_t mode, voi
       return *e->mode_host;
     }
     case SPECTRE_STEP_DRAFT:
-      if (mode == 'O' || mode == 'P') TRY(e->draft_phase(mode, s));
+      if (mode == 'O' || mode == 'P' || mode == 'M') TRY(e->draft_phase(mode, s));
       return SPECTRE_OK;
     case SPECTRE_STEP_VERIFY:
       TRY(e->verify_phase(s));
@@ -940,6 +949,9 @@ extern "C" int spectre_engine_exchange(void* src, void* dst, int32_t direction,
     SPECTRE_CUDA_TRY(ints(b->st.done, a->st.done));
     SPECTRE_CUDA_TRY(ints(b->st.cached_len, a->st.cached_len));
     SPECTRE_CUDA_TRY(ints(b->st.in_rollback, a->st.in_rollback));
+    SPECTRE_CUDA_TRY(ints(b->st.req_mode, a->st.req_mode));
+    SPECTRE_CUDA_TRY(ints(b->st.q_round, a->st.q_round));
+    SPECTRE_CUDA_TRY(ints(b->st.q_serial, a->st.q_serial));
     SPECTRE_CUDA_TRY(cp(b->st.committed + (size_t)dst_req0 * b->cfg.output_len,
                         a->st.committed + (size_t)src_req0 * a->cfg.output_len,
                         (size_t)n * a->cfg.output_len * sizeof(uint64_t)));
@@ -951,6 +963,8 @@ extern "C" int spectre_engine_exchange(void* src, void* dst, int32_t direction,
     SPECTRE_CUDA_TRY(ints(b->st.gen_count, a->st.gen_count));
     SPECTRE_CUDA_TRY(ints(b->st.gen_done, a->st.gen_done));
     SPECTRE_CUDA_TRY(ints(b->st.gen_start, a->st.gen_start));
+    SPECTRE_CUDA_TRY(ints(b->st.r_round, a->st.r_round));
+    SPECTRE_CUDA_TRY(ints(b->st.r_serial, a->st.r_serial));
     // draft phase timing only: the target's own clock fields stay untouched
     SPECTRE_CUDA_TRY(cp(&b->st.ctrl->t_draft_begin, &a->st.ctrl->t_draft_begin,
                         2 * sizeof(long long)));

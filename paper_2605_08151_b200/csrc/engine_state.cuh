@@ -38,6 +38,9 @@ struct CtrlDev {
   int has_tT, has_tD, has_tpar, has_tord;
   double tT, tD, tpar, tord;   // measured EMAs (seconds)
   double r_star;
+  // circuit breaker (target_engine.py:337-380); round ids are 1-based as in sim.py:519
+  int streak, disabled_until, activations;
+  int n_stale;       // this round: queried requests without a matching reply
 };
 
 struct RoundTraceDev {
@@ -54,6 +57,7 @@ struct RoundTraceDev {
   double* r_hat_ema;
   double* accepted_len_ema;
   double* r_star;
+  int* n_stale;
 };
 
 struct DecodeStateDev {
@@ -89,6 +93,13 @@ struct DecodeStateDev {
   int sampling;          // 1: accept from samp_a / samp_bonus (rejection sampling)
   int* samp_a;           // [n_req] accepted candidates
   int* samp_bonus;       // [n_req] bonus / resampled token
+  int breaker_threshold, breaker_cooldown;
+  // query / reply versioning (target_engine.py:314-331, sim.py:816-844)
+  int* req_mode;         // [n_req] this round's mode per request (draft side: 'M' phases)
+  int* q_round;          // [n_req] outstanding query tag (target side)
+  int* q_serial;
+  int* r_round;          // [n_req] tag of the reply held in hist / gen_* (draft stamps)
+  int* r_serial;
 };
 
 // launchers (model_protocol.cu)

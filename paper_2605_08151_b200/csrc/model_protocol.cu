@@ -92,8 +92,14 @@ __global__ void k_admit(DecodeStateDev s, BatchDev bt) {
     c.has_tT = c.has_tD = c.has_tpar = c.has_tord = 0;
     c.tT = c.tD = c.tpar = c.tord = 0.0;
     c.r_star = 0.0;
+    c.streak = c.disabled_until = c.activations = 0;
+    c.n_stale = 0;
   }
   if (b >= s.n_req) return;
+  s.req_mode[b] = 0;
+  s.q_round[b] = s.r_round[b] = -1;
+  s.q_serial[b] = 0;
+  s.r_serial[b] = -1;
   const int row = bt.q_off[b] + bt.n_new[b] - 1;
   s.committed[(size_t)b * s.out_len] = (uint64_t)bt.out_tok[row];
   s.pos[b] = 1;
@@ -109,17 +115,39 @@ __global__ void k_admit(DecodeStateDev s, BatchDev bt) {
 
 // ------------------------------------------------------------ round begin
 // Controller (sim.py:447-467) + conditional-node selection.
-__global__ void k_round_begin(DecodeStateDev s) {
+__device__ int round_choose_mode(DecodeStateDev& s, CtrlDev& c);
+
+// Thread 0 picks the mode; every thread then stamps its requests' queries
+// with a (round, serial) tag (sim.py:492-512: ordinary queries requests
+// without a cache at round_tag = round, parallel queries all at round + 1).
+__global__ void __launch_bounds__(kProtoThreads) k_round_begin(DecodeStateDev s) {
   pdl_wait();
   pdl_trigger();
-  if (threadIdx.x != 0) return;
+  __shared__ int s_mode;
   CtrlDev& c = *s.ctrl;
+  if (threadIdx.x == 0) s_mode = round_choose_mode(s, c);
+  __syncthreads();
+  const int mode = s_mode;
+  const int round_id = c.round + 1;
+  for (int b = threadIdx.x; b < s.n_req; b += blockDim.x) {
+    s.req_mode[b] = mode;
+    if (!s.done[b] && (mode == 'P' || (mode == 'O' && s.cached_len[b] == 0))) {
+      s.q_serial[b] += 1;
+      s.q_round[b] = mode == 'P' ? round_id + 1 : round_id;
+    }
+  }
+}
+
+__device__ int round_choose_mode(DecodeStateDev& s, CtrlDev& c) {
   c.t_round_begin = globaltimer();
   c.t_draft_begin = c.t_draft_end = 0;
   c.draft_steps = 0;
+  c.n_stale = 0;
   int mode = 0;
   if (c.n_active > 0 && c.error == 0 && c.round < s.max_rounds && c.round < c.round_limit) {
     if (s.variant == SPECTRE_VARIANT_AR) mode = 'F';
+    // breaker window: speculation off, controller untouched (sim.py:520-533)
+    else if (c.round + 1 < c.disabled_until) mode = 'F';
     else if (s.variant == SPECTRE_VARIANT_ORDINARY) mode = 'O';
     else if (s.variant == SPECTRE_VARIANT_PARALLEL) mode = 'P';
     else {
@@ -171,6 +199,7 @@ __global__ void k_round_begin(DecodeStateDev s) {
     cudaGraphSetConditional(s.h_par, mode == 'P' ? 1u : 0u);
     cudaGraphSetConditional(s.h_ar, mode == 'F' ? 1u : 0u);
   }
+  return mode;
 }
 
 // ------------------------------------------------------------ draft phase
@@ -184,7 +213,8 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_prep(DecodeStateDev s, 
   __shared__ int sh[kProtoThreads];
   CtrlDev& c = *s.ctrl;
   const int mode = c.mode;
-  if (mode != which_mode) {  // phase not selected this round: empty batch
+  const bool mixed = which_mode == 'M';   // per-request modes (disaggregated shards)
+  if (!mixed && mode != which_mode) {  // phase not selected this round: empty batch
     if (threadIdx.x == 0) *bt.t_dev = 0;
     if (threadIdx.x < s.n_req) bt.n_new[threadIdx.x] = 0;
     return;
@@ -196,9 +226,11 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_prep(DecodeStateDev s, 
     bt.rslot[b] = b;
     s.gen_count[b] = 0;
     const bool active = !s.done[b];
-    const bool queried = active && mode == which_mode &&
-                         (which_mode == 'P' || s.cached_len[b] == 0);
+    const int rm = mixed ? s.req_mode[b] : which_mode;
+    const bool queried = active && (rm == 'P' || (rm == 'O' && s.cached_len[b] == 0));
     if (queried) {
+      s.r_round[b] = s.q_round[b];     // the reply answers this query
+      s.r_serial[b] = s.q_serial[b];
       uint64_t* h = s.hist + (size_t)b * s.hist_cap;
       const uint64_t* com = s.committed + (size_t)b * s.out_len;
       const int pos = s.pos[b];
@@ -209,8 +241,8 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_prep(DecodeStateDev s, 
                            [&](int32_t k) { return com[start + k]; }, ref, &inv);
       kvd = min(s.kvd[b], inv);
       s.synced[b] = pos;
-      const int count = which_mode == 'O' ? s.gamma - 1 : s.gamma;
-      if (which_mode == 'O' || hl + count > s.hist_cap) {
+      const int count = rm == 'O' ? s.gamma - 1 : s.gamma;
+      if (rm == 'O' || hl + count > s.hist_cap) {
         // repair anchor (sim.py:550-555) / speculation-window cap
         hl = session_rebase(h, hl, pos, ref, &inv);
         kvd = min(kvd, inv);
@@ -239,7 +271,7 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_prep(DecodeStateDev s, 
   }
   if (threadIdx.x == 0) {
     *bt.t_dev = total;
-    if (mode == which_mode) c.draft_steps = which_mode == 'O' ? s.gamma - 1 : s.gamma;
+    c.draft_steps = which_mode == 'O' ? s.gamma - 1 : s.gamma;
   }
 }
 
@@ -250,7 +282,7 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_append(DecodeStateDev s
   pdl_trigger();
   __shared__ int sh[kProtoThreads];
   CtrlDev& c = *s.ctrl;
-  if (c.mode != which_mode) {
+  if (which_mode != 'M' && c.mode != which_mode) {
     if (threadIdx.x == 0) *bt.t_dev = 0;
     if (threadIdx.x < s.n_req) bt.n_new[threadIdx.x] = 0;
     return;
@@ -283,7 +315,7 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_append(DecodeStateDev s
   }
   if (threadIdx.x == 0) {
     *bt.t_dev = total;
-    if (last_step && c.mode == which_mode) c.t_draft_end = globaltimer();
+    if (last_step) c.t_draft_end = globaltimer();
   }
 }
 
@@ -314,6 +346,11 @@ __global__ void __launch_bounds__(kProtoThreads) k_verify_prep(DecodeStateDev s,
       m = s.cached_len[b];
       const uint64_t* ct = s.cached_tok + (size_t)b * (s.gamma + 1);
       for (int j = 0; j < m; ++j) cand[j] = ct[j];
+    } else if (mode == 'O' &&
+               (s.r_serial[b] != s.q_serial[b] || s.r_round[b] != s.q_round[b])) {
+      // repair reply missing or superseded: FALLBACK (sim.py:568-577)
+      kind = kFallback;
+      atomicAdd(&s.ctrl->n_stale, 1);
     } else if (mode == 'O') {
       kind = kRepaired;
       m = s.gamma - 1;
@@ -367,9 +404,13 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
   pdl_wait();
   pdl_trigger();
   __shared__ long long s_tv;
+  __shared__ int s_trip;
   CtrlDev& c = *s.ctrl;
   const int mode = c.mode;
-  if (threadIdx.x == 0) s_tv = globaltimer();
+  if (threadIdx.x == 0) {
+    s_tv = globaltimer();
+    s_trip = 0;
+  }
   __syncthreads();
   if (mode == 0) {
     if (threadIdx.x == 0 && s.use_handles) cudaGraphSetConditional(s.h_loop, 0u);
@@ -395,8 +436,11 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
     }
     const int accepted_count = a + (kind == kCached ? 0 : 1);
     const int real = kind == kRepaired ? s.gamma : (kind == kCached ? m : 1);
-    // this round's prepared segment (parallel mode): the draft's speculation
-    const bool prep = (mode == 'P') && s.gen_count[b] > 0;
+    // this round's prepared segment (parallel mode): the draft's speculation,
+    // used only if its reply answers this round's query (target_engine.py:314-331)
+    const bool fresh = s.r_serial[b] == s.q_serial[b] && s.r_round[b] == s.q_round[b];
+    if (mode == 'P' && !fresh) atomicAdd(&s.ctrl->n_stale, 1);
+    const bool prep = (mode == 'P') && fresh && s.gen_count[b] > 0;
     const uint64_t* h = s.hist + (size_t)b * s.hist_cap;
     const int pstart = s.gen_start[b];
     const int plen = prep ? s.gen_done[b] : 0;
@@ -470,7 +514,23 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
       if (!c.has_tord) { c.tord = tr; c.has_tord = 1; } else { c.tord = ema_step(d, c.tord, tr); }
     }
     const int ri = c.round;
+    // circuit breaker after a speculative round (sim.py:703-718,
+    // target_engine.py:356-380): a missing reply is a timeout here — the
+    // exchange is synchronous, so a reply absent at commit never arrives
+    if (mode != 'F') {
+      const int round_id = ri + 1;
+      const int streak = c.n_stale > 0 ? c.streak + 1 : 0;
+      if (streak >= s.breaker_threshold) {
+        c.streak = 0;
+        c.disabled_until = round_id + s.breaker_cooldown + 1;
+        c.activations += 1;
+        s_trip = 1;
+      } else {
+        c.streak = streak;
+      }
+    }
     if (ri < s.max_rounds) {
+      s.trace.n_stale[ri] = c.n_stale;
       s.trace.mode[ri] = mode;
       s.trace.participants[ri] = P;
       s.trace.delta[ri] = dsum;
@@ -491,6 +551,14 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
                                          c.round < s.max_rounds && c.round < c.round_limit)
                                             ? 1u
                                             : 0u);
+  }
+  __syncthreads();
+  if (s_trip) {   // the window invalidates all in-flight speculation (sim.py:711-718)
+    for (int r = threadIdx.x; r < s.n_req; r += blockDim.x) {
+      s.cached_len[r] = 0;
+      s.in_rollback[r] = 1;
+      s.q_serial[r] += 1;   // outstanding queries cleared: no late reply can match
+    }
   }
 }
 
@@ -520,7 +588,7 @@ int launch_admit(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s) {
   return SPECTRE_OK;
 }
 int launch_round_begin(const DecodeStateDev& st, cudaStream_t s) {
-  SPECTRE_LAUNCH_PDL("k_round_begin", k_round_begin, dim3(1), dim3(32), 0, s, st);
+  SPECTRE_LAUNCH_PDL("k_round_begin", k_round_begin, dim3(1), dim3(256), 0, s, st);
   return SPECTRE_OK;
 }
 int launch_draft_prep(const DecodeStateDev& st, const BatchDev& bt, int which, cudaStream_t s) {

@@ -12,6 +12,14 @@ each own a shard.  A round is host-driven:
   parallel:  draft DRAFT  ∥  target VERIFY ; join ; exchange draft -> target ; ACCEPT
   ar:        target VERIFY ; ACCEPT
 
+Each target shard runs its own controller and may pick its own mode; one
+draft phase serves all speculating shards (mode 'M' when they differ: the
+draft reads each request's mode from the exchange).  Every query carries a
+(round, serial) tag the draft's reply must echo (target_engine.py:314-331):
+a reply that never arrives (`run(drop=...)`) degrades its requests to
+FALLBACK / PADDED candidates, counts as a timeout for that shard's circuit
+breaker (target_engine.py:337-380) and never costs losslessness.
+
 Exchanges are device-to-device copies of a few KB per request
 (`spectre_engine_exchange`, cudaMemcpyDefault: NVLink peer copies when the
 engines sit on different GPUs); the cross-device ordering is CUDA events.
@@ -24,7 +32,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from . import _native
-from .decoder import PolicyVariant
+from .decoder import PolicyVariant  # noqa: F401  (re-exported for callers)
 from .model import DecodeSpec, ModelPair, SpectreEngine, report_from_trace
 
 STEP_BEGIN, STEP_DRAFT, STEP_VERIFY, STEP_ACCEPT = 0, 1, 2, 3
@@ -46,12 +54,15 @@ def _device_of(pair: ModelPair) -> int:
 
 class DisaggregatedDecoder:
     """One draft server + target shards.  `shards` is a list of
-    (target_pair, n_requests); the draft pair serves their concatenation."""
+    (target_pair, n_requests) or (target_pair, n_requests, spec_overrides);
+    the draft pair serves their concatenation.  Overrides (e.g. a replica's
+    own t_target / t_draft latency model) apply to that shard's controller."""
 
     def __init__(self, draft_pair: ModelPair, target_pairs: list[tuple[ModelPair, int]],
                  spec: DecodeSpec, variant: PolicyVariant | str):
         torch = _native.require_cuda()
-        n_total = sum(n for _, n in target_pairs)
+        target_pairs = [tuple(t) + ({},) * (3 - len(t)) for t in target_pairs]
+        n_total = sum(t[1] for t in target_pairs)
         if n_total != spec.n_req:
             raise ValueError("shard sizes must add up to spec.n_req")
         self.spec = spec
@@ -61,20 +72,16 @@ class DisaggregatedDecoder:
             self.draft_stream = torch.cuda.Stream()
         self.shards = []
         r0 = 0
-        for pair, n in target_pairs:
+        for pair, n, over in target_pairs:
             dev = _device_of(pair)
             _native.check(_native.lib().spectre_enable_peer_access(self.draft_device, dev),
                           "spectre_enable_peer_access")
-            sub = DecodeSpec(**{**spec.__dict__, "n_req": n})
+            sub = DecodeSpec(**{**spec.__dict__, **over, "n_req": n})
             with torch.cuda.device(dev):
                 eng = SpectreEngine(pair, sub, variant, role="target")
                 self.shards.append(Shard(eng, r0, n, torch.cuda.Stream(), dev))
             r0 += n
         self.variant = self.draft.variant
-        if len(self.shards) > 1 and self.variant == PolicyVariant.HYBRID:
-            # one draft phase per round serves every shard: shard controllers
-            # must agree, which only fixed-mode variants guarantee
-            raise ValueError("multi-shard disaggregation supports ar / ordinary / parallel")
 
     def _on(self, sh):
         torch = _native.require_cuda()
@@ -97,11 +104,15 @@ class DisaggregatedDecoder:
         for dev in {self.draft_device, *(sh.device for sh in self.shards)}:
             torch.cuda.synchronize(dev)
 
-    def run(self, max_rounds: int | None = None) -> int:
+    def run(self, max_rounds: int | None = None, drop=None) -> int:
+        """Decode to completion (or `max_rounds`).  `drop(round, shard) -> bool`
+        (fault injection) loses that shard's draft reply: its draft -> target
+        exchange is skipped, as a lost DRAFT_REPLY would be (sim.py:816-844)."""
         torch = _native.require_cuda()
         rounds = 0
         limit = max_rounds if max_rounds is not None else self.shards[0].engine.max_rounds
         ds = self.draft_stream
+        O, P = ord("O"), ord("P")
         while rounds < limit:
             # every shard runs its own controller (the paper decides per batch)
             modes = []
@@ -110,45 +121,43 @@ class DisaggregatedDecoder:
                     modes.append(sh.engine.step(STEP_BEGIN, stream=sh.stream))
             if all(m == 0 for m in modes):
                 break
-            if len(set(m for m in modes if m)) > 1:
-                raise RuntimeError("target shards disagree on the round mode")
-            mode = next(m for m in modes if m)
-            for sh in self.shards:
+            live = {m for m in modes if m}
+            # one draft phase serves every speculating shard; shards that chose
+            # different modes get a mixed phase (per-request mode, 'M')
+            draft_mode = (next(iter(live)) if live in ({O}, {P})
+                          else ord("M") if live & {O, P} else 0)
+            for sh, m in zip(self.shards, modes):
+                if not m:
+                    continue
                 with self._on(sh):
                     self._xchg(sh.engine, self.draft, TO_DRAFT, 0, sh.req0, sh.n, sh.stream)
                     ev = torch.cuda.Event()
                     ev.record(sh.stream)
                 ds.wait_event(ev)
-            if mode == ord("O"):
+            ev_draft = None
+            if draft_mode:
                 with self._on(None):
-                    self.draft.step(STEP_DRAFT, mode, stream=ds)
-                    ev = torch.cuda.Event()
-                    ev.record(ds)
-                for sh in self.shards:
-                    with self._on(sh):
-                        sh.stream.wait_event(ev)
-                        self._xchg(self.draft, sh.engine, TO_TARGET, sh.req0, 0, sh.n, sh.stream)
-                        sh.engine.step(STEP_VERIFY, stream=sh.stream)
-                        sh.engine.step(STEP_ACCEPT, stream=sh.stream)
-            elif mode == ord("P"):
-                with self._on(None):
-                    self.draft.step(STEP_DRAFT, mode, stream=ds)     # overlaps the verify
-                for sh in self.shards:
+                    self.draft.step(STEP_DRAFT, draft_mode, stream=ds)
+                    ev_draft = torch.cuda.Event()
+                    ev_draft.record(ds)
+            # parallel shards verify while the draft speculates
+            for sh, m in zip(self.shards, modes):
+                if m == P:
                     with self._on(sh):
                         sh.engine.step(STEP_VERIFY, stream=sh.stream)
-                with self._on(None):
-                    ev = torch.cuda.Event()
-                    ev.record(ds)
-                for sh in self.shards:
-                    with self._on(sh):
-                        sh.stream.wait_event(ev)
-                        self._xchg(self.draft, sh.engine, TO_TARGET, sh.req0, 0, sh.n, sh.stream)
-                        sh.engine.step(STEP_ACCEPT, stream=sh.stream)
-            else:
-                for sh in self.shards:
-                    with self._on(sh):
+            for sh, m in zip(self.shards, modes):
+                if not m:
+                    continue
+                k = self.shards.index(sh)
+                with self._on(sh):
+                    if m in (O, P):
+                        sh.stream.wait_event(ev_draft)
+                        if drop is None or not drop(rounds, k):
+                            self._xchg(self.draft, sh.engine, TO_TARGET, sh.req0, 0, sh.n,
+                                       sh.stream)
+                    if m != P:
                         sh.engine.step(STEP_VERIFY, stream=sh.stream)
-                        sh.engine.step(STEP_ACCEPT, stream=sh.stream)
+                    sh.engine.step(STEP_ACCEPT, stream=sh.stream)
             for sh in self.shards:   # next round's draft sync starts after this accept
                 with self._on(sh):
                     ev = torch.cuda.Event()

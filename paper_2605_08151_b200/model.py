@@ -182,6 +182,8 @@ class DecodeSpec:
     fixed_threshold_l: float | None = None
     max_rounds: int | None = None
     temperature: float = 0.0        # 0: greedy; > 0: speculative rejection sampling (config 3)
+    breaker_threshold: int = 3      # circuit breaker (core.py:93-94, target_engine.py:337-380)
+    breaker_cooldown: int = 5
 
     def ctx_cap(self) -> int:
         need = self.prompt_len + self.output_len + 4 * self.gamma + 16
@@ -219,7 +221,9 @@ class SpectreEngine:
             has_fixed_l=int(spec.fixed_threshold_l is not None), alpha=spec.alpha,
             t_target=spec.t_target, t_draft=spec.t_draft, ema_decay=spec.ema_decay,
             fixed_threshold_l=float(spec.fixed_threshold_l or 0.0),
-            temperature=float(spec.temperature), role=ROLES[role])
+            temperature=float(spec.temperature), role=ROLES[role],
+            breaker_threshold=int(spec.breaker_threshold),
+            breaker_cooldown=int(spec.breaker_cooldown))
         self.role = role
         self._tdims = pair.target.spec.dims()
         self._ddims = pair.draft.spec.dims()
@@ -377,6 +381,11 @@ def report_from_trace(variant: PolicyVariant, seed: int, trace: dict, total: int
         steady_mean_rollback_ratio=(sum(r_hat[i] for i in steady) / len(steady)) if steady else 0.0,
         sim_duration=device_seconds, total_committed=total, total_rounds=n,
         requests_completed=0, fallback_rounds=sum(1 for m in trace["mode"] if m == ord("F")),
+        breaker_activations=0 if variant == PolicyVariant.AR else sum(
+            1 for i, m in enumerate(trace["mode"])
+            if m == ord("F") and (i == 0 or trace["mode"][i - 1] != ord("F"))),
+        stale_replies=int(trace["n_stale"].sum()) if "n_stale" in trace else 0,
+        timeout_rounds=int((trace["n_stale"] > 0).sum()) if "n_stale" in trace else 0,
         draft_tokens_generated=0)
 
 

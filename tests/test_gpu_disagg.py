@@ -58,3 +58,98 @@ def test_two_target_shards_match_engine(M, variant):
     committed, pos, _ = dd.read()
     assert (pos == spec.output_len).all()
     assert torch.equal(committed, ref.committed.cpu())
+
+
+def test_shards_with_different_modes_match_per_shard_runs(M):
+    """Hybrid shards with their own latency models pick different modes in
+    the same round; one mixed ('M') draft phase serves both.  Multi-shard
+    results must equal the union of per-shard single-engine runs (SURVEY
+    §8e).  alpha = 1: draft noise is keyed by request index, which differs
+    between the shared draft server and a per-shard engine."""
+    import numpy as np
+    import torch
+    from paper_2605_08151_b200.disagg import DisaggregatedDecoder
+    n, na = 8, 3
+    pair = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=n, ctx_cap=256, seed=23)
+    spec = _spec(M, n, seed=23, alpha=1.0)
+    # r* = (g-1) L T_D / ((T_T + (g-1) T_D)(L-1)) (analytics.py:57-70):
+    fast_draft = dict(t_draft=1e-9)     # r* ~ 0: ordinary unless r-hat is 0
+    slow_draft = dict(t_draft=1.0)      # r* ~ L/(L-1) > 1: always parallel
+    prompts = M.synthetic_prompts(n, spec.prompt_len, M.TINY_TARGET.vocab, spec.seed)
+    t1 = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=na, ctx_cap=256, seed=23)
+    t2 = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=n - na, ctx_cap=256, seed=23)
+    dd = DisaggregatedDecoder(pair, [(t1, na, fast_draft), (t2, n - na, slow_draft)], spec,
+                              "hybrid")
+    dd.prefill(prompts)
+    dd.run()
+    committed, pos, traces = dd.read()
+    assert (pos == spec.output_len).all()
+    refs = []
+    for (lo, hi, over) in ((0, na, fast_draft), (na, n, slow_draft)):
+        sub = M.DecodeSpec(**{**spec.__dict__, **over, "n_req": hi - lo})
+        p1 = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=hi - lo, ctx_cap=256, seed=23)
+        refs.append(M.decode(p1, sub, "hybrid", prompts=prompts[lo:hi].contiguous(),
+                             use_graph=False))
+    assert torch.equal(committed, torch.cat([r.committed.cpu() for r in refs]))
+    for tr, r in zip(traces, refs):
+        assert (tr["mode"] == r.trace["mode"]).all()
+    m0, m1 = traces[0]["mode"], traces[1]["mode"]
+    k = min(len(m0), len(m1))
+    assert (m0[:k] != m1[:k]).any(), "shards never chose different modes"
+    assert np.all(traces[0]["n_stale"] == 0) and np.all(traces[1]["n_stale"] == 0)
+
+
+@pytest.mark.parametrize("variant", ["ordinary", "parallel", "hybrid"])
+def test_lost_replies_stay_lossless(M, variant):
+    """Replies lost in chosen rounds (draft -> target exchange skipped): the
+    target discards the stale segment (tags mismatch), degrades the requests
+    to FALLBACK / PADDED and still commits the autoregressive stream."""
+    import torch
+    from paper_2605_08151_b200.disagg import DisaggregatedDecoder
+    n = 8
+    pair = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=n, ctx_cap=256, seed=24)
+    spec = _spec(M, n, seed=24, breaker_threshold=100)
+    ar = M.decode(pair, spec, "ar", use_graph=False)
+    lost = {1, 2, 5, 9}
+    dd = DisaggregatedDecoder(pair, [(pair, n)], spec, variant)
+    dd.prefill(M.synthetic_prompts(n, spec.prompt_len, M.TINY_TARGET.vocab, spec.seed))
+    dd.run(drop=lambda r, k: r in lost)
+    committed, pos, traces = dd.read()
+    assert (pos == spec.output_len).all()
+    assert torch.equal(committed, ar.committed.cpu())
+    stale = traces[0]["n_stale"]
+    modes = "".join(chr(int(m)) for m in traces[0]["mode"])
+    for r in range(len(stale)):
+        if r not in lost:
+            assert stale[r] == 0, (r, modes)
+        elif modes[r] == "P":      # parallel queries every active request
+            assert stale[r] > 0, (r, modes)
+    assert stale.sum() > 0
+
+
+@pytest.mark.parametrize("variant", ["ordinary", "parallel", "hybrid"])
+def test_total_loss_trips_breaker_in_periodic_windows(M, variant):
+    """Every reply lost (the reference's drop_prob = 1, tests/test_sim.py:156-173):
+    threshold 3 / cooldown 5 -> speculation-off windows.  The device exchange
+    is synchronous, so a missing reply is a timeout in the round it was due
+    (the reference's simulated channel detects it two commits later): strikes
+    at rounds 1-3 -> window 4-8, strikes 9-11 -> 12-16, 17-19 -> 20-24."""
+    import torch
+    from paper_2605_08151_b200.disagg import DisaggregatedDecoder
+    n = 8
+    pair = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=n, ctx_cap=256, seed=25)
+    spec = _spec(M, n, seed=25, output_len=48)
+    ar = M.decode(pair, spec, "ar", use_graph=False)
+    dd = DisaggregatedDecoder(pair, [(pair, n)], spec, variant)
+    dd.prefill(M.synthetic_prompts(n, spec.prompt_len, M.TINY_TARGET.vocab, spec.seed))
+    dd.run(drop=lambda r, k: True)
+    committed, pos, traces = dd.read()
+    assert torch.equal(committed, ar.committed.cpu())
+    timeline = "".join(chr(int(m)) for m in traces[0]["mode"])
+    for lo, hi in ((4, 8), (12, 16), (20, 24)):       # 1-based round ids
+        assert timeline[lo - 1:hi] == "F" * (hi - lo + 1), timeline
+        assert "F" not in timeline[hi:hi + 3], timeline
+    assert "F" not in timeline[:3]
+    rep = dd.report()
+    assert rep.breaker_activations >= 3
+    assert rep.timeout_rounds == sum(1 for m in timeline if m != "F")
