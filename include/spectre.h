@@ -271,6 +271,20 @@ int spectre_engine_exchange(void* src, void* dst, int32_t direction, int32_t src
                             int32_t dst_req0, int32_t n, void* stream);
 /* Enable direct peer access between two GPUs (both directions; idempotent). */
 int spectre_enable_peer_access(int32_t dev_a, int32_t dev_b);
+/* One process per GPU: export a device pointer (an engine workspace) as a
+ * CUDA IPC handle + offset into its allocation; a peer process opens it
+ * (peer access enabled lazily) and attaches a layout-only engine view built
+ * from the owner's dims and config.  spectre_engine_exchange between a local
+ * engine and an attached view writes directly into the peer's state.  An
+ * attached view supports only exchange and destroy. */
+#define SPECTRE_IPC_HANDLE_BYTES 64
+int spectre_ipc_export(const void* dev_ptr, uint8_t* handle_out, uint64_t* offset_out);
+int spectre_ipc_open(const uint8_t* handle, uint64_t offset, void** base_out,
+                     void** dev_ptr_out);
+int spectre_ipc_close(void* base);
+void* spectre_engine_attach(const SpectreModelDims* target, const SpectreModelDims* draft,
+                            const SpectreDecodeConfig* cfg, void* workspace,
+                            size_t workspace_bytes);
 /* Prefill both models with prompts [n_req][prompt_len] (device int32) and
  * commit output token 0 (target greedy) — admission (target_engine.py:105-126). */
 int spectre_engine_prefill(void* engine, const int32_t* prompts, void* stream);

@@ -128,6 +128,10 @@ def _bind_model(L) -> None:
     _sig(L, "spectre_engine_step", C.c_int, [_P, i32, i32, _P])
     _sig(L, "spectre_engine_exchange", C.c_int, [_P, _P, i32, i32, i32, i32, _P])
     _sig(L, "spectre_enable_peer_access", C.c_int, [i32, i32])
+    _sig(L, "spectre_ipc_export", C.c_int, [_P, _P, C.POINTER(C.c_uint64)])
+    _sig(L, "spectre_ipc_open", C.c_int, [_P, C.c_uint64, C.POINTER(_P), C.POINTER(_P)])
+    _sig(L, "spectre_ipc_close", C.c_int, [_P])
+    _sig(L, "spectre_engine_attach", _P, [_P, _P, _P, _P, C.c_size_t])
     _sig(L, "spectre_engine_workspace_bytes", C.c_size_t,
          [C.POINTER(ModelDims), C.POINTER(ModelDims), C.POINTER(DecodeConfig)])
     _sig(L, "spectre_engine_create", C.c_void_p,

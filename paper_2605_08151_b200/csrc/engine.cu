@@ -348,6 +348,7 @@ struct Engine {
   int warmed = 0;
   int par_draft_ctas = 0, par_target_ctas = 0;   // parallel-round CTA budgets (0: whole GPU)
   int device = 0;
+  int attached = 0;           // layout-only view of a peer process's engine (IPC)
   cudaStream_t s_cap2 = nullptr;
   // rejection sampling (temperature > 0): draft q-store by output position
   int qwin = 0;               // slots per request (positions mod qwin)
@@ -741,7 +742,7 @@ extern "C" int spectre_engine_destroy(void* engine) {
 
 extern "C" int spectre_engine_prefill(void* engine, const int32_t* prompts, void* stream) {
   auto* e = reinterpret_cast<Engine*>(engine);
-  if (!e || !prompts) return arg_fail("spectre_engine_prefill");
+  if (!e || !prompts || e->attached) return arg_fail("spectre_engine_prefill");
   cudaStream_t s = as_stream(stream);
   const int P = e->cfg.prompt_len, cs = e->prefill_cs;
   for (ModelRT* m : {&e->drf, &e->tgt}) {
@@ -760,7 +761,7 @@ extern "C" int spectre_engine_prefill(void* engine, const int32_t* prompts, void
 extern "C" int spectre_engine_run(void* engine, int32_t max_rounds, int32_t use_graph,
                                   int32_t* rounds_run, void* stream) {
   auto* e = reinterpret_cast<Engine*>(engine);
-  if (!e || max_rounds < 0) return arg_fail("spectre_engine_run");
+  if (!e || max_rounds < 0 || e->attached) return arg_fail("spectre_engine_run");
   cudaStream_t caller = as_stream(stream);
   cudaStream_t s = e->s_main;  // capturable stream, ordered after the caller's work
   SPECTRE_CUDA_TRY(cudaEventRecord(e->ev_in, caller));
@@ -902,7 +903,7 @@ extern "C" int spectre_engine_forward(void* engine, int32_t which, const int32_t
 
 extern "C" int spectre_engine_step(void* engine, int32_t step, int32_t mode, void* stream) {
   auto* e = reinterpret_cast<Engine*>(engine);
-  if (!e) return arg_fail("spectre_engine_step");
+  if (!e || e->attached) return arg_fail("spectre_engine_step");
   cudaStream_t s = as_stream(stream);
   switch (step) {
     case SPECTRE_STEP_BEGIN: {
@@ -995,4 +996,76 @@ extern "C" int spectre_enable_peer_access(int32_t dev_a, int32_t dev_b) {
   }
   SPECTRE_CUDA_TRY(cudaSetDevice(cur));
   return SPECTRE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// One process per GPU (config 5): a peer process maps this engine's workspace
+// through CUDA IPC and attaches a layout-only view of it, so
+// spectre_engine_exchange writes straight into the peer's state (NVLink peer
+// copies across GPUs; the same device also works).
+
+#include <cuda.h>
+
+extern "C" int spectre_ipc_export(const void* dev_ptr, uint8_t* handle_out, uint64_t* offset_out) {
+  if (!dev_ptr || !handle_out || !offset_out) return arg_fail("spectre_ipc_export");
+  // allocation base: the IPC handle names the whole cudaMalloc block
+  using AddrRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static AddrRange get_range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<AddrRange>(fn);
+  }();
+  if (!get_range) return arg_fail("spectre_ipc_export: cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return arg_fail("spectre_ipc_export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  SPECTRE_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(h) == SPECTRE_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = reinterpret_cast<uint64_t>(dev_ptr) - static_cast<uint64_t>(base);
+  return SPECTRE_OK;
+}
+
+extern "C" int spectre_ipc_open(const uint8_t* handle, uint64_t offset, void** base_out,
+                                void** dev_ptr_out) {
+  if (!handle || !base_out || !dev_ptr_out) return arg_fail("spectre_ipc_open");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  SPECTRE_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *base_out = base;
+  *dev_ptr_out = static_cast<char*>(base) + offset;
+  return SPECTRE_OK;
+}
+
+extern "C" int spectre_ipc_close(void* base) {
+  if (!base) return arg_fail("spectre_ipc_close");
+  SPECTRE_CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return SPECTRE_OK;
+}
+
+extern "C" void* spectre_engine_attach(const SpectreModelDims* target,
+                                       const SpectreModelDims* draft,
+                                       const SpectreDecodeConfig* cfg, void* workspace,
+                                       size_t workspace_bytes) {
+  if (!dims_ok(target) || !dims_ok(draft) || !cfg || !workspace) {
+    arg_fail("spectre_engine_attach");
+    return nullptr;
+  }
+  auto e = std::make_unique<Engine>();
+  e->configure(*target, SpectreModelWeights{}, *draft, SpectreModelWeights{}, *cfg);
+  Bump b{reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255))};
+  e->layout(b);   // same dims + config -> the owner's exact layout
+  if (b.off + 256 > workspace_bytes) {
+    arg_fail("spectre_engine_attach: workspace too small");
+    return nullptr;
+  }
+  e->attached = 1;
+  return e.release();
 }
