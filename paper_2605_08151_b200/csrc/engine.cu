@@ -185,8 +185,16 @@ struct ModelRT {
       // SwiGLU needs full K per tile: 128-row tiles when they fit one wave
       // (draft), else 256-row tiles (two accumulators share every X stage)
       const bool gu128 = (2 * F) / 128 <= gemm_sk_grid();
-      TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
-                    1, 0, 0, gu128 ? 128 : 256));
+      static const bool gu_sk = [] {   // stream-K SwiGLU (owner fix-up) for 256-row tiles
+        const char* v = getenv("SPECTRE_GU_SK");
+        return v && atoi(v) != 0;
+      }();
+      if (gu_sk && !gu128)
+        TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
+                      1, 0, 0, 256, sk_part, sk_flag));
+      else
+        TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
+                      1, 0, 0, gu128 ? 128 : 256));
       TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
                     0, 0, tr));
       if (half_gemm) {

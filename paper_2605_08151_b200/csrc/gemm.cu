@@ -288,6 +288,29 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
     if (int e = gemm_set_half(&p)) return e;
   if (int e = gemm_set_outputs(&p, partial, amax_val, amax_idx, act, ld_act)) return e;
   if (const char* dg = getenv("SPECTRE_GEMM_DIAG")) p.args.diag = atoi(dg);
+  static unsigned long long* stall = nullptr;
+  if (getenv("SPECTRE_GEMM_STALL")) {   // producer / MMA wait and issue cycles per stage
+    if (!stall) SPECTRE_CUDA_TRY(cudaMalloc(&stall, 2 * 148 * 4 * 8));
+    SPECTRE_CUDA_TRY(cudaMemsetAsync(stall, 0, 2 * 148 * 4 * 8, as_stream(stream)));
+    p.args.stall = stall;
+    int r = gemm_run(p, as_stream(stream));
+    std::vector<unsigned long long> h(2 * 148 * 4);
+    SPECTRE_CUDA_TRY(cudaMemcpyAsync(h.data(), stall, h.size() * 8, cudaMemcpyDeviceToHost,
+                                     as_stream(stream)));
+    SPECTRE_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+    double e = 0, f = 0, is = 0, n = 0;
+    for (int c = 0; c < p.grid; ++c) {
+      e += h[c * 4];
+      f += h[c * 4 + 1];
+      is += h[c * 4 + 2];
+      n += h[c * 4 + 3];
+    }
+    printf("stall grid %d stages/cta %.1f  per stage cycles: producer empty-wait %.0f  "
+           "mma full-wait %.0f  mma issue %.0f\n",
+           p.grid, n / p.grid, e / n, f / n, is / n);
+    fflush(stdout);
+    return r;
+  }
   static unsigned long long* dbg = nullptr;
   if (getenv("SPECTRE_GEMM_DBG")) {
     if (!dbg) SPECTRE_CUDA_TRY(cudaMalloc(&dbg, 148 * 8 * 8));

@@ -96,6 +96,8 @@ struct GemmArgs {
   long long pf_bytes;       //   (static data, so issued before griddepcontrol.wait)
   GemmPost post;            // fused split-K reduction phase (gemm_post.cuh)
   int l2_ahead;             // producer L2-prefetches weight boxes this many k-steps ahead
+  unsigned long long* stall;   // diagnostics: per CTA {producer empty-wait, MMA full-wait,
+                               // MMA issue, stages} in cycles (null = off)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -304,6 +306,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       pdl_wait();
       pdl_trigger();
       int g = 0;
+      long long st_empty = 0;
       for (; have; have = sched.next(j)) {
         const int x_boxes = (j.nt + 63) >> 6;
         const uint32_t tx = (uint32_t)j.boxes * kWBox + (uint32_t)x_boxes * kXBox;
@@ -317,7 +320,11 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
             for (int b = 0; b < j.boxes; ++b)
               tma_prefetch_2d(&tmap_w, (k + a.l2_ahead) * BK, n0 + b * 128);
           if (g >= pre) {
-            if (g >= stages) mbar_wait(&empty[s], ((uint32_t)(g / stages) & 1u) ^ 1u);
+            if (g >= stages) {
+              const long long t_w = a.stall ? clock64() : 0;
+              mbar_wait(&empty[s], ((uint32_t)(g / stages) & 1u) ^ 1u);
+              if (a.stall) st_empty += clock64() - t_w;
+            }
             mbar_arrive_expect_tx(&full[s], tx);
             for (int b = 0; b < j.boxes; ++b)
               tma_load_2d(st + b * kWBox, &tmap_w, &full[s], k * BK, n0 + b * 128, pol_w);
@@ -326,6 +333,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
             tma_load_2d(st + w_bytes + b * kXBox, &tmap_x, &full[s], k * BK, j.t0 + b * 64, pol_x);
         }
       }
+      if (a.stall) a.stall[blockIdx.x * 4 + 0] = (unsigned long long)st_empty;
     } else {
       pdl_wait();
       pdl_trigger();
@@ -334,6 +342,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread)
     int g = 0, jn = 0;
+    long long st_full = 0, st_issue = 0;
     GemmJob j;
     while (sched.next(j)) {
       const int t_pad = (j.nt + 15) & ~15;
@@ -349,7 +358,10 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       }
       for (int k = j.k0; k < j.k1; ++k, ++g) {
         const int s = g % stages;
+        const long long t_w = a.stall ? clock64() : 0;
         mbar_wait(&full[s], (uint32_t)(g / stages) & 1u);
+        const long long t_i = a.stall ? clock64() : 0;
+        st_full += t_i - t_w;
         tc_fence_after();
         if (lane == 0 && !(a.diag & 1)) {
           const uint32_t sa = smem_u32(pipe + s * stage_bytes);
@@ -375,10 +387,16 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
           mma_commit(&empty[s]);
         }
         __syncwarp();
+        if (a.stall) st_issue += clock64() - t_i;
       }
       if (lane == 0) mma_commit(&tmem_full[buf]);
       __syncwarp();
       ++jn;
+    }
+    if (a.stall && lane == 0) {
+      a.stall[blockIdx.x * 4 + 1] = (unsigned long long)st_full;
+      a.stall[blockIdx.x * 4 + 2] = (unsigned long long)st_issue;
+      a.stall[blockIdx.x * 4 + 3] = (unsigned long long)g;
     }
   } else {
     // ---------------- epilogue warps 2..9: lane quarter q = warp % 4, group = (warp-2)/4

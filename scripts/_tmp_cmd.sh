@@ -1,1 +1,1 @@
-for a in 0 4 8 16; do echo "== l2 ahead $a"; SPECTRE_GEMM_L2_AHEAD=$a SPECTRE_GEMM_DBG=1 timeout 300 python scripts/one_gemm.py 16384 2048 2 64 1000 1 > gpurun_out/dbg.txt 2>&1; grep "cta 127" gpurun_out/dbg.txt | tail -1; SPECTRE_GEMM_L2_AHEAD=$a timeout 300 python scripts/kprof.py --variant ordinary --warm-rounds 160 --rounds 3 2>&1 | grep -E "phase (draft|target)|swapab"; done
+for v in 0 1; do echo "== GU_SK=$v"; SPECTRE_GU_SK=$v timeout 600 python scripts/kprof.py --variant ordinary --warm-rounds 160 --rounds 3 2>&1 | grep -E "phase|<2, 64, 0>"; done
