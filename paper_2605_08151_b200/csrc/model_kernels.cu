@@ -216,6 +216,82 @@ __global__ void __launch_bounds__(128) k_qkv_rope_kv(const float* __restrict__ p
   }
 }
 
+// Vectorised variant: four consecutive pairs per thread (float4 partial loads,
+// 8-byte bf16 stores); per element the same split order and arithmetic.
+__device__ __forceinline__ void st_bf16x4(__nv_bfloat16* dst, float a0, float a1, float a2,
+                                          float a3) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a0, a1), hi = __floats2bfloat162_rn(a2, a3);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(dst) = u;
+}
+
+__global__ void __launch_bounds__(128) k_qkv_rope_kv4(const float* __restrict__ part, int splits,
+                                                      int rows_cap, const int* __restrict__ t_dev,
+                                                      const int* __restrict__ tok_pos,
+                                                      const int* __restrict__ tok_slot,
+                                                      const float2* __restrict__ rope,
+                                                      __nv_bfloat16* __restrict__ q,
+                                                      __nv_bfloat16* __restrict__ kc,
+                                                      __nv_bfloat16* __restrict__ vc, int n_q,
+                                                      int n_kv, int hd, int ctx_cap) {
+  pdl_wait();
+  pdl_trigger();
+  const int T = *t_dev;
+  const int half = hd / 2;
+  const int n_quads = (n_q + 2 * n_kv) * half / 4;
+  const int per_tok = (n_quads + 127) / 128;
+  const int N = (n_q + 2 * n_kv) * hd;
+  const size_t sstride = (size_t)rows_cap * N;
+  for (int wi = blockIdx.x; wi < T * per_tok; wi += gridDim.x) {   // (token, quad block)
+    const int t = wi / per_tok;
+    const int c = ((wi % per_tok) * 128 + threadIdx.x) * 4;        // first pair index
+    if (c >= n_quads * 4) continue;
+    const int head = c / half, i = c % half;
+    const float* p0 = part + (size_t)t * N + head * hd + i;
+    float4 la[kMaxSplits], lb[kMaxSplits];
+#pragma unroll
+    for (int sp = 0; sp < kMaxSplits; ++sp)
+      if (sp < splits) {
+        la[sp] = __ldg(reinterpret_cast<const float4*>(p0 + sp * sstride));
+        lb[sp] = __ldg(reinterpret_cast<const float4*>(p0 + sp * sstride + half));
+      }
+    float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int sp = 0; sp < kMaxSplits; ++sp)
+      if (sp < splits) {
+        a[0] += la[sp].x; a[1] += la[sp].y; a[2] += la[sp].z; a[3] += la[sp].w;
+        b[0] += lb[sp].x; b[1] += lb[sp].y; b[2] += lb[sp].z; b[3] += lb[sp].w;
+      }
+    const int pos = tok_pos[t];
+    if (head < n_q + n_kv) {
+      const float4* cs4 = reinterpret_cast<const float4*>(rope + (size_t)pos * half + i);
+      const float4 c01 = cs4[0], c23 = cs4[1];
+      const float cx[4] = {c01.x, c01.z, c23.x, c23.z}, cy[4] = {c01.y, c01.w, c23.y, c23.w};
+      float ra[4], rb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        ra[k] = a[k] * cx[k] - b[k] * cy[k];
+        rb[k] = b[k] * cx[k] + a[k] * cy[k];
+      }
+      __nv_bfloat16* dst;
+      if (head < n_q) {
+        dst = q + ((size_t)t * n_q + head) * hd;
+      } else {
+        dst = kc + (((size_t)tok_slot[t] * n_kv + (head - n_q)) * ctx_cap + pos) * hd;
+      }
+      st_bf16x4(dst + i, ra[0], ra[1], ra[2], ra[3]);
+      st_bf16x4(dst + i + half, rb[0], rb[1], rb[2], rb[3]);
+    } else {
+      __nv_bfloat16* dst =
+          vc + (((size_t)tok_slot[t] * n_kv + (head - n_q - n_kv)) * ctx_cap + pos) * hd;
+      st_bf16x4(dst + i, a[0], a[1], a[2], a[3]);
+      st_bf16x4(dst + i + half, b[0], b[1], b[2], b[3]);
+    }
+  }
+}
+
 // ------------------------------------------------------------ argmax reduce
 // (max, lowest index) over the lm_head tiles for each token row.
 __global__ void __launch_bounds__(256) k_argmax_reduce(const float* __restrict__ val,
@@ -286,8 +362,8 @@ __global__ void k_rope_table(float2* rope, int ctx_cap, int hd, double theta) {
 constexpr int kSms = 148;
 static int rope_ctas_per_sm() {
   static const int v = [] {
-    const char* e = getenv("SPECTRE_ROPE_CTAS");   // measured: 24 per SM hides the load chains
-    return e ? atoi(e) : 24;
+    const char* e = getenv("SPECTRE_ROPE_CTAS");   // measured: 24 per SM (scalar), 8 (float4)
+    return e ? atoi(e) : 0;
   }();
   return v;
 }
@@ -335,8 +411,25 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
                        cudaStream_t s) {
   if (splits > kMaxSplits) return arg_fail("qkv_rope_kv: splits");
   const int pairs = (n_q + 2 * n_kv) * hd / 2;
+  static const bool vec4 = [] {
+    const char* e = getenv("SPECTRE_ROPE_VEC");   // 0: one pair per thread
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (vec4 && (hd / 2) % 4 == 0) {
+    const int quads = pairs / 4;
+    SPECTRE_LAUNCH_PDL("k_qkv_rope_kv4", k_qkv_rope_kv4,
+                       dim3(cap_grid(std::min(t_cap * ((quads + 127) / 128),
+                                              (rope_ctas_per_sm() ? rope_ctas_per_sm() : 8) * kSms))),
+                       dim3(128), 0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
+                       reinterpret_cast<const float2*>(rope), reinterpret_cast<__nv_bfloat16*>(q),
+                       reinterpret_cast<__nv_bfloat16*>(kc), reinterpret_cast<__nv_bfloat16*>(vc),
+                       n_q, n_kv, hd, ctx_cap);
+    return SPECTRE_OK;
+  }
   SPECTRE_LAUNCH_PDL("k_qkv_rope_kv", k_qkv_rope_kv,
-                     dim3(cap_grid(std::min(t_cap * ((pairs + 127) / 128), rope_ctas_per_sm() * kSms))), dim3(128),
+                     dim3(cap_grid(std::min(t_cap * ((pairs + 127) / 128),
+                                            (rope_ctas_per_sm() ? rope_ctas_per_sm() : 24) * kSms))),
+                     dim3(128),
                      0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
                      reinterpret_cast<const float2*>(rope), reinterpret_cast<__nv_bfloat16*>(q),
                      reinterpret_cast<__nv_bfloat16*>(kc), reinterpret_cast<__nv_bfloat16*>(vc),
