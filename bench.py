@@ -259,6 +259,24 @@ def run_ours(args):
     roof = None
     if not args.no_roofline and rank == 0:
         roof = roofline_gate_up(pair, args)
+    # ---- whole-round roofline: algorithmic HBM bytes of one ordinary
+    # round at the run's mean context vs the measured ordinary round time
+    round_roof = None
+    if "ordinary" in results and args.temperature <= 0:
+        peaks, src = load_peaks()
+        r = results["ordinary"]
+        ctx = args.prompt_len + args.out_len / 2.0
+        tgt, drf = M.LLAMA_31_8B, M.LLAMA_32_1B
+        bytes_t = 2 * linear_params(tgt) + B * ctx * kv_bytes_per_token(tgt)
+        bytes_d = 2 * linear_params(drf) + B * ctx * kv_bytes_per_token(drf)
+        rbytes = bytes_t + (g - 1) * bytes_d
+        ideal_ms = rbytes / (peaks["hbm_gbs"] * 1e9) * 1e3
+        committed_per_round = tokens_per_step / max(1, r["rounds"])
+        round_roof = {"mode": "ordinary", "bytes": int(rbytes), "mean_ctx": ctx,
+                      "ms_at_hbm_peak": round(ideal_ms, 3), "measured_ms": round(r["t_round_ms"], 3),
+                      "frac": round(ideal_ms / r["t_round_ms"], 4),
+                      "tok_s_at_roofline": round(committed_per_round / ideal_ms * 1e3, 1),
+                      "peak_source": src}
     # ---- CPU baseline (oracle port of the reference loop), rank 0, N=1 only
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and ws == 1:
@@ -284,7 +302,7 @@ def run_ours(args):
                        "draft_alpha": args.alpha, "branch_scale": args.branch,
                        "controller": args.controller, "parallelism": f"dp{ws} (request shards)",
                        "l2": "inputs > L2 (15 GB weights + KV streamed per round)"},
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "roofline": roof, "round_roofline": round_roof, "cpu_baseline": cpu,
             "clocks": head["clocks"], "gpu_launches": head["gpu_launches"],
             "modes": {v: {k: (round(x, 4) if isinstance(x, float) else x)
                           for k, x in r.items() if k not in ("clocks", "timeline")}
@@ -292,6 +310,19 @@ def run_ours(args):
             "timeline_head": head["timeline"][:80],
         }
         print(json.dumps(line))
+
+
+def linear_params(spec) -> int:
+    """Weights streamed by one forward pass: every layer's linears + lm_head
+    (SURVEY §8d P_T / P_D; embeddings are row lookups, norms negligible)."""
+    d, hd = spec.d_model, spec.head_dim
+    per_layer = (d * (spec.n_q_heads + 2 * spec.n_kv_heads) * hd + spec.n_q_heads * hd * d +
+                 3 * d * spec.ffn)
+    return spec.n_layers * per_layer + spec.vocab * d
+
+
+def kv_bytes_per_token(spec) -> int:
+    return spec.n_layers * spec.n_kv_heads * spec.head_dim * 2 * 2
 
 
 def alpha_from_L(L: float, gamma: int) -> float:

@@ -113,3 +113,21 @@ def test_host_accounting_reproduces_reference_reports(golden_runs, idx):
     assert [vars(t) for t in res.round_trace] == case["round_trace"]
     assert [vars(t) for t in res.draft_records] == case["draft_records"]
     assert res.channel_counters == case["channel_counters"]
+
+
+def test_bench_round_roofline_matches_survey_figures():
+    """bench.py's whole-round roofline uses SURVEY §8d's algorithmic bytes:
+    P_T = 7,504,658,432, P_D = 1,235,746,816, KV 131,072 / 32,768 B per token,
+    C2 ordinary round (ctx 640) = 20.38 + 3 x 3.81 GB."""
+    import sys
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import bench
+    from paper_2605_08151_b200 import model as M
+    t, d = M.LLAMA_31_8B, M.LLAMA_32_1B
+    assert bench.linear_params(t) == 7_504_658_432
+    assert bench.linear_params(d) == 1_235_746_816
+    assert bench.kv_bytes_per_token(t) == 131_072
+    assert bench.kv_bytes_per_token(d) == 32_768
+    bt = 2 * bench.linear_params(t) + 64 * 640 * bench.kv_bytes_per_token(t)
+    bd = 2 * bench.linear_params(d) + 64 * 640 * bench.kv_bytes_per_token(d)
+    assert abs(bt / 1e9 - 20.38) < 0.01 and abs(bd / 1e9 - 3.81) < 0.01
