@@ -96,6 +96,7 @@ struct ModelRT {
   SpectreModelWeights w{};
   int n_req = 0, rows_cap = 0, ctx_cap = 0, max_new = 1, split_max = 1, rb_cap = 1;
   int sp_qkv = 1, sp_o = 1, sp_d = 1;
+  int tr_qkv = 256, tr_o = 256, tr_d = 256;   // weight rows per tile, per GEMM
   int tile_rows = 256;   // weight rows per GEMM CTA (128 for small-T models)
   long long pf_cap = 0;   // L2 prefetch of the next GEMM's weights (bytes; measured: off)
   bool half_gemm = false; // decode GEMMs in the half-SM config (2 CTAs per SM, 128-row tiles)
@@ -129,9 +130,20 @@ struct ModelRT {
     const int d = dm.d_model, R = rows_cap;
     const int qd = dm.n_q_heads * dm.head_dim;
     const int tr = half_gemm ? 128 : tile_rows, ctas = half_gemm ? 296 : 148;
-    sp_qkv = pick_splits((nqkv() + tr - 1) / tr, d / 64, ctas);
-    sp_o = pick_splits((d + tr - 1) / tr, qd / 64, ctas);
-    sp_d = pick_splits((d + tr - 1) / tr, dm.ffn / 64, ctas);
+    tr_qkv = tr_o = tr_d = tr;
+    if (!half_gemm) {
+      // per-GEMM tile height.  q/k/v and o: 128-row tiles halve the split
+      // count, and at T=256 the fp32 split-K partials (s*T*N*4 B, written and
+      // re-read) cost as much HBM as the weights; measured -0.12 ms/round.
+      // down (K = ffn) keeps 256-row tiles (its partials are 0.3x its weights).
+      tr_qkv = tr_o = 128;
+      if (const char* v = getenv("SPECTRE_QKV_TILE")) tr_qkv = atoi(v) == 128 ? 128 : tr;
+      if (const char* v = getenv("SPECTRE_O_TILE")) tr_o = atoi(v) == 128 ? 128 : tr;
+      if (const char* v = getenv("SPECTRE_DOWN_TILE")) tr_d = atoi(v) == 128 ? 128 : tr;
+    }
+    sp_qkv = pick_splits((nqkv() + tr_qkv - 1) / tr_qkv, d / 64, ctas);
+    sp_o = pick_splits((d + tr_o - 1) / tr_o, qd / 64, ctas);
+    sp_d = pick_splits((d + tr_d - 1) / tr_d, dm.ffn / 64, ctas);
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
     attn_chunk = attn_chunk_default();
     split_max = (ctx_cap + attn_chunk - 1) / attn_chunk;
@@ -179,9 +191,9 @@ struct ModelRT {
     const int tr = half_gemm ? 128 : tile_rows;
     for (int l = 0; l < L; ++l) {
       TRY(gemm_plan(&pq[l], bf(w.wqkv) + (size_t)l * nqkv() * d, nqkv(), d, x, rows_cap,
-                    kPartial, sp_qkv, 0, 0, tr));
+                    kPartial, sp_qkv, 0, 0, tr_qkv));
       TRY(gemm_plan(&po[l], bf(w.wo) + (size_t)l * d * qd, d, qd, attn, rows_cap, kPartial,
-                    sp_o, 0, 0, tr));
+                    sp_o, 0, 0, tr_o));
       // SwiGLU needs full K per tile: 128-row tiles when they fit one wave
       // (draft), else 256-row tiles (two accumulators share every X stage)
       const bool gu128 = (2 * F) / 128 <= gemm_sk_grid();
@@ -196,7 +208,7 @@ struct ModelRT {
         TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
                       1, 0, 0, gu128 ? 128 : 256));
       TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
-                    0, 0, tr));
+                    0, 0, tr_d));
       if (half_gemm) {
         // partial GEMMs only: the SwiGLU GEMM measured faster in the full config
         for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) TRY(gemm_set_half(p));
