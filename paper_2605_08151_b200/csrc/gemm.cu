@@ -187,12 +187,21 @@ static int l2_ahead_default() {
   return v;
 }
 
+static int ksub_env() {
+  static const int v = [] {
+    const char* e = getenv("SPECTRE_GEMM_KSUB");   // k blocks per stage override (1 / 2)
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 int gemm_run(const GemmPlan& p0, cudaStream_t s) {
   GemmPlan stripped;
   const GemmPlan* pp = &p0;
-  if (l2_ahead_default() != p0.args.l2_ahead) {
+  if (l2_ahead_default() != p0.args.l2_ahead || (ksub_env() && ksub_env() != p0.args.ksub)) {
     stripped = p0;
     stripped.args.l2_ahead = l2_ahead_default();
+    if (ksub_env()) stripped.args.ksub = ksub_env();
     pp = &stripped;
   }
   if (p0.args.post.kind != kPostNone && no_grid_sync_ref()) {   // concurrent: no grid barrier

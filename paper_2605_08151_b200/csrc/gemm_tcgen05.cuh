@@ -96,6 +96,7 @@ struct GemmArgs {
   long long pf_bytes;       //   (static data, so issued before griddepcontrol.wait)
   GemmPost post;            // fused split-K reduction phase (gemm_post.cuh)
   int l2_ahead;             // producer L2-prefetches weight boxes this many k-steps ahead
+  int ksub;                 // 1: one BK block per stage; 0: two when >= 2 such stages fit
   unsigned long long* stall;   // diagnostics: per CTA {producer empty-wait, MMA full-wait,
                                // MMA issue, stages} in cycles (null = off)
 };
@@ -220,7 +221,15 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   const bool wide = (T <= 256 && a.tile_rows == 256);
   const int w_bytes = wide ? 2 * kWBox : kWBox;
   const int x_rows = wide ? ((T + 63) & ~63) : min((T + 63) & ~63, Cfg::kPass);
-  const int stage_bytes = w_bytes + x_rows * kRow;
+  // a stage holds `ksub` consecutive BK-wide k blocks (one expect-tx, one
+  // MMA commit): fewer commit groups per byte when the MMAs are small (T=64)
+  const int sub_bytes = w_bytes + x_rows * kRow;
+  // two k blocks per stage whenever >= 2 such stages fit (measured: draft
+  // SwiGLU 27.3 -> 22.5 us, draft lm_head 107 -> 98 us, target 128-row q/k/v/o
+  // GEMMs -0.12 ms/round); a.ksub = 1 forces one block, >= 3 raises the minimum
+  const int ksub_min_stages = a.ksub >= 2 ? a.ksub : 2;
+  const int ksub = (a.ksub != 1 && ksub_min_stages * 2 * sub_bytes <= kPipeB) ? 2 : 1;
+  const int stage_bytes = ksub * sub_bytes;
   int stages = stage_bytes > 0 ? kPipeB / stage_bytes : 1;
   stages = stages > kGemmMaxStages ? kGemmMaxStages : (stages < 1 ? 1 : stages);
   if (a.max_stages > 0 && stages > a.max_stages) stages = a.max_stages;
@@ -295,12 +304,14 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       if (have) {
         const int x_boxes = (j.nt + 63) >> 6;
         const uint32_t tx = (uint32_t)j.boxes * kWBox + (uint32_t)x_boxes * kXBox;
-        pre = min(j.k1 - j.k0, stages);
+        pre = min((j.k1 - j.k0 + ksub - 1) / ksub, stages);
         for (int i = 0; i < pre; ++i) {
-          mbar_arrive_expect_tx(&full[i], tx);
-          for (int b = 0; b < j.boxes; ++b)
-            tma_load_2d(pipe + i * stage_bytes + b * kWBox, &tmap_w, &full[i], (j.k0 + i) * BK,
-                        j.tile * a.tile_rows + j.row_off + b * 128, pol_w);
+          const int kb = j.k0 + i * ksub, nk = min(ksub, j.k1 - kb);
+          mbar_arrive_expect_tx(&full[i], tx * (uint32_t)nk);
+          for (int q = 0; q < nk; ++q)
+            for (int b = 0; b < j.boxes; ++b)
+              tma_load_2d(pipe + i * stage_bytes + q * sub_bytes + b * kWBox, &tmap_w, &full[i],
+                          (kb + q) * BK, j.tile * a.tile_rows + j.row_off + b * 128, pol_w);
         }
       }
       pdl_wait();
@@ -311,8 +322,9 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
         const int x_boxes = (j.nt + 63) >> 6;
         const uint32_t tx = (uint32_t)j.boxes * kWBox + (uint32_t)x_boxes * kXBox;
         const int n0 = j.tile * a.tile_rows + j.row_off;
-        for (int k = j.k0; k < j.k1; ++k, ++g) {
+        for (int k = j.k0; k < j.k1; k += ksub, ++g) {
           const int s = g % stages;
+          const int nk = min(ksub, j.k1 - k);
           uint8_t* st = pipe + s * stage_bytes;
           // L2 prefetch one ring ahead: the smem ring then refills from L2
           // instead of waiting a full HBM round trip per slot
@@ -325,12 +337,16 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
               mbar_wait(&empty[s], ((uint32_t)(g / stages) & 1u) ^ 1u);
               if (a.stall) st_empty += clock64() - t_w;
             }
-            mbar_arrive_expect_tx(&full[s], tx);
-            for (int b = 0; b < j.boxes; ++b)
-              tma_load_2d(st + b * kWBox, &tmap_w, &full[s], k * BK, n0 + b * 128, pol_w);
+            mbar_arrive_expect_tx(&full[s], tx * (uint32_t)nk);
+            for (int q = 0; q < nk; ++q)
+              for (int b = 0; b < j.boxes; ++b)
+                tma_load_2d(st + q * sub_bytes + b * kWBox, &tmap_w, &full[s], (k + q) * BK,
+                            n0 + b * 128, pol_w);
           }
-          for (int b = 0; b < x_boxes; ++b)
-            tma_load_2d(st + w_bytes + b * kXBox, &tmap_x, &full[s], k * BK, j.t0 + b * 64, pol_x);
+          for (int q = 0; q < nk; ++q)
+            for (int b = 0; b < x_boxes; ++b)
+              tma_load_2d(st + q * sub_bytes + w_bytes + b * kXBox, &tmap_x, &full[s],
+                          (k + q) * BK, j.t0 + b * 64, pol_x);
         }
       }
       if (a.stall) a.stall[blockIdx.x * 4 + 0] = (unsigned long long)st_empty;
@@ -356,19 +372,21 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
         mbar_wait(&tmem_empty[buf], (uint32_t)((jn / nbuf) - 1) & 1u);
         tc_fence_after();
       }
-      for (int k = j.k0; k < j.k1; ++k, ++g) {
+      for (int k = j.k0; k < j.k1; k += ksub, ++g) {
         const int s = g % stages;
+        const int nk = min(ksub, j.k1 - k);
         const long long t_w = a.stall ? clock64() : 0;
         mbar_wait(&full[s], (uint32_t)(g / stages) & 1u);
         const long long t_i = a.stall ? clock64() : 0;
         st_full += t_i - t_w;
         tc_fence_after();
         if (lane == 0 && !(a.diag & 1)) {
-          const uint32_t sa = smem_u32(pipe + s * stage_bytes);
+          for (int q = 0; q < nk; ++q) {
+          const uint32_t sa = smem_u32(pipe + s * stage_bytes + q * sub_bytes);
           const uint32_t xa = sa + (uint32_t)w_bytes;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t accf = (k > j.k0 || kk > 0) ? 1u : 0u;
+            const uint32_t accf = (k > j.k0 || q > 0 || kk > 0) ? 1u : 0u;
             const uint64_t bd = umma_desc_kmajor<kRow>(xa + kk * 32);
             if (j.boxes == 2) {
               mma_bf16_ss(acc, umma_desc_kmajor<kRow>(sa + kk * 32), bd, id0, accf);
@@ -381,6 +399,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
                 mma_bf16_ss(acc + 256, ad, umma_desc_kmajor<kRow>(xa + 256 * kRow + kk * 32),
                             id1, accf);
             }
+          }
           }
           mma_commit(&empty[s]);
         } else if (lane == 0) {
