@@ -198,10 +198,16 @@ static int ksub_env() {
 int gemm_run(const GemmPlan& p0, cudaStream_t s) {
   GemmPlan stripped;
   const GemmPlan* pp = &p0;
-  if (l2_ahead_default() != p0.args.l2_ahead || (ksub_env() && ksub_env() != p0.args.ksub)) {
+  static const int ksub_max_env = [] {
+    const char* e = getenv("SPECTRE_GEMM_KSUBMAX");
+    return e ? atoi(e) : 0;
+  }();
+  if (l2_ahead_default() != p0.args.l2_ahead || (ksub_env() && ksub_env() != p0.args.ksub) ||
+      (ksub_max_env && ksub_max_env != p0.args.ksub_max)) {
     stripped = p0;
     stripped.args.l2_ahead = l2_ahead_default();
     if (ksub_env()) stripped.args.ksub = ksub_env();
+    if (ksub_max_env) stripped.args.ksub_max = ksub_max_env;
     pp = &stripped;
   }
   if (p0.args.post.kind != kPostNone && no_grid_sync_ref()) {   // concurrent: no grid barrier

@@ -97,6 +97,7 @@ struct GemmArgs {
   GemmPost post;            // fused split-K reduction phase (gemm_post.cuh)
   int l2_ahead;             // producer L2-prefetches weight boxes this many k-steps ahead
   int ksub;                 // 1: one BK block per stage; 0: two when >= 2 such stages fit
+  int ksub_max;             // most BK blocks per stage (0: 4)
   unsigned long long* stall;   // diagnostics: per CTA {producer empty-wait, MMA full-wait,
                                // MMA issue, stages} in cycles (null = off)
 };
@@ -228,7 +229,14 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   // SwiGLU 27.3 -> 22.5 us, draft lm_head 107 -> 98 us, target 128-row q/k/v/o
   // GEMMs -0.12 ms/round); a.ksub = 1 forces one block, >= 3 raises the minimum
   const int ksub_min_stages = a.ksub >= 2 ? a.ksub : 2;
-  const int ksub = (a.ksub != 1 && ksub_min_stages * 2 * sub_bytes <= kPipeB) ? 2 : 1;
+  const int ksub_max = a.ksub_max > 0 ? a.ksub_max : 4;   // draft SwiGLU: 22.5 -> 21.1 us at 4
+  int ksub = 1;
+  if (a.ksub != 1)
+    for (int c = ksub_max; c >= 2; --c)
+      if (ksub_min_stages * c * sub_bytes <= kPipeB) {
+        ksub = c;
+        break;
+      }
   const int stage_bytes = ksub * sub_bytes;
   int stages = stage_bytes > 0 ? kPipeB / stage_bytes : 1;
   stages = stages > kGemmMaxStages ? kGemmMaxStages : (stages < 1 ? 1 : stages);
