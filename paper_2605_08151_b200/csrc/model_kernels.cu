@@ -86,32 +86,52 @@ __global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restr
                                                              float* __restrict__ h,
                                                              __nv_bfloat16* __restrict__ x,
                                                              int d, float eps) {
+  __shared__ float sh[40];
+  const int nv = d >> 2;
+  const size_t sstride = (size_t)rows_cap * d / 4;
+  const float4* w4 = reinterpret_cast<const float4*>(w);
+  // Before griddepcontrol.wait: everything that does not come from the
+  // preceding (split-K GEMM) launch.  The row count, the residual row and the
+  // norm weight were written at least two launches back, and the preceding
+  // launch itself waited for its predecessor before releasing this grid.
+  const int T = *t_dev;
+  float4 wv[kVec], hv[kVec];
+  if ((int)blockIdx.x < T) {
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int i = threadIdx.x + j * blockDim.x;
+      if (i < nv) {
+        wv[j] = __ldg(w4 + i);
+        hv[j] = reinterpret_cast<const float4*>(h + (size_t)blockIdx.x * d)[i];
+      }
+    }
+  }
   pdl_wait();
   pdl_trigger();
-  __shared__ float sh[40];
-  const int T = *t_dev;
   for (int t = blockIdx.x; t < T; t += gridDim.x) {   // grid-stride over the live rows
-  const int nv = d >> 2;
-  float4 v[kVec];
-  const float4* h4 = reinterpret_cast<const float4*>(h + (size_t)t * d);
-  const size_t sstride = (size_t)rows_cap * d / 4;
-  const float4* p4 = reinterpret_cast<const float4*>(part + (size_t)t * d);
+  if (t != (int)blockIdx.x) {
 #pragma unroll
-  for (int j = 0; j < kVec; ++j) {
-    const int i = threadIdx.x + j * blockDim.x;
-    if (i < nv) {
-      float4 acc = h4[i];
-      float4 ld[kMaxSplits];
-#pragma unroll
-      for (int sp = 0; sp < kMaxSplits; ++sp)
-        if (sp < splits) ld[sp] = __ldg(p4 + sp * sstride + i);
-#pragma unroll
-      for (int sp = 0; sp < kMaxSplits; ++sp)
-        if (sp < splits) {
-          acc.x += ld[sp].x; acc.y += ld[sp].y; acc.z += ld[sp].z; acc.w += ld[sp].w;
-        }
-      v[j] = acc;
+    for (int j = 0; j < kVec; ++j) {
+      const int i = threadIdx.x + j * blockDim.x;
+      if (i < nv) hv[j] = reinterpret_cast<const float4*>(h + (size_t)t * d)[i];
     }
+  }
+  const float4* p4 = reinterpret_cast<const float4*>(part + (size_t)t * d);
+  float4 v[kVec];
+#pragma unroll
+  for (int j = 0; j < kVec; ++j) {   // one chunk's split loads in flight (register budget:
+    const int i = threadIdx.x + j * blockDim.x;   // two 512-thread CTAs per SM)
+    float4 ld[kMaxSplits];
+#pragma unroll
+    for (int sp = 0; sp < kMaxSplits; ++sp)
+      if (sp < splits && i < nv) ld[sp] = __ldg(p4 + sp * sstride + i);
+    float4 acc = hv[j];
+#pragma unroll
+    for (int sp = 0; sp < kMaxSplits; ++sp)
+      if (sp < splits) {
+        acc.x += ld[sp].x; acc.y += ld[sp].y; acc.z += ld[sp].z; acc.w += ld[sp].w;
+      }
+    v[j] = acc;
   }
   float ss = 0.f;
   float4* ho = reinterpret_cast<float4*>(h + (size_t)t * d);
@@ -137,13 +157,12 @@ __global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restr
   }
   __syncthreads();
   const float r = rsqrtf(sh[32] / (float)d + eps);
-  const float4* w4 = reinterpret_cast<const float4*>(w);
   __nv_bfloat162* xo = reinterpret_cast<__nv_bfloat162*>(x + (size_t)t * d);
 #pragma unroll
   for (int j = 0; j < kVec; ++j) {
     const int i = threadIdx.x + j * blockDim.x;
     if (i < nv) {
-      const float4 ww = w4[i];
+      const float4 ww = wv[j];
       xo[2 * i] = __floats2bfloat162_rn(v[j].x * r * ww.x, v[j].y * r * ww.y);
       xo[2 * i + 1] = __floats2bfloat162_rn(v[j].z * r * ww.z, v[j].w * r * ww.w);
     }
@@ -236,18 +255,35 @@ __global__ void __launch_bounds__(128) k_qkv_rope_kv4(const float* __restrict__ 
                                                       __nv_bfloat16* __restrict__ kc,
                                                       __nv_bfloat16* __restrict__ vc, int n_q,
                                                       int n_kv, int hd, int ctx_cap) {
-  pdl_wait();
-  pdl_trigger();
+  // token count, positions, slots and the cos/sin table come from launches at
+  // least two back (see k_residual_rmsnorm_v): fetch the first item's before
+  // the wait, so only the split-K partial loads follow it
   const int T = *t_dev;
   const int half = hd / 2;
   const int n_quads = (n_q + 2 * n_kv) * half / 4;
   const int per_tok = (n_quads + 127) / 128;
   const int N = (n_q + 2 * n_kv) * hd;
   const size_t sstride = (size_t)rows_cap * N;
+  int pos_pre = 0, slot_pre = 0;
+  float4 c01_pre = make_float4(0.f, 0.f, 0.f, 0.f), c23_pre = c01_pre;
+  if ((int)blockIdx.x < T * per_tok) {
+    const int t = blockIdx.x / per_tok;
+    const int c = ((blockIdx.x % per_tok) * 128 + threadIdx.x) * 4;
+    pos_pre = tok_pos[t];
+    slot_pre = tok_slot[t];
+    if (c < n_quads * 4 && c / half < n_q + n_kv) {
+      const float4* cs4 = reinterpret_cast<const float4*>(rope + (size_t)pos_pre * half + c % half);
+      c01_pre = cs4[0];
+      c23_pre = cs4[1];
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
   for (int wi = blockIdx.x; wi < T * per_tok; wi += gridDim.x) {   // (token, quad block)
     const int t = wi / per_tok;
     const int c = ((wi % per_tok) * 128 + threadIdx.x) * 4;        // first pair index
     if (c >= n_quads * 4) continue;
+    const bool first = wi == (int)blockIdx.x;
     const int head = c / half, i = c % half;
     const float* p0 = part + (size_t)t * N + head * hd + i;
     float4 la[kMaxSplits], lb[kMaxSplits];
@@ -264,10 +300,15 @@ __global__ void __launch_bounds__(128) k_qkv_rope_kv4(const float* __restrict__ 
         a[0] += la[sp].x; a[1] += la[sp].y; a[2] += la[sp].z; a[3] += la[sp].w;
         b[0] += lb[sp].x; b[1] += lb[sp].y; b[2] += lb[sp].z; b[3] += lb[sp].w;
       }
-    const int pos = tok_pos[t];
+    const int pos = first ? pos_pre : tok_pos[t];
+    const int slot = first ? slot_pre : tok_slot[t];
     if (head < n_q + n_kv) {
-      const float4* cs4 = reinterpret_cast<const float4*>(rope + (size_t)pos * half + i);
-      const float4 c01 = cs4[0], c23 = cs4[1];
+      float4 c01 = c01_pre, c23 = c23_pre;
+      if (!first) {
+        const float4* cs4 = reinterpret_cast<const float4*>(rope + (size_t)pos * half + i);
+        c01 = cs4[0];
+        c23 = cs4[1];
+      }
       const float cx[4] = {c01.x, c01.z, c23.x, c23.z}, cy[4] = {c01.y, c01.w, c23.y, c23.w};
       float ra[4], rb[4];
 #pragma unroll
@@ -279,13 +320,13 @@ __global__ void __launch_bounds__(128) k_qkv_rope_kv4(const float* __restrict__ 
       if (head < n_q) {
         dst = q + ((size_t)t * n_q + head) * hd;
       } else {
-        dst = kc + (((size_t)tok_slot[t] * n_kv + (head - n_q)) * ctx_cap + pos) * hd;
+        dst = kc + (((size_t)slot * n_kv + (head - n_q)) * ctx_cap + pos) * hd;
       }
       st_bf16x4(dst + i, ra[0], ra[1], ra[2], ra[3]);
       st_bf16x4(dst + i + half, rb[0], rb[1], rb[2], rb[3]);
     } else {
       __nv_bfloat16* dst =
-          vc + (((size_t)tok_slot[t] * n_kv + (head - n_q - n_kv)) * ctx_cap + pos) * hd;
+          vc + (((size_t)slot * n_kv + (head - n_q - n_kv)) * ctx_cap + pos) * hd;
       st_bf16x4(dst + i, a[0], a[1], a[2], a[3]);
       st_bf16x4(dst + i + half, b[0], b[1], b[2], b[3]);
     }
