@@ -131,3 +131,14 @@ def test_bench_round_roofline_matches_survey_figures():
     bt = 2 * bench.linear_params(t) + 64 * 640 * bench.kv_bytes_per_token(t)
     bd = 2 * bench.linear_params(d) + 64 * 640 * bench.kv_bytes_per_token(d)
     assert abs(bt / 1e9 - 20.38) < 0.01 and abs(bd / 1e9 - 3.81) < 0.01
+
+
+def test_acceptance_criteria_1_2_closed_form():
+    """The reference's `specsim verify` criteria 1-2 (acceptance.py:40-119)
+    against this package's closed-form model."""
+    import json
+    from paper_2605_08151_b200 import acceptance as A
+    golden = json.loads((Path(__file__).parent / "golden" / "acceptance.json").read_text())
+    for r in A.run_all((1, 2)):
+        assert r.passed, r
+        assert (r.name, r.detail) == (golden[str(r.cid)]["name"], golden[str(r.cid)]["detail"])
