@@ -109,6 +109,14 @@ typedef struct SpectreOracleConfig {
   double t_target_slope;
   double ema_decay;
   double fixed_threshold_l;
+  /* draft latency model (draft_engine.py:158-164, 205-216): a round's step
+   * latency is t_draft + t_draft_slope * max(0, queries - t_draft_free_batch),
+   * with t_draft already scaled by the prompt-compression factor and alpha
+   * already the compression-adjusted alpha; t_draft_init is the target's
+   * T_D^mix before the first reply (sim.py:283-288) */
+  double t_draft_slope;
+  double t_draft_init;
+  int32_t t_draft_free_batch;
 } SpectreOracleConfig;
 
 typedef struct SpectreOracleOutputs {

@@ -36,6 +36,9 @@ class OracleConfig(C.Structure):
         ("t_target_slope", C.c_double),
         ("ema_decay", C.c_double),
         ("fixed_threshold_l", C.c_double),
+        ("t_draft_slope", C.c_double),
+        ("t_draft_init", C.c_double),
+        ("t_draft_free_batch", C.c_int32),
     ]
 
 

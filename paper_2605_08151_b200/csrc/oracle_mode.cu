@@ -144,6 +144,7 @@ k_oracle_decode_loop(SpectreOracleConfig cfg, const double* __restrict__ arrival
   const bool spec = cfg.variant != SPECTRE_VARIANT_AR;
 
   __shared__ double s_now, s_ema, s_L, s_rstar;
+  __shared__ double s_tdm;   // target's last reply T_D^mix (sim.py:283-288, 833-834)
   __shared__ int s_has_ema, s_has_L, s_prev_mode, s_mode, s_round, s_admitted, s_limit,
       s_active, s_lo, s_stop, s_finished;
   __shared__ long long s_cursor;
@@ -160,6 +161,7 @@ k_oracle_decode_loop(SpectreOracleConfig cfg, const double* __restrict__ arrival
     s_has_ema = 0;
     s_has_L = 0;
     s_ema = 0.0;
+    s_tdm = cfg.t_draft_init;
     s_L = 0.0;
     s_prev_mode = 0;
     s_cursor = 0;
@@ -223,9 +225,9 @@ k_oracle_decode_loop(SpectreOracleConfig cfg, const double* __restrict__ arrival
           } else {
             const bool hasL = cfg.has_fixed_l ? true : (s_has_L != 0);
             const double L = cfg.has_fixed_l ? cfg.fixed_threshold_l : s_L;
-            // T_D fed to the controller = last reply's t_d_mix = t_draft here
+            // T_D fed to the controller = the last reply's t_d_mix
             mode = choose_mode_hybrid(s_prev_mode, s_has_ema != 0, s_ema, hasL, L, g,
-                                      cfg.t_target, cfg.t_draft, &r_star);
+                                      cfg.t_target, s_tdm, &r_star);
             s_prev_mode = mode;
           }
         }
@@ -412,15 +414,22 @@ k_oracle_decode_loop(SpectreOracleConfig cfg, const double* __restrict__ arrival
       const double nan = __longlong_as_double(0x7ff8000000000000ll);
       double dispatch = now, dstart = nan, ddone = nan;
       int steps = 0;
+      // draft step latency of this round: all-speculative base (compression
+      // factor applied on the host) + contention slope beyond the free batch
+      // (draft_engine.py:158-164, 335-344)
+      const int over = queries > cfg.t_draft_free_batch ? queries - cfg.t_draft_free_batch : 0;
+      const double tdm = __dadd_rn(cfg.t_draft, __dmul_rn(cfg.t_draft_slope, (double)over));
       if (mode == 'O' && queries > 0) {
         steps = g - 1;
         dstart = __dadd_rn(now, cfg.delay);
-        ddone = __dadd_rn(dstart, __dmul_rn((double)steps, cfg.t_draft));
+        ddone = __dadd_rn(dstart, __dmul_rn((double)steps, tdm));
         dispatch = __dadd_rn(ddone, cfg.delay);
+        s_tdm = tdm;
       } else if (mode == 'P') {
         steps = g;
         dstart = __dadd_rn(now, cfg.delay);
-        ddone = __dadd_rn(dstart, __dmul_rn((double)steps, cfg.t_draft));
+        ddone = __dadd_rn(dstart, __dmul_rn((double)steps, tdm));
+        s_tdm = tdm;
       }
       const double t_t =
           __dadd_rn(cfg.t_target, __dmul_rn(cfg.t_target_slope, (double)(participants - 1)));

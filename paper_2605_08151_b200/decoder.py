@@ -168,6 +168,27 @@ class RunResult:
     device_trace: dict = field(default_factory=dict)
 
 
+def draft_latency(cfg: SimConfig):
+    """(alpha_eff, all-speculative step base, slope, free batch, the target's
+    initial T_D^mix): prompt compression scales the draft's alpha and its
+    speculative step latency (draft_engine.py:205-216, 335-338); the target
+    starts from mixed_step_latency(1, unscaled) (sim.py:283-288)."""
+    p = cfg.compression_p
+    if p < 1.0:
+        alpha_eff = cfg.alpha * (1.0 - cfg.compression_beta * (1.0 - p))
+        factor = cfg.compression_latency_frac + (1.0 - cfg.compression_latency_frac) * p
+    else:
+        alpha_eff, factor = cfg.alpha, 1.0
+    slope, free = cfg.t_draft_slope, cfg.t_draft_free_batch
+    return (alpha_eff, cfg.t_draft * factor, slope, free,
+            cfg.t_draft + slope * max(0, 1 - free))
+
+
+def mixed_step_latency(base: float, slope: float, free: int, scheduled: int) -> float:
+    """draft_engine.py:158-164."""
+    return base + slope * max(0, scheduled - free)
+
+
 def _check_domain(cfg: SimConfig, variant: PolicyVariant) -> float:
     kind, args = parse_delay_spec(cfg.delay_dist)
     if kind != "constant":
@@ -177,8 +198,6 @@ def _check_domain(cfg: SimConfig, variant: PolicyVariant) -> float:
         raise OutsideDeviceDomain("message drops / reorders")
     if cfg.background_qps > 0 and cfg.background_requests > 0:
         raise OutsideDeviceDomain("background draft tenants")
-    if cfg.compression_p != 1.0 or cfg.t_draft_slope != 0.0:
-        raise OutsideDeviceDomain("draft prompt compression / contention model")
     if d > cfg.stale_timeout or d >= cfg.heartbeat_period or \
             cfg.heartbeat_period + d > cfg.heartbeat_expiry:
         raise OutsideDeviceDomain("liveness / staleness timeouts would fire")
@@ -188,9 +207,11 @@ def _check_domain(cfg: SimConfig, variant: PolicyVariant) -> float:
             raise OutsideDeviceDomain("gamma < 2 (empty repair replies time out)")
         if cfg.max_concurrency > cfg.draft_capacity:
             raise OutsideDeviceDomain("batch larger than draft capacity")
-        if 2 * d + (g - 1) * cfg.t_draft >= cfg.reply_timeout:
+        t_d_max = max(draft_latency(cfg)[4],
+                      mixed_step_latency(*draft_latency(cfg)[1:4], cfg.max_concurrency))
+        if 2 * d + (g - 1) * t_d_max >= cfg.reply_timeout:
             raise OutsideDeviceDomain("ordinary repairs would time out")
-        if g * cfg.t_draft > cfg.t_target:
+        if g * t_d_max > cfg.t_target:
             raise OutsideDeviceDomain("conservative rounds (gamma*T_D > T_T)")
     return d
 
@@ -265,14 +286,16 @@ def run(config: SimConfig, variant: PolicyVariant | str, workload: Workload | No
     max_rounds = n * max(OL - 1, 1) + 1
     seed64 = cfg.seed & ((1 << 64) - 1)
 
+    dl = draft_latency(cfg)
     c = _native.OracleConfig(
         seed=seed64, n_requests=n, max_concurrency=cfg.max_concurrency, gamma=g,
         output_len=OL, variant=_VARIANT_CODE[variant],
         fairness_period=cfg.fairness_period,
         has_fixed_l=int(cfg.fixed_threshold_l is not None), max_rounds=max_rounds,
-        alpha=cfg.alpha, t_target=cfg.t_target, t_draft=cfg.t_draft, delay=d,
+        alpha=dl[0], t_target=cfg.t_target, t_draft=dl[1], delay=d,
         t_target_slope=cfg.t_target_slope, ema_decay=cfg.ema_decay,
-        fixed_threshold_l=float(cfg.fixed_threshold_l or 0.0))
+        fixed_threshold_l=float(cfg.fixed_threshold_l or 0.0),
+        t_draft_slope=dl[2], t_draft_init=dl[4], t_draft_free_batch=dl[3])
     ws_bytes = L.spectre_oracle_workspace_bytes(c)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     arr = torch.tensor(arrivals, dtype=torch.float64, device=dev)
@@ -369,7 +392,8 @@ def _assemble_result(cfg, variant, workload, d, h, cpos, fin_at, adm_at, committ
             draft_records.append(DraftRoundRecord(
                 started_at=float(h["round_draft_start"][k]),
                 finished_at=float(h["round_draft_done"][k]), n_speculative=q, n_regular=0,
-                regular_pending_at_start=0, forced_regular=False, t_d_mix=cfg.t_draft,
+                regular_pending_at_start=0, forced_regular=False,
+                t_d_mix=mixed_step_latency(*draft_latency(cfg)[1:4], q),
                 steps=steps, counter_after=counter))
             n_queries += q
             draft_tokens += int(h["round_draft_tokens"][k])

@@ -20,6 +20,12 @@ def golden_runs():
 
 
 @pytest.fixture(scope="session")
+def golden_runs_draft_model():
+    """Compression / contention runs (scripts/make_golden_draft_model.py)."""
+    return json.loads((GOLDEN / "runs_draft_model.json").read_text())["cases"]
+
+
+@pytest.fixture(scope="session")
 def golden_streams():
     return json.loads((GOLDEN / "streams.json").read_text())
 

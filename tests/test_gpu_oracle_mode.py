@@ -101,6 +101,14 @@ def test_device_decode_loop_matches_reference(pkg, golden_runs, idx):
     assert digest == case["committed_sha256"]
 
 
+@pytest.mark.parametrize("idx", range(14))
+def test_device_loop_draft_model_matches_reference(pkg, golden_runs_draft_model, idx):
+    """Prompt compression + draft contention model (§8f rows 2-3, fault-free
+    part): the CUDA loop reproduces the reference's reports, traces and every
+    draft round's T_D^mix."""
+    test_device_decode_loop_matches_reference(pkg, golden_runs_draft_model, idx)
+
+
 def test_device_loop_outside_domain_refused(pkg):
     with pytest.raises(pkg.OutsideDeviceDomain):
         pkg.run(pkg.SimConfig(batch_size=4, n_requests=4, output_len=8, drop_prob=0.1), "hybrid")

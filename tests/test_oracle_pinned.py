@@ -71,6 +71,14 @@ def test_lockstep_matches_reference_run(golden_runs, idx):
     assert digest == case["committed_sha256"]
 
 
+@pytest.mark.parametrize("idx", range(14))
+def test_lockstep_matches_reference_draft_model(golden_runs_draft_model, idx):
+    """Draft prompt compression and the contention latency model (§8f rows 2-3,
+    fault-free part): reports, round traces and draft records equal the
+    reference's, including every round's T_D^mix."""
+    test_lockstep_matches_reference_run(golden_runs_draft_model, idx)
+
+
 def test_verify_semantics():
     # /root/reference/pkg/tests/test_oracle.py:119-178
     cand = [L.reference_token(0, 1, i) for i in range(4)]
