@@ -384,6 +384,69 @@ __global__ void __launch_bounds__(256) k_argmax_reduce(const float* __restrict__
   }
 }
 
+// Row-group variant: lanes are 32 consecutive rows (coalesced 128 B loads of
+// one slot), the 32 warps split the slots, then a fixed-order cross-warp
+// reduction.  (max value, lowest index among equals) is order independent,
+// so the result equals k_argmax_reduce's.
+__global__ void __launch_bounds__(1024) k_argmax_reduce_rows(const float* __restrict__ val,
+                                                            const int* __restrict__ idx,
+                                                            int n_tiles, int rows_cap,
+                                                            const int* __restrict__ t_dev,
+                                                            int* __restrict__ out_tok,
+                                                            float* __restrict__ out_val) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float sv[32][33];
+  __shared__ int si[32][33];
+  const int T = *t_dev;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t0 = blockIdx.x * 32; t0 < T; t0 += gridDim.x * 32) {
+    const int t = t0 + lane;
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    if (t < T) {
+      int i = warp;
+#pragma unroll 1
+      for (; i + 224 < n_tiles; i += 256) {   // eight independent slots in flight
+        float v[8];
+        int ix[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          v[u] = val[(size_t)(i + 32 * u) * rows_cap + t];
+          ix[u] = idx[(size_t)(i + 32 * u) * rows_cap + t];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (v[u] > best || (v[u] == best && ix[u] < bi)) {
+            best = v[u];
+            bi = ix[u];
+          }
+      }
+      for (; i < n_tiles; i += 32) {
+        const float v = val[(size_t)i * rows_cap + t];
+        const int ix = idx[(size_t)i * rows_cap + t];
+        if (v > best || (v == best && ix < bi)) {
+          best = v;
+          bi = ix;
+        }
+      }
+    }
+    sv[warp][lane] = best;
+    si[warp][lane] = bi;
+    __syncthreads();
+    if (warp == 0 && t < T) {
+      for (int w = 1; w < 32; ++w)
+        if (sv[w][lane] > best || (sv[w][lane] == best && si[w][lane] < bi)) {
+          best = sv[w][lane];
+          bi = si[w][lane];
+        }
+      out_tok[t] = bi;
+      if (out_val) out_val[t] = best;
+    }
+    __syncthreads();   // sv / si reused by the next row group
+  }
+}
+
 // RoPE table: rope[p][i] = (cos(p * theta^(-2i/hd)), sin(...)), double precision.
 __global__ void k_rope_table(float2* rope, int ctx_cap, int hd, double theta) {
   const int half = hd / 2;
@@ -481,6 +544,16 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
 int launch_argmax_reduce(const float* val, const int* idx, int n_tiles, int rows_cap,
                          const int* t_dev, int t_cap, int* out_tok, float* out_val,
                          cudaStream_t s) {
+  static const bool rows = [] {
+    const char* e = getenv("SPECTRE_ARGMAX_ROWS");   // 0: one CTA per row (strided slots)
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (rows) {
+    SPECTRE_LAUNCH_PDL("k_argmax_reduce_rows", k_argmax_reduce_rows,
+                       dim3(cap_grid(std::min((t_cap + 31) / 32, kSms))), dim3(1024), 0, s, val,
+                       idx, n_tiles, rows_cap, t_dev, out_tok, out_val);
+    return SPECTRE_OK;
+  }
   SPECTRE_LAUNCH_PDL("k_argmax_reduce", k_argmax_reduce, dim3(cap_grid(std::min(t_cap, 2 * kSms))), dim3(256), 0, s, val, idx,
                      n_tiles, rows_cap, t_dev, out_tok, out_val);
   return SPECTRE_OK;
