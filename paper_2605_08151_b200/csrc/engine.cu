@@ -144,6 +144,13 @@ struct ModelRT {
     sp_qkv = pick_splits((nqkv() + tr_qkv - 1) / tr_qkv, d / 64, ctas);
     sp_o = pick_splits((d + tr_o - 1) / tr_o, qd / 64, ctas);
     sp_d = pick_splits((d + tr_d - 1) / tr_d, dm.ffn / 64, ctas);
+    if (half_gemm)
+      if (const char* v = getenv("SPECTRE_DRAFT_SPLIT_CAP")) {   // measured: caps 8/6/4 slower
+        const int cap = std::max(1, atoi(v));
+        sp_qkv = std::min(sp_qkv, cap);
+        sp_o = std::min(sp_o, cap);
+        sp_d = std::min(sp_d, cap);
+      }
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
     attn_chunk = attn_chunk_default();
     split_max = (ctx_cap + attn_chunk - 1) / attn_chunk;
