@@ -353,10 +353,14 @@ def roofline_gate_up(pair, args):
     times = []
     n_layers = pair.target.spec.n_layers
 
+    # the engine's launch shape: CTA pairs (cta_group::2) unless SPECTRE_GU_PAIR=0,
+    # one 256-row tile per CTA (no stream-K)
+    flags = 4000 if os.environ.get("SPECTRE_GU_PAIR", "1") != "0" else 2000
+
     def launch(layer):
         _native.check(L.spectre_gemm_bf16(X.data_ptr(), pair.target.wgu[layer].data_ptr(), None, T,
                                           512, F2, K, 1, 2, None, None, None, act.data_ptr(),
-                                          F2 // 2, 2000, int(s.cuda_stream)), "gemm")
+                                          F2 // 2, flags, int(s.cuda_stream)), "gemm")
 
     # back-to-back launches over every layer's weights (> L2, PDL-chained as in
     # the verify pass), CUDA events on the launching stream; repeated 4 times

@@ -216,6 +216,13 @@ struct ModelRT {
                       1, 0, 0, gu128 ? 128 : 256));
       TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
                     0, 0, tr_d));
+      static const bool gu_pair = [] {   // CTA pairs (cta_group::2) for the 256-row SwiGLU
+        const char* v = getenv("SPECTRE_GU_PAIR");   // tiles: half the token tile per CTA,
+        return v ? atoi(v) != 0 : true;              // measured 68.7 -> 66.4 us (bit-identical)
+      }();
+      if (gu_pair && !gu128 && !half_gemm && !(gu_sk && !gu128) &&
+          (2 * F / 256) % 2 == 0 && 2 * F / 256 <= gemm_sk_grid())
+        TRY(gemm_set_pair(&pgu[l]));
       if (half_gemm) {
         // partial GEMMs only: the SwiGLU GEMM measured faster in the full config
         for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) TRY(gemm_set_half(p));

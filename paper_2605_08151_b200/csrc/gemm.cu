@@ -104,10 +104,10 @@ int gemm_set_outputs(GemmPlan* p, float* part, float* amax_val, int* amax_idx, v
   return SPECTRE_OK;
 }
 
-template <int kEpi, int BK, int kHalf>
+template <int kEpi, int BK, int kHalf, int kPair = 0>
 static int launch_one(const GemmPlan& p, cudaStream_t s) {
   using Cfg = GemmCfg<kHalf>;
-  auto kern = gemm_bf16_swapab<kEpi, BK, kHalf>;
+  auto kern = gemm_bf16_swapab<kEpi, BK, kHalf, kPair>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     SPECTRE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -116,8 +116,49 @@ static int launch_one(const GemmPlan& p, cudaStream_t s) {
   }
   if (p.args.stream_k && cap_grid(p.grid) != p.grid)
     return arg_fail("gemm: stream-K plans need the whole grid");
+  if (kPair) {
+    if (kHalf || cap_grid(p.grid) != p.grid) return arg_fail("gemm: pair plans need the whole grid");
+    if (getenv("SPECTRE_GEMM_PAIR_DBG")) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(p.grid);
+      cfg.blockDim = dim3(Cfg::kThreads);
+      cfg.dynamicSmemBytes = Cfg::kSmem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = -1;
+      cudaError_t q = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+      printf("pair: max active clusters %d (%s), grid %d\n", n, cudaGetErrorString(q), p.grid);
+    }
+    cudaError_t e = launch_pdl_cluster(kern, dim3(p.grid), dim3(Cfg::kThreads), Cfg::kSmem, s, 2,
+                                       p.tmap_w, p.tmap_x, p.tmap_out, p.tmap_sk, p.args);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm_bf16_swapab (pair)");
+    if (getenv("SPECTRE_GEMM_PAIR_DBG")) {
+      e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return cuda_fail(e, "gemm_bf16_swapab (pair, sync)");
+    }
+    return SPECTRE_OK;
+  }
   SPECTRE_LAUNCH_PDL("gemm_bf16_swapab", kern, dim3(cap_grid(p.grid)), dim3(Cfg::kThreads),
                      Cfg::kSmem, s, p.tmap_w, p.tmap_x, p.tmap_out, p.tmap_sk, p.args);
+  return SPECTRE_OK;
+}
+
+static int num_sms();
+
+// CTA-pair launch for a wide single-job GEMM: every CTA owns exactly one
+// 256-row tile (full K), the grid is an even number of CTAs in clusters of 2.
+int gemm_set_pair(GemmPlan* p) {
+  if (p->half || p->bk != 64 || p->epi != kSwiGLU || p->args.tile_rows != 256 || p->args.splits != 1 ||
+      p->args.stream_k || p->args.post.kind != kPostNone || p->n_tiles % 2 ||
+      p->n_tiles > num_sms())
+    return arg_fail("gemm_set_pair: one 256-row tile per CTA, BK 64, no split / stream-K");
+  p->grid = p->n_tiles;
+  p->args.pair = 1;
   return SPECTRE_OK;
 }
 
@@ -216,6 +257,10 @@ int gemm_run(const GemmPlan& p0, cudaStream_t s) {
     pp = &stripped;
   }
   const GemmPlan& p = *pp;
+  if (p.args.pair) {
+    if (p.epi != kSwiGLU || p.bk != 64) return arg_fail("gemm: CTA pairs: SwiGLU, BK 64");
+    return launch_one<kSwiGLU, 64, 0, 1>(p, s);
+  }
   if (p.half) {
     if (p.bk != 64 || p.epi == kArgmax) return arg_fail("gemm: half config needs BK 64, no argmax");
     if (p.epi == kPartial) return launch_one<kPartial, 64, 1>(p, s);
@@ -274,10 +319,16 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
                                  float* amax_val, int32_t* amax_idx, void* act, int32_t ld_act,
                                  int32_t max_stages, void* stream) {
   GemmPlan p;
-  // test knobs: max_stages < 0 forces 32-wide K blocks; >= 2000 disables stream-K;
-  // >= 1000 selects 128-row tiles
+  // test knobs: max_stages < 0 forces 32-wide K blocks; >= 4000 CTA pairs; >= 3000 the
+  // half-SM config; >= 2000 disables stream-K; >= 1000 selects 128-row tiles
   bool sk = true;
   bool half = false;
+  bool pair = false;
+  if (max_stages >= 4000) {   // CTA-pair launch (256-row tiles, no stream-K)
+    pair = true;
+    sk = false;
+    max_stages -= 4000;
+  }
   if (max_stages >= 3000) {
     half = true;
     sk = false;
@@ -301,6 +352,8 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
   p.args.t_static = t_static;
   if (half)
     if (int e = gemm_set_half(&p)) return e;
+  if (pair)
+    if (int e = gemm_set_pair(&p)) return e;
   if (int e = gemm_set_outputs(&p, partial, amax_val, amax_idx, act, ld_act)) return e;
   if (const char* dg = getenv("SPECTRE_GEMM_DIAG")) p.args.diag = atoi(dg);
   static unsigned long long* stall = nullptr;

@@ -38,5 +38,6 @@ int gemm_set_outputs(GemmPlan* p, float* part, float* amax_val, int* amax_idx, v
 int gemm_run(const GemmPlan& p, cudaStream_t s);
 // Switch a 128-row-tile partial / SwiGLU plan to the half-SM configuration.
 int gemm_set_half(GemmPlan* p);
+int gemm_set_pair(GemmPlan* p);   // CTA pairs (cta_group::2) for wide single-tile plans
 
 }  // namespace spectre

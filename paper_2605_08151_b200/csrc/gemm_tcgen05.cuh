@@ -98,6 +98,8 @@ struct GemmArgs {
   int l2_ahead;             // producer L2-prefetches weight boxes this many k-steps ahead
   int ksub;                 // 1: one BK block per stage; 0: two when >= 2 such stages fit
   int ksub_max;             // most BK blocks per stage (0: 4)
+  int pair;                 // launched as CTA pairs (cluster 2): M=256 cta_group::2 MMAs
+                            // whenever the tile is wide (T <= 256, 256-row tiles)
   unsigned long long* stall;   // diagnostics: per CTA {producer empty-wait, MMA full-wait,
                                // MMA issue, stages} in cycles (null = off)
 };
@@ -108,7 +110,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+// x * sigmoid(x) with the fast reciprocal: the IEEE division expanded to a long
+// sequence with a slow path and was ~40 % of the SwiGLU epilogue at T=256
+__device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
 // One accumulation job of a CTA: a k-range of one tile and one token pass.
 struct GemmJob {
@@ -195,7 +199,10 @@ struct GemmSched {
   }
 };
 
-template <int kEpi, int BK, int kHalf>
+// kPair: the CTA-pair instantiation (contains cta_group::2 instructions, so it
+// must be launched in clusters of 2; it falls back to per-CTA MMAs when the
+// tile is not wide).
+template <int kEpi, int BK, int kHalf, int kPair = 0>
 __global__ void __launch_bounds__(GemmCfg<kHalf>::kThreads, GemmCfg<kHalf>::kMinBlocks)
 gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
                  const __grid_constant__ CUtensorMap tmap_x,
@@ -221,7 +228,14 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   constexpr int kXBox = 64 * kRow;          // one 64-row activation box
   const bool wide = (T <= 256 && a.tile_rows == 256);
   const int w_bytes = wide ? 2 * kWBox : kWBox;
-  const int x_rows = wide ? ((T + 63) & ~63) : min((T + 63) & ~63, Cfg::kPass);
+  // CTA pair: each CTA holds its own 256 weight rows and HALF of the token
+  // tile; one M=256 MMA per box spans both CTAs (the leader issues it)
+  const bool pair = kPair && wide && !kHalf;
+  const uint32_t crank = kPair ? cluster_rank() : 0u;
+  const bool leader = crank == 0;
+  const int x_half = ((T + 15) & ~15) / 2;         // tokens held by each CTA of a pair
+  const int x_rows = pair ? ((x_half + 63) & ~63)
+                          : (wide ? ((T + 63) & ~63) : min((T + 63) & ~63, Cfg::kPass));
   // a stage holds `ksub` consecutive BK-wide k blocks (one expect-tx, one
   // MMA commit): fewer commit groups per byte when the MMAs are small (T=64)
   const int sub_bytes = w_bytes + x_rows * kRow;
@@ -268,9 +282,13 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if (kPair && pair) tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+    else tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync();   // peer barriers initialised before any TMA signals them
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -309,17 +327,35 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       // Weights never change: the first stages' weight tiles are requested
       // before waiting on the previous kernel (its tail overlaps our fill).
       int pre = 0;
+      // pair: both CTAs' loads complete on the leader's barrier, which
+      // expects both CTAs' bytes; the peer never arrives on it
+      auto load_w = [&](void* dst, int s2, int c0, int c1) {
+        if (kPair && pair) tma_load_2d_pair(dst, &tmap_w, mapa_shared(&full[s2], 0), c0, c1, pol_w);
+        else tma_load_2d(dst, &tmap_w, &full[s2], c0, c1, pol_w);
+      };
+      auto load_x = [&](void* dst, int s2, int c0, int c1) {
+        if (kPair && pair) tma_load_2d_pair(dst, &tmap_x, mapa_shared(&full[s2], 0), c0, c1, pol_x);
+        else tma_load_2d(dst, &tmap_x, &full[s2], c0, c1, pol_x);
+      };
+      auto expect = [&](int s2, uint32_t bytes) {
+        if (!pair) mbar_arrive_expect_tx(&full[s2], bytes);
+        else if (leader) mbar_arrive_expect_tx(&full[s2], 2 * bytes);
+      };
+      auto x_boxes_of = [&](const GemmJob& jj) {
+        return pair ? (x_half + 63) >> 6 : (jj.nt + 63) >> 6;
+      };
+      const int x_t0 = pair ? (int)crank * x_half : 0;
       if (have) {
-        const int x_boxes = (j.nt + 63) >> 6;
+        const int x_boxes = x_boxes_of(j);
         const uint32_t tx = (uint32_t)j.boxes * kWBox + (uint32_t)x_boxes * kXBox;
         pre = min((j.k1 - j.k0 + ksub - 1) / ksub, stages);
         for (int i = 0; i < pre; ++i) {
           const int kb = j.k0 + i * ksub, nk = min(ksub, j.k1 - kb);
-          mbar_arrive_expect_tx(&full[i], tx * (uint32_t)nk);
+          expect(i, tx * (uint32_t)nk);
           for (int q = 0; q < nk; ++q)
             for (int b = 0; b < j.boxes; ++b)
-              tma_load_2d(pipe + i * stage_bytes + q * sub_bytes + b * kWBox, &tmap_w, &full[i],
-                          (kb + q) * BK, j.tile * a.tile_rows + j.row_off + b * 128, pol_w);
+              load_w(pipe + i * stage_bytes + q * sub_bytes + b * kWBox, i, (kb + q) * BK,
+                     j.tile * a.tile_rows + j.row_off + b * 128);
         }
       }
       pdl_wait();
@@ -327,7 +363,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       int g = 0;
       long long st_empty = 0;
       for (; have; have = sched.next(j)) {
-        const int x_boxes = (j.nt + 63) >> 6;
+        const int x_boxes = x_boxes_of(j);
         const uint32_t tx = (uint32_t)j.boxes * kWBox + (uint32_t)x_boxes * kXBox;
         const int n0 = j.tile * a.tile_rows + j.row_off;
         for (int k = j.k0; k < j.k1; k += ksub, ++g) {
@@ -345,16 +381,15 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
               mbar_wait(&empty[s], ((uint32_t)(g / stages) & 1u) ^ 1u);
               if (a.stall) st_empty += clock64() - t_w;
             }
-            mbar_arrive_expect_tx(&full[s], tx * (uint32_t)nk);
+            expect(s, tx * (uint32_t)nk);
             for (int q = 0; q < nk; ++q)
               for (int b = 0; b < j.boxes; ++b)
-                tma_load_2d(st + q * sub_bytes + b * kWBox, &tmap_w, &full[s], (k + q) * BK,
-                            n0 + b * 128, pol_w);
+                load_w(st + q * sub_bytes + b * kWBox, s, (k + q) * BK, n0 + b * 128);
           }
           for (int q = 0; q < nk; ++q)
             for (int b = 0; b < x_boxes; ++b)
-              tma_load_2d(st + q * sub_bytes + w_bytes + b * kXBox, &tmap_x, &full[s],
-                          (k + q) * BK, j.t0 + b * 64, pol_x);
+              load_x(st + q * sub_bytes + w_bytes + b * kXBox, s, (k + q) * BK,
+                     j.t0 + x_t0 + b * 64);
         }
       }
       if (a.stall) a.stall[blockIdx.x * 4 + 0] = (unsigned long long)st_empty;
@@ -364,6 +399,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     }
     __syncwarp();   // reconverge the producer lane before the CTA-wide barrier
   } else if (warp == 1) {
+    if (!pair || leader) {   // pair: the leader issues for both CTAs
     // ---------------- MMA issuer (one thread)
     int g = 0, jn = 0;
     long long st_full = 0, st_issue = 0;
@@ -372,7 +408,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       const int t_pad = (j.nt + 15) & ~15;
       const int nc0 = t_pad < 256 ? t_pad : 256;
       const int nc1 = t_pad - nc0;
-      const uint32_t id0 = idesc_bf16_f32(128, (uint32_t)nc0);
+      const uint32_t id0 = idesc_bf16_f32(pair ? 256 : 128, (uint32_t)nc0);
       const uint32_t id1 = idesc_bf16_f32(128, (uint32_t)(nc1 > 0 ? nc1 : 16));
       const int buf = jn % nbuf;
       const uint32_t acc = tmem_base + (uint32_t)(buf * kBufCols);
@@ -396,7 +432,11 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint32_t accf = (k > j.k0 || q > 0 || kk > 0) ? 1u : 0u;
             const uint64_t bd = umma_desc_kmajor<kRow>(xa + kk * 32);
-            if (j.boxes == 2) {
+            if (kPair && pair) {   // rows: this box in both CTAs; tokens: both CTAs' halves
+              mma_bf16_ss_pair(acc, umma_desc_kmajor<kRow>(sa + kk * 32), bd, id0, accf);
+              mma_bf16_ss_pair(acc + (uint32_t)half_stride,
+                               umma_desc_kmajor<kRow>(sa + kWBox + kk * 32), bd, id0, accf);
+            } else if (j.boxes == 2) {
               mma_bf16_ss(acc, umma_desc_kmajor<kRow>(sa + kk * 32), bd, id0, accf);
               mma_bf16_ss(acc + (uint32_t)half_stride,
                           umma_desc_kmajor<kRow>(sa + kWBox + kk * 32), bd, id0, accf);
@@ -409,14 +449,19 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
             }
           }
           }
-          mma_commit(&empty[s]);
+          if (kPair && pair) mma_commit_pair(&empty[s]);
+          else mma_commit(&empty[s]);
         } else if (lane == 0) {
-          mma_commit(&empty[s]);
+          if (kPair && pair) mma_commit_pair(&empty[s]);
+          else mma_commit(&empty[s]);
         }
         __syncwarp();
         if (a.stall) st_issue += clock64() - t_i;
       }
-      if (lane == 0) mma_commit(&tmem_full[buf]);
+      if (lane == 0) {
+        if (kPair && pair) mma_commit_pair(&tmem_full[buf]);
+        else mma_commit(&tmem_full[buf]);
+      }
       __syncwarp();
       ++jn;
     }
@@ -424,6 +469,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       a.stall[blockIdx.x * 4 + 1] = (unsigned long long)st_full;
       a.stall[blockIdx.x * 4 + 2] = (unsigned long long)st_issue;
       a.stall[blockIdx.x * 4 + 3] = (unsigned long long)g;
+    }
     }
   } else {
     // ---------------- epilogue warps 2..9: lane quarter q = warp % 4, group = (warp-2)/4
@@ -490,9 +536,20 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
         }
         asm volatile("bar.sync 3, %0;" ::"r"(kEpiThreads) : "memory");
       }
+      // TMEM loads are software-pipelined: chunk cc+step is in flight while
+      // chunk cc is processed (columns past t_pad: unused)
+      uint32_t rcur[32], rnext[32];
+      if (chunk0 < t_pad && !(a.diag & 2)) {
+        tmem_ld32_issue(tq + (uint32_t)(col_base + chunk0), rcur);
+        tmem_ld_wait(rcur);
+      }
       for (int cc = chunk0; cc < t_pad && !(a.diag & 2); cc += chunk_step) {
+        const bool more = cc + chunk_step < t_pad;
+        if (more) tmem_ld32_issue(tq + (uint32_t)(col_base + cc + chunk_step), rnext);
         float v[32];
-        tmem_ld32(tq + (uint32_t)(col_base + cc), v);   // columns past t_pad: unused
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) v[jj] = __uint_as_float(rcur[jj]);
+        do {   // chunk body (a `continue` leaves the body, not the chunk loop)
         if (j.k1 <= j.k0) {   // empty k-range (K < splits): this split contributes zeros
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) v[jj] = 0.f;
@@ -606,7 +663,11 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
             const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
             const float g = odd ? recv : v[jj];
             const float u = odd ? v[jj + 16] : recv;
-            out[jj] = silu_f(g) * u;
+            out[jj] = (a.diag & 16) ? g * u : silu_f(g) * u;   // diag 16: no SiLU
+          }
+          if (a.diag & 8) {   // diagnostics: no staging / store
+            if (out[0] == 12345.f) a.part[0] = out[1];
+            continue;
           }
           // stage [32 tokens][64 features] bf16, store the box at (f0, c0)
           stage_begin();
@@ -620,6 +681,12 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
             tma_store_2d(&tmap_out, stg, (j.tile * a.tile_rows + j.row_off + box * 128) >> 1, c0);
             bulk_commit();
           }
+        }
+              } while (0);
+        if (more) {
+          tmem_ld_wait(rnext);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) rcur[jj] = rnext[jj];
         }
       }
       if (a.dbg && etid == 0 && jn < 5) a.dbg[blockIdx.x * 8 + 1 + jn] = gtimer() | ((unsigned long long)j.role << 62);
@@ -671,9 +738,11 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     if (a.post.kind == kPostRope) post_rope(a.post, a.part, a.splits, a.rows_cap, T);
     else post_resid(a.post, a.part, a.splits, a.rows_cap, T, a.N, post_sh);
   }
+  if (kPair) cluster_sync();   // the leader's MMAs and both epilogues are done with both TMEMs
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    if (kPair && pair) tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
+    else tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   }
 }
 
