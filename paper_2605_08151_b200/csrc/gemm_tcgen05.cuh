@@ -113,6 +113,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // x * sigmoid(x) with the fast reciprocal: the IEEE division expanded to a long
 // sequence with a slow path and was ~40 % of the SwiGLU epilogue at T=256
 __device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
+// one MUFU op: sigmoid(x) = 0.5 tanh(x/2) + 0.5 (tanh.approx: ~2^-11 relative,
+// below the bf16 output's precision)
+__device__ __forceinline__ float silu_tanh(float x) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+  return x * fmaf(0.5f, t, 0.5f);
+}
 
 // One accumulation job of a CTA: a k-range of one tile and one token pass.
 struct GemmJob {
@@ -663,7 +670,8 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
             const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
             const float g = odd ? recv : v[jj];
             const float u = odd ? v[jj + 16] : recv;
-            out[jj] = (a.diag & 16) ? g * u : silu_f(g) * u;   // diag 16: no SiLU
+            out[jj] = (a.diag & 16) ? g * u
+                      : ((a.diag & 32) ? silu_f(g) : silu_tanh(g)) * u;   // diag 16: no SiLU
           }
           if (a.diag & 8) {   // diagnostics: no staging / store
             if (out[0] == 12345.f) a.part[0] = out[1];
