@@ -87,7 +87,7 @@ int gemm_set_outputs(GemmPlan* p, float* part, float* amax_val, int* amax_idx, v
     if ((p->args.N * 4) % 16) return arg_fail("gemm: partial rows must be 16-byte aligned");
     if (int e = make_tmap_store(&p->tmap_out, part, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                                 (uint64_t)p->args.N,
-                                (uint64_t)p->args.splits * p->args.rows_cap, 128, 16))
+                                (uint64_t)p->args.splits * p->args.rows_cap, 32, 16))
       return e;
   }
   if (p->epi == kSwiGLU && act) {
