@@ -799,6 +799,7 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
       }
       continue;
     }
+    if (a.debug & 2) continue;   // diagnostics: no partial write / merge
     // multi-split (contexts past a.chunk): partial + last-arriver merge in split order
     const size_t pbase = (((size_t)b * a.n_kv + kvh) * a.rb_max + rblk) * a.split_max;
 #pragma unroll
@@ -814,7 +815,7 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
         a.part_ml[pi * 2 + 1] = lrow[hr];
       }
     }
-    __threadfence();
+    if (!(a.debug & 8)) __threadfence();   // debug 8: no fence (diagnostics only)
     __syncwarp();
     int last = 0;
     if (lane == 0) {
@@ -824,8 +825,12 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
       if (last) *cnt = 0;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) continue;
+    if (!last || (a.debug & 4)) continue;   // debug 4: no merge (diagnostics only)
     __threadfence();
+    // fixed trip count (16 * HD / 4 / 32): unrolled so every iteration's
+    // partial loads are in flight together instead of one L2 round trip chain
+    // per iteration (the merge was most of a split item's time)
+#pragma unroll
     for (int c = lane; c < 16 * HD / 4; c += 32) {
       const int rr = (c * 4) / HD, dcol = (c * 4) % HD;
       const int R = row_lo + rr;
