@@ -462,21 +462,34 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
     s.delta[b] = delta;
     s.rolled[b] = rolled;
   }
+  // per-request outcomes staged in shared memory by every thread, so the
+  // in-order (bit-exact) estimator loop below reads smem, not global memory
+  __shared__ int s_kind[kProtoThreads], s_delta[kProtoThreads];
+  __shared__ unsigned char s_roll[kProtoThreads], s_done[kProtoThreads];
+  __syncthreads();
+  if (threadIdx.x < s.n_req) {
+    const int r = threadIdx.x;
+    s_kind[r] = s.vkind[r];
+    s_delta[r] = s.delta[r];
+    s_roll[r] = (unsigned char)s.rolled[r];
+    s_done[r] = (unsigned char)s.done[r];
+    s.vkind[r] = 0;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     const long long t_now = globaltimer();
     int P = 0, dsum = 0, nroll = 0, csum = 0, cn = 0, npad = 0;
     for (int r = 0; r < s.n_req; ++r) {
-      const int k = s.vkind[r];
+      const int k = s_kind[r];
       if (k == 0) continue;
       ++P;
-      dsum += s.delta[r];
-      nroll += s.rolled[r];
+      dsum += s_delta[r];
+      nroll += s_roll[r];
       if (k == kPadded) ++npad;
       if (k == kCached || k == kRepaired) {
-        csum += s.delta[r];
+        csum += s_delta[r];
         ++cn;
-        const double dv = (double)s.delta[r];
+        const double dv = (double)s_delta[r];
         if (!c.has_L) {
           c.L = dv;
           c.has_L = 1;
@@ -484,8 +497,7 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
           c.L = ema_step(s.ema_decay, c.L, dv);
         }
       }
-      if (s.done[r]) --c.n_active;
-      s.vkind[r] = 0;
+      if (s_done[r]) --c.n_active;
     }
     const int num = s.r_kind == 1 ? npad : nroll;
     const double r_hat = __ddiv_rn((double)num, (double)(P > 0 ? P : 1));
