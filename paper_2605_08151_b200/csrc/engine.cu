@@ -68,10 +68,17 @@ static int tile_rows_default(int fallback) {
   return atoi(v) == 128 ? 128 : 256;
 }
 
-static int attn_chunk_default() {
-  const char* v = getenv("SPECTRE_ATTN_CHUNK");
-  const int c = v ? atoi(v) : 1024;
-  return (c >= 64 && c % 64 == 0 && c <= 8192) ? c : 1024;
+// Keys per attention item.  Key splits only pay when (request, kv head)
+// items are too few to fill the SMs: with n_req * n_kv >= SMs one item per
+// (request, head) already keeps every SM busy, and a split adds a partial
+// round trip + merge (measured at ctx 1093, C2: target 110 vs ~61 us).
+static int attn_chunk_default(int n_items, int ctx_cap) {
+  if (const char* v = getenv("SPECTRE_ATTN_CHUNK")) {
+    const int c = atoi(v);
+    return (c >= 64 && c % 64 == 0 && c <= 8192) ? c : 1024;
+  }
+  if (n_items >= 148) return std::max(1024, (ctx_cap + 63) / 64 * 64);
+  return 1024;
 }
 
 static int jobs_per_cta() {
@@ -152,7 +159,7 @@ struct ModelRT {
         sp_d = std::min(sp_d, cap);
       }
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
-    attn_chunk = attn_chunk_default();
+    attn_chunk = attn_chunk_default(n_req * dm.n_kv_heads, ctx_cap);
     split_max = (ctx_cap + attn_chunk - 1) / attn_chunk;
     // m-tiles per request, in whole attention row blocks (2 m-tiles at hd 128, 3 at hd 64)
     rb_cap = round_up((max_new * group() + 15) / 16, dm.head_dim == 128 ? 2 : 3);
