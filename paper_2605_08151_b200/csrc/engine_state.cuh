@@ -38,6 +38,12 @@ struct CtrlDev {
   int has_tT, has_tD, has_tpar, has_tord;
   double tT, tD, tpar, tord;   // measured EMAs (seconds)
   double r_star;
+  // `round` controller: the paper's r measured directly — PADDED fraction of
+  // steady parallel rounds (a parallel round after a parallel round)
+  int has_rpar, last_mode;
+  double rpar;
+  int has_rho;       // T_par / T_ord measured at the same context (steady P round vs
+  double rho;        // the ordinary EMA at that time): round times grow with context
   // circuit breaker (target_engine.py:337-380); round ids are 1-based as in sim.py:519
   int streak, disabled_until, activations;
   int n_stale;       // this round: queried requests without a matching reply

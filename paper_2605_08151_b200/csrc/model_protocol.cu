@@ -91,6 +91,11 @@ __global__ void k_admit(DecodeStateDev s, BatchDev bt) {
     c.error_req = -1;
     c.has_tT = c.has_tD = c.has_tpar = c.has_tord = 0;
     c.tT = c.tD = c.tpar = c.tord = 0.0;
+    c.has_rpar = 0;
+    c.rpar = 0.0;
+    c.has_rho = 0;
+    c.rho = 0.0;
+    c.last_mode = 0;
     c.r_star = 0.0;
     c.streak = c.disabled_until = c.activations = 0;
     c.n_stale = 0;
@@ -176,12 +181,17 @@ __device__ int round_choose_mode(DecodeStateDev& s, CtrlDev& c) {
           mode = 'P';
           r_star = 0.0;
         } else {
-          const double r_hat = c.has_ema ? c.ema : 0.0;
+          // r: the PADDED fraction parallel rounds actually produced (the
+          // paper's r) once measured; before that the reference's r-hat.  At
+          // T=1 r-hat from ordinary rounds (~0.75) under-predicts it (~1.0)
+          const double r_hat = c.has_rpar ? c.rpar : (c.has_ema ? c.ema : 0.0);
           if (!hasL || L <= 1.0 + 1e-9) {
             r_star = __longlong_as_double(0x7ff0000000000000ll);
           } else {
-            r_star = __ddiv_rn(__dmul_rn(L, __dsub_rn(1.0, __ddiv_rn(c.tpar, c.tord))),
-                               __dsub_rn(L, 1.0));
+            // T_par / T_ord from rounds at the same context; a T_par measured
+            // early against a T_ord that keeps growing would inflate r*
+            const double ratio = c.has_rho ? c.rho : __ddiv_rn(c.tpar, c.tord);
+            r_star = __ddiv_rn(__dmul_rn(L, __dsub_rn(1.0, ratio)), __dsub_rn(L, 1.0));
           }
           if (c.prev_mode == 'P')
             mode = (r_hat > __dmul_rn(r_star, kExitParallelMargin)) ? 'O' : 'P';
@@ -517,14 +527,22 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
       const double td = (double)(c.t_draft_end - c.t_draft_begin) * 1e-9 / c.draft_steps;
       if (!c.has_tD) { c.tD = td; c.has_tD = 1; } else { c.tD = ema_step(d, c.tD, td); }
     }
-    // per-committed-token cost of each mode, normalised to the round shape
-    // an all-PADDED parallel round is the one-off switch-over from ordinary
-    // (sim.py:455-458): its short verify is not the steady parallel round time
-    if (mode == 'P' && npad < P) {
+    // per-committed-token cost of each mode, normalised to the round shape.
+    // The first parallel round after another mode is the switch-over (no
+    // prepared segments: all PADDED, sim.py:455-458) — neither its time nor
+    // its PADDED fraction is the steady parallel round's
+    if (mode == 'P' && c.last_mode == 'P') {
       if (!c.has_tpar) { c.tpar = tr; c.has_tpar = 1; } else { c.tpar = ema_step(d, c.tpar, tr); }
+      const double rp = __ddiv_rn((double)npad, (double)(P > 0 ? P : 1));
+      if (!c.has_rpar) { c.rpar = rp; c.has_rpar = 1; } else { c.rpar = ema_step(d, c.rpar, rp); }
+      if (c.has_tord) {
+        const double rv = __ddiv_rn(tr, c.tord);
+        if (!c.has_rho) { c.rho = rv; c.has_rho = 1; } else { c.rho = ema_step(d, c.rho, rv); }
+      }
     } else if (mode == 'O') {
       if (!c.has_tord) { c.tord = tr; c.has_tord = 1; } else { c.tord = ema_step(d, c.tord, tr); }
     }
+    c.last_mode = mode;
     const int ri = c.round;
     // circuit breaker after a speculative round (sim.py:703-718,
     // target_engine.py:356-380): a missing reply is a timeout here — the
