@@ -212,10 +212,11 @@ def run_ours(args):
         samp = args.temperature > 0
         launches = sum(kernels_per_round(m, g, M.LLAMA_31_8B.n_layers, M.LLAMA_32_1B.n_layers,
                                          samp) for m in modes) + 1   # + set_round_limit
-        cs = max(1, min(8, 512 // B))          # engine prefill chunk (engine.cu:Engine::sizes)
+        cs = max(1, min(16, 512 // B))         # engine prefill chunk (engine.cu:prefill_chunk)
         chunks = (args.prompt_len + cs - 1) // cs
         prefill_launches = 2 * chunks + 1  # batch kernels + admit
         prefill_launches += chunks * (forward_kernels(32, samp) + forward_kernels(16, samp))
+        prefill_launches -= 2 * (2 * chunks - 1)   # lm_head + reduce: target's last chunk only
         results[v] = dict(
             ms_per_step=ms_max / args.steps, value=total_tokens / (ms_max / 1e3),
             rounds=len(modes), timeline=modes, clocks=clocks.summary(),

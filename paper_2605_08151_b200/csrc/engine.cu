@@ -81,6 +81,16 @@ static int attn_chunk_default(int n_items, int ctx_cap) {
   return 1024;
 }
 
+// prompt tokens per request per prefill forward: a row budget of
+// SPECTRE_PREFILL_ROWS (default 512) split over the requests, at most 16
+static int prefill_chunk(int n_req) {
+  static const int rows = [] {
+    const char* v = getenv("SPECTRE_PREFILL_ROWS");
+    return v ? std::max(64, atoi(v)) : 512;
+  }();
+  return std::max(1, std::min(16, rows / std::max(1, n_req)));
+}
+
 static int jobs_per_cta() {
   const char* v = getenv("SPECTRE_JOBS_PER_CTA");
   const int j = v ? atoi(v) : 1;
@@ -308,7 +318,10 @@ struct ModelRT {
   // n_new[b] (sizes the attention row blocks).
   // sample_rows: in sampling mode also draw a token for every row (target
   // verify / prefill); the draft's decode steps sample per request instead.
-  int forward(int new_per_req, cudaStream_t s, void* out_x = nullptr, bool sample_rows = true) {
+  // head = false: stop after the last layer's residual (prefill chunks whose
+  // next-token prediction nobody reads)
+  int forward(int new_per_req, cudaStream_t s, void* out_x = nullptr, bool sample_rows = true,
+              bool head = true) {
     const int d = dm.d_model, L = dm.n_layers, hd = dm.head_dim;
     const float eps = dm.rms_eps;
     const int rows = new_per_req * group();
@@ -356,6 +369,12 @@ struct ModelRT {
       if (!fused)
         TRY(launch_residual_rmsnorm(part, sp_d, rows_cap, bt.t_dev, rows_cap, next, h, x, d, eps,
                                     s));
+    }
+    if (!head) {
+      if (out_x)
+        SPECTRE_CUDA_TRY(cudaMemcpyAsync(out_x, x, (size_t)rows_cap * d * 2,
+                                         cudaMemcpyDeviceToDevice, s));
+      return SPECTRE_OK;
     }
     TRY(gemm_run(plm, s));
     if (sampling) {
@@ -412,7 +431,7 @@ struct Engine {
 
   static void sizes(const SpectreModelDims& t, const SpectreModelDims& d,
                     const SpectreDecodeConfig& c, int* rows_t, int* rows_d, int* cs, int* dnew) {
-    *cs = std::max(1, std::min(8, 512 / std::max(1, c.n_req)));
+    *cs = prefill_chunk(c.n_req);
     *dnew = 2 * c.gamma + 4;
     *rows_t = round_up(std::max(c.n_req * (c.gamma + 1), c.n_req * *cs), 64);
     *rows_d = round_up(std::max(c.n_req * *dnew, c.n_req * *cs), 64);
@@ -792,7 +811,9 @@ extern "C" int spectre_engine_prefill(void* engine, const int32_t* prompts, void
       continue;   // disaggregated: this side holds only one model
     for (int c0 = 0; c0 < P; c0 += cs) {
       TRY(launch_prefill_batch(prompts, P, e->cfg.n_req, c0, cs, m->bt, s));
-      TRY(m->forward(cs, s));
+      // only the target's prediction at the last prompt position is read
+      // (admission commits it as output token 0)
+      TRY(m->forward(cs, s, nullptr, true, m == &e->tgt && c0 + cs >= P));
     }
   }
   TRY(launch_admit(e->st, e->tgt.bt, s));
