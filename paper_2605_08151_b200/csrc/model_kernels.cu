@@ -78,7 +78,9 @@ __global__ void __launch_bounds__(256) k_embed_rmsnorm(const int* __restrict__ t
 // order sum so the loads overlap instead of forming a latency chain.
 constexpr int kMaxSplits = 12;
 
-template <int kVec>
+// kS: most splits the kernel keeps in flight per chunk (register budget: with
+// kS = 4 a 512-thread CTA fits twice per SM, so T=256 rows run in one wave)
+template <int kVec, int kS = kMaxSplits>
 __global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restrict__ part,
                                                              int splits, int rows_cap,
                                                              const int* __restrict__ t_dev,
@@ -121,13 +123,13 @@ __global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restr
 #pragma unroll
   for (int j = 0; j < kVec; ++j) {   // one chunk's split loads in flight (register budget:
     const int i = threadIdx.x + j * blockDim.x;   // two 512-thread CTAs per SM)
-    float4 ld[kMaxSplits];
+    float4 ld[kS];
 #pragma unroll
-    for (int sp = 0; sp < kMaxSplits; ++sp)
+    for (int sp = 0; sp < kS; ++sp)
       if (sp < splits && i < nv) ld[sp] = __ldg(p4 + sp * sstride + i);
     float4 acc = hv[j];
 #pragma unroll
-    for (int sp = 0; sp < kMaxSplits; ++sp)
+    for (int sp = 0; sp < kS; ++sp)
       if (sp < splits) {
         acc.x += ld[sp].x; acc.y += ld[sp].y; acc.z += ld[sp].z; acc.w += ld[sp].w;
       }
@@ -497,6 +499,9 @@ int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const i
   const dim3 grid(cap_grid(std::min(t_cap, resid_ctas_per_sm() * kSms)));
   if (vec <= 1)
     SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<1>, grid, dim3(threads),
+                       0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
+  else if (vec <= 2 && splits <= 4)
+    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<2, 4>, grid, dim3(threads),
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
   else if (vec <= 2)
     SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<2>, grid, dim3(threads),
