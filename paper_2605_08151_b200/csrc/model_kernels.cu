@@ -251,6 +251,10 @@ __device__ __forceinline__ void st_bf16x4(__nv_bfloat16* dst, float a0, float a1
   *reinterpret_cast<uint2*>(dst) = u;
 }
 
+// kB: split partials in flight per batch — 4 (80 registers) when the GEMM had
+// <= 4 splits (target: 6.9 -> 4.8 us), all 12 otherwise (a 12-split draft
+// q/k/v is latency-bound and would pay three round trips)
+template <int kB>
 __global__ void __launch_bounds__(128) k_qkv_rope_kv4(const float* __restrict__ part, int splits,
                                                       int rows_cap, const int* __restrict__ t_dev,
                                                       const int* __restrict__ tok_pos,
@@ -291,20 +295,23 @@ __global__ void __launch_bounds__(128) k_qkv_rope_kv4(const float* __restrict__ 
     const bool first = wi == (int)blockIdx.x;
     const int head = c / half, i = c % half;
     const float* p0 = part + (size_t)t * N + head * hd + i;
-    float4 la[kMaxSplits], lb[kMaxSplits];
-#pragma unroll
-    for (int sp = 0; sp < kMaxSplits; ++sp)
-      if (sp < splits) {
-        la[sp] = __ldg(reinterpret_cast<const float4*>(p0 + sp * sstride));
-        lb[sp] = __ldg(reinterpret_cast<const float4*>(p0 + sp * sstride + half));
-      }
     float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
+    // splits in batches (same summation order), so more CTAs stay resident
+    for (int s0 = 0; s0 < splits; s0 += kB) {
+      float4 la[kB], lb[kB];
 #pragma unroll
-    for (int sp = 0; sp < kMaxSplits; ++sp)
-      if (sp < splits) {
-        a[0] += la[sp].x; a[1] += la[sp].y; a[2] += la[sp].z; a[3] += la[sp].w;
-        b[0] += lb[sp].x; b[1] += lb[sp].y; b[2] += lb[sp].z; b[3] += lb[sp].w;
-      }
+      for (int sp = 0; sp < kB; ++sp)
+        if (s0 + sp < splits) {
+          la[sp] = __ldg(reinterpret_cast<const float4*>(p0 + (s0 + sp) * sstride));
+          lb[sp] = __ldg(reinterpret_cast<const float4*>(p0 + (s0 + sp) * sstride + half));
+        }
+#pragma unroll
+      for (int sp = 0; sp < kB; ++sp)
+        if (s0 + sp < splits) {
+          a[0] += la[sp].x; a[1] += la[sp].y; a[2] += la[sp].z; a[3] += la[sp].w;
+          b[0] += lb[sp].x; b[1] += lb[sp].y; b[2] += lb[sp].z; b[3] += lb[sp].w;
+        }
+    }
     const int pos = first ? pos_pre : tok_pos[t];
     const int slot = first ? slot_pre : tok_slot[t];
     if (head < n_q + n_kv) {
@@ -537,7 +544,16 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
   }();
   if (vec4 && (hd / 2) % 4 == 0) {
     const int quads = pairs / 4;
-    SPECTRE_LAUNCH_PDL("k_qkv_rope_kv4", k_qkv_rope_kv4,
+    if (splits <= 4)
+      SPECTRE_LAUNCH_PDL("k_qkv_rope_kv4", k_qkv_rope_kv4<4>,
+                       dim3(cap_grid(std::min(t_cap * ((quads + 127) / 128),
+                                              (rope_ctas_per_sm() ? rope_ctas_per_sm() : 8) * kSms))),
+                       dim3(128), 0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
+                       reinterpret_cast<const float2*>(rope), reinterpret_cast<__nv_bfloat16*>(q),
+                       reinterpret_cast<__nv_bfloat16*>(kc), reinterpret_cast<__nv_bfloat16*>(vc),
+                       n_q, n_kv, hd, ctx_cap);
+    else
+      SPECTRE_LAUNCH_PDL("k_qkv_rope_kv4", k_qkv_rope_kv4<kMaxSplits>,
                        dim3(cap_grid(std::min(t_cap * ((quads + 127) / 128),
                                               (rope_ctas_per_sm() ? rope_ctas_per_sm() : 8) * kSms))),
                        dim3(128), 0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
