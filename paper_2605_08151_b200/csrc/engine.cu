@@ -254,7 +254,11 @@ struct ModelRT {
       TRY(gemm_set_outputs(&plm, logits, nullptr, nullptr, nullptr, 0));
     } else {
       // whole tiles per CTA (no stream-K): logits independent of the CTA budget
-      TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, 256));
+      static const int lm_tile = [] {
+        const char* v = getenv("SPECTRE_LM_TILE");
+        return (v && atoi(v) == 128) ? 128 : 256;
+      }();
+      TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, lm_tile));
       TRY(gemm_set_outputs(&plm, nullptr, amax_v, amax_i, nullptr, 0));
     }
     // each GEMM prefetches the next GEMM's weights into L2 (capped: the
