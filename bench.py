@@ -10,16 +10,21 @@ so no explicit L2 flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Multi-GPU (torchrun, one process per GPU): requests are independent, so each
-rank decodes its own batch of 64 (weak scaling); NCCL only gathers counters.
---impl reference times the CPU restatement of the reference decode loop
-(oracle/lockstep.py — the reference itself is Python and absent on the GPU
-box) on this host's cores for the same config.
+Multi-GPU (one process per GPU): requests are independent, so each rank
+decodes its own batch of 64 (weak scaling, default) or its shard of a global
+batch (`--shard`: --batch is the job's total, split by dist.shard_requests —
+strong scaling); NCCL only gathers counters.  Under torchrun the ranks come
+from the environment; `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks.
+--impl reference times the reference's own decode loop — stock `specsim.run`
+from baseline/_ref (the unmodified reference package, installed there) or, if
+that is absent, its CPU restatement oracle/lockstep.py — on every host core.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -33,6 +38,10 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 PEAKS_DEFAULT = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+# draft/target agreement of the C2 pair (branch 0.004, alpha 1): the alpha_measured
+# the GPU arm reports (it inverts the content accepted length); the reference arm,
+# launched separately, runs the reference loop at this agreement rate
+ALPHA_MEAS_C2 = 0.8707
 METRIC = "SPECTRE output tok/s (8B target, B=64, gamma=4) vs ordinary/parallel SD; r* crossover"
 
 
@@ -123,6 +132,10 @@ def allreduce_sum(x: float, ws: int) -> float:
     return float(t.item())
 
 
+def allreduce_min(x: float, ws: int) -> float:
+    return -allreduce_max(-x, ws)
+
+
 def barrier(ws):
     if ws > 1:
         import torch.distributed as dist
@@ -160,14 +173,22 @@ def run_ours(args):
 
     ws, rank, local = dist_setup()
     dev_index = local
-    B, g = args.batch, args.gamma
+    g = args.gamma
+    if args.shard:   # strong scaling: --batch requests in total, one contiguous shard per rank
+        from paper_2605_08151_b200.dist import shard_requests
+        sh = shard_requests(args.batch, ws, rank)
+        B, req0, seed = sh.count, sh.start, args.seed
+        if B < 1:
+            raise SystemExit(f"--shard: {args.batch} requests over {ws} ranks leaves rank {rank} empty")
+    else:            # weak scaling: --batch requests per rank
+        B, req0, seed = args.batch, 0, args.seed + rank
     spec_kw = dict(n_req=B, gamma=g, output_len=args.out_len, prompt_len=args.prompt_len,
-                   alpha=args.alpha, seed=args.seed + rank, controller=args.controller,
+                   alpha=args.alpha, seed=seed, controller=args.controller,
                    temperature=args.temperature)
     base = M.DecodeSpec(**spec_kw)
     pair = M.build_pair(M.LLAMA_31_8B, M.LLAMA_32_1B, n_req=B, ctx_cap=base.ctx_cap(),
                         seed=args.seed, target_branch=args.branch, draft_branch=args.branch)
-    prompts = M.synthetic_prompts(B, args.prompt_len, M.LLAMA_31_8B.vocab, seed=args.seed + rank)
+    prompts = M.synthetic_prompts(B, args.prompt_len, M.LLAMA_31_8B.vocab, seed=seed, req0=req0)
     variants = [args.variant] + [v for v in ("ordinary", "parallel") if v != args.variant and
                                  not args.headline_only]
     engines = {v: M.SpectreEngine(pair, base, v) for v in variants}
@@ -204,6 +225,7 @@ def run_ours(args):
         done = int((pos == args.out_len).sum().item())
         if done != B:
             raise RuntimeError(f"{v}: only {done}/{B} requests finished")
+        digest = hashlib.sha256(committed.cpu().numpy().tobytes()).hexdigest()[:16]
         total_tokens = allreduce_sum(tokens_per_step * args.steps, ws)
         rep = M.report_from_trace(__import__("paper_2605_08151_b200").PolicyVariant.parse(v),
                                   args.seed, trace, tokens_per_step,
@@ -228,7 +250,7 @@ def run_ours(args):
             t_draft_ms=float(trace["t_draft_ns"][trace["t_draft_ns"] > 0].mean() * 1e-6)
             if (trace["t_draft_ns"] > 0).any() else 0.0,
             gpu_launches=(launches + prefill_launches) * args.steps,
-            ordinary_share=modes.count("O") / max(1, len(modes)))
+            ordinary_share=modes.count("O") / max(1, len(modes)), committed_sha256=digest)
 
     head = results[args.variant]
     # ---- end-to-end through the public API with host buffers
@@ -255,6 +277,20 @@ def run_ours(args):
         e2e = {"value": allreduce_sum(tokens_per_step * args.steps, ws) / (ms / 1e3),
                "unit": "tok/s", "h2d_bytes_per_step": int(host_prompts.numel() * 4),
                "d2h_bytes_per_step": int(out_host.numel() * 8)}
+        e2e_digest = hashlib.sha256(out_host.numpy().tobytes()).hexdigest()[:16]
+
+    # ---- parity: greedy speculative decoding is lossless, so every mode (and the
+    # end-to-end pass through the public API) must commit the same token stream
+    digests = {v: r["committed_sha256"] for v, r in results.items()}
+    if e2e is not None:
+        digests["e2e"] = e2e_digest
+    parity = {"committed_sha256": digests,
+              "identical": len(set(digests.values())) == 1,
+              "rule": ("greedy: all modes commit the autoregressive stream (bit-exact)"
+                       if args.temperature <= 0 else
+                       "T>0: distributional (per-position uniforms differ by mode)")}
+    if ws > 1:
+        parity["identical"] = bool(allreduce_min(float(parity["identical"]), ws))
 
     # ---- roofline of the dominant kernel, timed live (CUDA events, its own stream)
     roof = None
@@ -278,17 +314,23 @@ def run_ours(args):
                       "frac": round(ideal_ms / r["t_round_ms"], 4),
                       "tok_s_at_roofline": round(committed_per_round / ideal_ms * 1e3, 1),
                       "peak_source": src}
-    # ---- CPU baseline (oracle port of the reference loop), rank 0, N=1 only
+    alpha_meas = alpha_from_L(head["content_L"], g)
+    # ---- like-for-like: the reference's own decode loop and model pair (hash
+    # stream + alpha-proposer) as the device-resident oracle-mode kernel
+    omode = None
+    if not args.no_oracle_mode and rank == 0:
+        omode = oracle_mode_speed(args, alpha_meas)
+    # ---- CPU baseline (stock reference loop, or its port), rank 0, N=1 only
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and ws == 1:
-        cpu = cpu_baseline(args, alpha_meas=alpha_from_L(head["content_L"], g))
+        cpu = cpu_baseline(args, alpha_meas=alpha_meas, omode=omode)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(head["value"], 2), "unit": "tok/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(head["ms_per_step"], 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic prompts (TokenStreamOracle prompt stream mod V), random-init "
                     "coupled weights",
             "config": {"workload": (f"C2: llama-3.1-8b-shape target / llama-3.2-1b-shape draft, "
@@ -301,16 +343,20 @@ def run_ours(args):
                        "variant": args.variant, "batch_per_gpu": B, "gamma": g,
                        "output_len": args.out_len, "prompt_len": args.prompt_len,
                        "draft_alpha": args.alpha, "branch_scale": args.branch,
-                       "controller": args.controller, "parallelism": f"dp{ws} (request shards)",
+                       "controller": args.controller,
+                       "parallelism": f"dp{ws} ({'shards of ' + str(args.batch) + ' requests' if args.shard else 'request batches'})",
                        "l2": "inputs > L2 (15 GB weights + KV streamed per round)"},
             "e2e": e2e, "roofline": roof, "round_roofline": round_roof, "cpu_baseline": cpu,
+            "parity": parity, "oracle_mode": omode, "alpha_measured": alpha_meas,
             "clocks": head["clocks"], "gpu_launches": head["gpu_launches"],
             "modes": {v: {k: (round(x, 4) if isinstance(x, float) else x)
                           for k, x in r.items() if k not in ("clocks", "timeline")}
                       for v, r in results.items()},
             "timeline_head": head["timeline"][:80],
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
+        if not parity["identical"] and args.temperature <= 0:
+            raise SystemExit("parity: modes committed different greedy streams")
 
 
 def linear_params(spec) -> int:
@@ -398,36 +444,100 @@ def roofline_gate_up(pair, args):
             "peak_source": src + " (MEASURED_PEAKS.json burst)"}
 
 
-def _lockstep_worker(job):
-    """One CPU worker: run the oracle port of specsim.run for one seed."""
-    cfg, variant = job
-    from oracle import lockstep as L
+# ----------------------------------------------------------------- the reference loop on CPU
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def reference_kind() -> str:
+    """'reference': stock specsim from baseline/_ref (the unmodified package);
+    'port': oracle/lockstep.py, its CPU restatement (pinned to 65 reference runs)."""
+    return "reference" if (REF_DIR / "specsim" / "__init__.py").exists() else "port"
+
+
+def _ref_worker(job):
+    """One CPU worker: one decode of the reference loop for one seed."""
+    cfg, variant, kind = job
     t0 = time.perf_counter()
+    if kind == "reference":
+        if str(REF_DIR) not in sys.path:
+            sys.path.insert(0, str(REF_DIR))
+        import specsim
+        from specsim.metrics import export_report
+        r = specsim.run(specsim.SimConfig(**cfg), variant)
+        return r.report.total_committed, time.perf_counter() - t0, export_report(r.report, "csv")
+    from oracle import lockstep as L
     r = L.run(cfg, variant)
-    return r.report["total_committed"], time.perf_counter() - t0
+    return r.report["total_committed"], time.perf_counter() - t0, L.export_csv(r.report)
 
 
-def _pool_run(cfgs, variant, procs):
+def _pool_run(cfgs, variant, procs, kind):
     import multiprocessing as mp
     ctx = mp.get_context("fork")
     with ctx.Pool(procs) as pool:
-        return pool.map(_lockstep_worker, [(c, variant) for c in cfgs])
+        return pool.map(_ref_worker, [(c, variant, kind) for c in cfgs])
 
 
-def cpu_baseline(args, alpha_meas: float, budget_s: float = 20.0):
-    """oracle/lockstep.py (CPU restatement of specsim.run), one process per host
-    core, one seed per process, for about budget_s of CPU work."""
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _ref_cfg(args, alpha):
+    return dict(batch_size=args.batch, n_requests=args.batch, gamma=args.gamma,
+                output_len=args.out_len, alpha=alpha, qps=1e6, seed=args.seed)
+
+
+def cpu_baseline(args, alpha_meas: float, omode=None):
+    """The reference's decode loop on CPU (stock specsim when installed in
+    baseline/_ref, else oracle/lockstep.py), one process per host core, one seed
+    per process, about one decode per core.  Also checks that the
+    device oracle-mode run reproduced the reference's report byte for byte."""
     procs = os.cpu_count() or 1
-    cfg = dict(batch_size=args.batch, n_requests=args.batch, gamma=args.gamma,
-               output_len=args.out_len, alpha=alpha_meas, qps=1e6, seed=args.seed)
+    kind = reference_kind()
+    cfg = _ref_cfg(args, alpha_meas)
     t0 = time.perf_counter()
-    res = _pool_run([{**cfg, "seed": args.seed + i} for i in range(procs)], "hybrid", procs)
+    res = _pool_run([{**cfg, "seed": args.seed + i} for i in range(procs)], "hybrid", procs, kind)
     dt = time.perf_counter() - t0
     toks = sum(r[0] for r in res)
-    return {"value": round(toks / dt, 1), "unit": "tok/s", "cores": procs, "kind": "port",
-            "sample": f"{procs} x oracle/lockstep.run(hybrid, B={args.batch}, gamma={args.gamma}, "
-                      f"output_len={args.out_len}, alpha={alpha_meas}), one process per host core "
-                      f"(multiprocessing); per-core {toks / sum(r[1] for r in res):.0f} tok/s"}
+    if omode is not None and "report_csv" in omode:
+        omode["report_identical_to_reference"] = omode.pop("report_csv") == res[0][2]
+        omode["checked_against"] = kind
+    return {"value": round(toks / dt, 1), "unit": "tok/s", "cores": procs, "kind": kind,
+            "cpu_model": cpu_model(),
+            "sample": f"{procs} x {'specsim.run' if kind == 'reference' else 'oracle/lockstep.run'}"
+                      f"(hybrid, B={args.batch}, gamma={args.gamma}, output_len={args.out_len}, "
+                      f"alpha={alpha_meas} = the GPU run's measured agreement), one process per "
+                      f"host core (multiprocessing); per-core "
+                      f"{toks / sum(r[1] for r in res):.0f} tok/s; {dt:.1f} s wall"}
+
+
+def oracle_mode_speed(args, alpha):
+    """The reference's protocol AND model pair (hash stream + alpha-proposer),
+    decoded by the device-resident oracle-mode loop through the public API
+    (host config in, host report out): the like-for-like figure against the
+    reference arm.  Wall time per decode, CUDA-synchronised on both sides."""
+    import torch
+    import paper_2605_08151_b200 as P
+    cfg = _ref_cfg(args, alpha)
+    P.run(P.SimConfig(**cfg), "hybrid")   # warm (allocations, module load)
+    torch.cuda.synchronize()
+    n = max(3, args.steps)
+    t0 = time.perf_counter()
+    for _ in range(n):
+        got = P.run(P.SimConfig(**cfg), "hybrid")
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / n
+    tok = got.report.total_committed
+    return {"value": round(tok / dt, 1), "unit": "tok/s", "ms_per_decode": round(dt * 1e3, 3),
+            "decodes": n, "config": f"hybrid, B={args.batch}, gamma={args.gamma}, output_len="
+                                    f"{args.out_len}, alpha={alpha}, seed={args.seed}",
+            "report_csv": P.export_report(got.report)}
 
 
 # ----------------------------------------------------------------- reference arm
@@ -438,50 +548,75 @@ def run_reference(args):
         return
     alpha = args.alpha_meas
     procs = os.cpu_count() or 1
-    cfg = dict(batch_size=args.batch, n_requests=args.batch, gamma=args.gamma,
-               output_len=args.out_len, alpha=alpha, qps=1e6, seed=args.seed)
+    kind = reference_kind()
+    cfg = _ref_cfg(args, alpha)
     _pool_run([{**cfg, "seed": args.seed + 1000 + i} for i in range(min(procs, args.warmup))],
-              args.variant, procs)
+              args.variant, procs, kind)
     t0 = time.perf_counter()
     toks = 0
     for step in range(args.steps):   # a step = one B=64 decode per host core
         res = _pool_run([{**cfg, "seed": args.seed + step * procs + i} for i in range(procs)],
-                        args.variant, procs)
+                        args.variant, procs, kind)
         toks += sum(r[0] for r in res)
     dt = time.perf_counter() - t0
     v = toks / dt
-    sample = (f"{args.steps} steps x {procs} processes x oracle/lockstep.run({args.variant}, "
-              f"B={args.batch}, gamma={args.gamma}, output_len={args.out_len}, alpha={alpha}); "
-              f"the reference (specsim, pure Python) cannot travel to the GPU box, this is its "
-              f"CPU port on every host core")
+    what = ("stock specsim.run from baseline/_ref (the unmodified reference package)"
+            if kind == "reference" else "oracle/lockstep.run (CPU restatement; baseline/_ref "
+                                        "absent)")
+    sample = (f"{args.steps} steps x {procs} processes x {what}({args.variant}, B={args.batch}, "
+              f"gamma={args.gamma}, output_len={args.out_len}, alpha={alpha}); one decode per "
+              f"host core per step")
     print(json.dumps({
         "metric": METRIC, "value": round(v, 2), "unit": "tok/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (reference TokenStreamOracle model pair)", "impl": "reference",
-        "config": {"workload": "C2 protocol shape on the reference's synthetic model pair",
+        "config": {"workload": "C2 protocol shape on the reference's synthetic model pair "
+                               "(the reference has no neural model)",
                    "variant": args.variant, "batch": args.batch, "gamma": args.gamma,
-                   "output_len": args.out_len},
-        "cpu_baseline": {"value": round(v, 2), "unit": "tok/s", "cores": procs, "kind": "port",
-                         "sample": sample},
+                   "output_len": args.out_len, "alpha": alpha},
+        "cpu_baseline": {"value": round(v, 2), "unit": "tok/s", "cores": procs, "kind": kind,
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(v, 2), "unit": "tok/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0}}))
+                "d2h_bytes_per_step": 0}}), flush=True)
 
 
-def main():
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n: int, argv: list[str], script: str | None = None) -> int:
+    """`--gpus N` without torchrun: re-launch under torch.distributed.run, one
+    process per GPU (rank 0 prints the JSON line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           script or str(Path(__file__).resolve()), *argv]
+    return subprocess.call(cmd)
+
+
+def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--variant", default="hybrid")
-    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--batch", type=int, default=64,
+                    help="requests per GPU (weak scaling) or in total with --shard")
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: split --batch requests over the ranks")
     ap.add_argument("--gamma", type=int, default=4)
     ap.add_argument("--out-len", type=int, default=1024)
     ap.add_argument("--prompt-len", type=int, default=128)
     ap.add_argument("--alpha", type=float, default=1.0, help="draft keep probability")
-    ap.add_argument("--alpha-meas", type=float, default=0.8,
-                    help="reference arm: agreement rate of the synthetic pair")
+    ap.add_argument("--alpha-meas", type=float, default=ALPHA_MEAS_C2,
+                    help="reference arm: agreement rate of the synthetic pair (the GPU run's "
+                         "measured draft/target agreement at C2)")
     ap.add_argument("--branch", type=float, default=0.004)
     ap.add_argument("--controller", default="round")
     ap.add_argument("--temperature", type=float, default=0.0,
@@ -491,12 +626,24 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--no-oracle-mode", action="store_true")
+    argv = sys.argv[1:] if argv is None else argv
+    args = ap.parse_args(argv)
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is not None and int(ws_env) != args.gpus and int(ws_env) > 1:
+        raise SystemExit(f"--gpus {args.gpus} disagrees with WORLD_SIZE={ws_env}")
     if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+        run_reference(args)      # rank 0 only; CPU work, no GPU needed
+        return 0
+    if args.gpus > 1 and ws_env is None:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"--gpus {args.gpus}: only {have} CUDA device(s) visible")
+        return spawn_ranks(args.gpus, argv)
+    run_ours(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -117,6 +117,10 @@ typedef struct SpectreOracleConfig {
   double t_draft_slope;
   double t_draft_init;
   int32_t t_draft_free_batch;
+  /* reply deadline (core.py:123, 2 * t_target by default): a conservative
+   * parallel round (gamma * T_D^mix > t_target, sim.py:143-146) commits when
+   * its replies land, which must be before this deadline (sim.py:599-606) */
+  double reply_timeout;
 } SpectreOracleConfig;
 
 typedef struct SpectreOracleOutputs {

@@ -39,6 +39,7 @@ class OracleConfig(C.Structure):
         ("t_draft_slope", C.c_double),
         ("t_draft_init", C.c_double),
         ("t_draft_free_batch", C.c_int32),
+        ("reply_timeout", C.c_double),
     ]
 
 

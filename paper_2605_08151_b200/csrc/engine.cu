@@ -718,6 +718,10 @@ struct Engine {
       return r;
     }
     graph_loop = g;
+    // the graph captured its own copy of the state with the conditional
+    // handles; eager rounds / host-driven steps launched later from `st`
+    // must not call cudaGraphSetConditional outside the graph
+    st.use_handles = 0;
     return SPECTRE_OK;
   }
 };
@@ -762,6 +766,12 @@ extern "C" void* spectre_engine_create(const SpectreModelDims* target,
       cfg->ctx_cap < cfg->prompt_len + cfg->output_len + 4 * cfg->gamma + 16 ||
       target->vocab != draft->vocab) {
     arg_fail("spectre_engine_create: decode config");
+    return nullptr;
+  }
+  if (cfg->temperature > 0.0 && cfg->alpha < 1.0) {
+    // rejection sampling tests min(1, p/q) against the draft's q; the alpha
+    // noise would replace the proposal by a token not drawn from q
+    arg_fail("spectre_engine_create: temperature > 0 needs alpha == 1 (no draft noise)");
     return nullptr;
   }
   auto e = std::make_unique<Engine>();

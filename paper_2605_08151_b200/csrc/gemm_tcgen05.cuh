@@ -316,6 +316,9 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   }
   GemmSched sched;
   sched.init(a, T, BK, Cfg::kPass);
+  // pair mode: the leader's issuer waits only on its own tmem_empty, so a
+  // pair CTA may own at most one job (gemm_set_pair: one tile per CTA)
+  if (kPair && pair && sched.n_tiles * sched.splits > sched.G) __trap();
   if (a.dbg && threadIdx.x == 64) a.dbg[blockIdx.x * 8 + 0] = gtimer();
   const bool no_work = (T == 0);
 

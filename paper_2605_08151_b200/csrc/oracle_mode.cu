@@ -117,7 +117,8 @@ enum OracleError : int64_t {
   kErrRegression = 2,
   kErrHistoryOverflow = 3,
   kErrUniformsExhausted = 4,
-  kErrLateReply = 5,       // parallel reply would miss the commit: outside domain
+  kErrLateReply = 5,       // parallel reply would miss the commit (or, conservative,
+                           // the reply deadline): outside domain
   kErrTraceOverflow = 6,
   kErrMisanchored = 7,
 };
@@ -419,6 +420,8 @@ k_oracle_decode_loop(SpectreOracleConfig cfg, const double* __restrict__ arrival
       // (draft_engine.py:158-164, 335-344)
       const int over = queries > cfg.t_draft_free_batch ? queries - cfg.t_draft_free_batch : 0;
       const double tdm = __dadd_rn(cfg.t_draft, __dmul_rn(cfg.t_draft_slope, (double)over));
+      // conservative_mode_check on the last reply's T_D^mix (sim.py:143-146, 599-602)
+      const bool conservative = mode == 'P' && __dmul_rn((double)g, s_tdm) > cfg.t_target;
       if (mode == 'O' && queries > 0) {
         steps = g - 1;
         dstart = __dadd_rn(now, cfg.delay);
@@ -433,9 +436,18 @@ k_oracle_decode_loop(SpectreOracleConfig cfg, const double* __restrict__ arrival
       }
       const double t_t =
           __dadd_rn(cfg.t_target, __dmul_rn(cfg.t_target_slope, (double)(participants - 1)));
-      const double commit = __dadd_rn(dispatch, t_t);
-      if (mode == 'P' && !(__dadd_rn(ddone, cfg.delay) < commit)) {
-        block_fail(out.scalars, kErrLateReply, -1);
+      double commit = __dadd_rn(dispatch, t_t);
+      if (mode == 'P') {
+        const double reply = __dadd_rn(ddone, cfg.delay);
+        if (conservative) {
+          // _try_commit waits for every queried reply (sim.py:624-640, 841-844);
+          // they must land before the wait deadline (no timeout in the domain)
+          if (!(__dsub_rn(reply, dispatch) < __dsub_rn(cfg.reply_timeout, 1e-12)))
+            block_fail(out.scalars, kErrLateReply, -1);
+          if (reply > commit) commit = reply;
+        } else if (!(reply < commit)) {
+          block_fail(out.scalars, kErrLateReply, -1);
+        }
       }
       out.round_mode[ridx] = mode;
       out.round_participants[ridx] = participants;

@@ -211,8 +211,6 @@ def _check_domain(cfg: SimConfig, variant: PolicyVariant) -> float:
                       mixed_step_latency(*draft_latency(cfg)[1:4], cfg.max_concurrency))
         if 2 * d + (g - 1) * t_d_max >= cfg.reply_timeout:
             raise OutsideDeviceDomain("ordinary repairs would time out")
-        if g * t_d_max > cfg.t_target:
-            raise OutsideDeviceDomain("conservative rounds (gamma*T_D > T_T)")
     return d
 
 
@@ -295,7 +293,8 @@ def run(config: SimConfig, variant: PolicyVariant | str, workload: Workload | No
         alpha=dl[0], t_target=cfg.t_target, t_draft=dl[1], delay=d,
         t_target_slope=cfg.t_target_slope, ema_decay=cfg.ema_decay,
         fixed_threshold_l=float(cfg.fixed_threshold_l or 0.0),
-        t_draft_slope=dl[2], t_draft_init=dl[4], t_draft_free_batch=dl[3])
+        t_draft_slope=dl[2], t_draft_init=dl[4], t_draft_free_batch=dl[3],
+        reply_timeout=cfg.reply_timeout)
     ws_bytes = L.spectre_oracle_workspace_bytes(c)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     arr = torch.tensor(arrivals, dtype=torch.float64, device=dev)
@@ -331,7 +330,8 @@ def run(config: SimConfig, variant: PolicyVariant | str, workload: Workload | No
     n_rounds, draws, err, err_req, n_fin = (int(x) for x in sc[:5])
     if err != 0:
         names = {1: "commit gap", 2: "position regression", 3: "draft history overflow",
-                 4: "uniform stream exhausted", 5: "parallel reply after commit",
+                 4: "uniform stream exhausted",
+                 5: "parallel reply after the commit / conservative reply after the deadline",
                  6: "round trace overflow", 7: "misanchored segment"}
         msg = names.get(err, f"error {err}")
         if err in (5,):
@@ -367,6 +367,12 @@ def _assemble_result(cfg, variant, workload, d, h, cpos, fin_at, adm_at, committ
     counter = 0
     n_queries = 0
     draft_tokens = 0
+    # conservative_mode_check (sim.py:143-146, 599-602) on the T_D^mix the target
+    # last received (sim.py:283-288, 833-834), exactly as the device loop did
+    lat = draft_latency(cfg)
+    last_tdm = lat[4]
+    n_conservative = 0
+    commit_push = []        # when the event that committed each round was pushed
     for k in range(n_rounds):
         mode = chr(int(h["round_mode"][k]))
         P = int(h["round_participants"][k])
@@ -374,10 +380,18 @@ def _assemble_result(cfg, variant, workload, d, h, cpos, fin_at, adm_at, committ
         r_hats.append(rh)
         timeline.append(mode)
         started, commit = float(h["round_started"][k]), float(h["round_commit"][k])
+        cons = mode == "P" and cfg.gamma * last_tdm > cfg.t_target
+        n_conservative += cons
+        push = float(h["round_dispatch"][k])
+        if cons:
+            t_t = cfg.t_target + cfg.t_target_slope * (P - 1)
+            if float(h["round_draft_done"][k]) + d > push + t_t:
+                push = float(h["round_draft_done"][k])   # committed by the reply DELIVERY
+        commit_push.append(push)
         trace.append(RoundTrace(round=k + 1, started_at=started, committed_at=commit,
                                 mode=mode, participants=P,
                                 committed_delta=int(h["round_delta"][k]), r_hat=rh,
-                                speculation_on=spec, timeout=False, conservative=False,
+                                speculation_on=spec, timeout=False, conservative=cons,
                                 breaker_streak=0, disabled_until=0))
         deltas_all_sum += int(h["round_delta"][k])
         deltas_all_n += P
@@ -393,8 +407,9 @@ def _assemble_result(cfg, variant, workload, d, h, cpos, fin_at, adm_at, committ
                 started_at=float(h["round_draft_start"][k]),
                 finished_at=float(h["round_draft_done"][k]), n_speculative=q, n_regular=0,
                 regular_pending_at_start=0, forced_regular=False,
-                t_d_mix=mixed_step_latency(*draft_latency(cfg)[1:4], q),
+                t_d_mix=mixed_step_latency(*lat[1:4], q),
                 steps=steps, counter_after=counter))
+            last_tdm = mixed_step_latency(*lat[1:4], q)
             n_queries += q
             draft_tokens += int(h["round_draft_tokens"][k])
     n = len(cpos)
@@ -416,7 +431,7 @@ def _assemble_result(cfg, variant, workload, d, h, cpos, fin_at, adm_at, committ
     s_time = sum(r[2] - r[1] for r in steady)
     s_dn = sum(r[0] for r in steady)
     s_cs, s_cn = sum(r[4] for r in steady), sum(r[5] for r in steady)
-    final_dispatch = float(h["round_dispatch"][-1]) if n_rounds else t_end
+    final_dispatch = commit_push[-1] if n_rounds else t_end
     hb_sent, hb_deliv = _heartbeat_counts(cfg.heartbeat_period, d, t_end, final_dispatch)
     closes = [float(t) for t in fin_at] if spec else []
     td_sent = 2 * n_queries + len(closes)
@@ -443,7 +458,7 @@ def _assemble_result(cfg, variant, workload, d, h, cpos, fin_at, adm_at, committ
         sim_duration=duration, total_committed=total, total_rounds=n_rounds,
         requests_completed=n, breaker_activations=0,
         fallback_rounds=sum(1 for m in timeline if m == "F"), timeout_rounds=0,
-        conservative_rounds=0, transport_sent=td_sent + tt_sent,
+        conservative_rounds=n_conservative, transport_sent=td_sent + tt_sent,
         transport_delivered=td_deliv + tt_deliv, transport_dropped=0, transport_stale=0,
         transport_rejected=0, stale_replies=0, draft_tokens_generated=draft_tokens,
         background_tokens=0, background_completed=0)

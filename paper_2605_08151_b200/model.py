@@ -185,6 +185,11 @@ class DecodeSpec:
     breaker_threshold: int = 3      # circuit breaker (core.py:93-94, target_engine.py:337-380)
     breaker_cooldown: int = 5
 
+    def __post_init__(self):
+        if self.temperature > 0 and self.alpha < 1.0:
+            raise ValueError("temperature > 0 (rejection sampling) needs alpha == 1: the "
+                             "alpha noise would replace proposals not drawn from q")
+
     def ctx_cap(self) -> int:
         need = self.prompt_len + self.output_len + 4 * self.gamma + 16
         return (need + 63) // 64 * 64
@@ -322,11 +327,12 @@ class SpectreEngine:
         return out_tok[:T], (out_x[:T] if want_x else None)
 
 
-def synthetic_prompts(n_req: int, prompt_len: int, vocab: int, seed: int = 0):
-    """Prompt ids = TokenStreamOracle(seed).prompt_tokens(req, P) mod V,
-    computed by the K8 stream kernel."""
+def synthetic_prompts(n_req: int, prompt_len: int, vocab: int, seed: int = 0, req0: int = 0):
+    """Prompt ids = TokenStreamOracle(seed).prompt_tokens(req, P) mod V for
+    the global requests req0 .. req0 + n_req - 1, computed by the K8 stream kernel."""
     torch = _native.require_cuda()
-    req = torch.arange(n_req, device="cuda", dtype=torch.int64).repeat_interleave(prompt_len)
+    req = torch.arange(req0, req0 + n_req, device="cuda",
+                       dtype=torch.int64).repeat_interleave(prompt_len)
     pos = torch.arange(prompt_len, device="cuda", dtype=torch.int64).repeat(n_req)
     out = torch.empty_like(req)
     _native.check(_native.lib().spectre_oracle_stream(

@@ -26,6 +26,12 @@ def golden_runs_draft_model():
 
 
 @pytest.fixture(scope="session")
+def golden_runs_conservative():
+    """Conservative parallel rounds (scripts/make_golden_conservative.py)."""
+    return json.loads((GOLDEN / "runs_conservative.json").read_text())["cases"]
+
+
+@pytest.fixture(scope="session")
 def golden_streams():
     return json.loads((GOLDEN / "streams.json").read_text())
 

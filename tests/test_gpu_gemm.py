@@ -210,3 +210,43 @@ def test_argmax_no_stale_partials(env):
             top2 = logits.topk(2, dim=1).values
             clear = (top2[:, 0] - top2[:, 1]) > 1e-2
             assert torch.equal(idx[clear], logits.argmax(1)[clear]), (seed, T)
+
+
+@pytest.mark.parametrize("T", [16, 100, 256])
+def test_cta_pair_swiglu_at_8b_gate_up(env, T):
+    """The verify gate/up GEMM exactly as the engine launches it at the 8B
+    shape (N = 2*14336, K = 4096): CTA pairs (cta_group::2, flag 4000) must be
+    bit-identical to the single-CTA 256-row kernel (flag 2000: same per-row
+    k order) and within bf16 tolerance of the fp32 reference."""
+    torch = env[0]
+    N, K = 2 * 14336, 4096
+    g = torch.Generator(device="cuda").manual_seed(T)
+    X = torch.randn(512, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).bfloat16()
+    _, _, _, single = _run(env, X, W, T, 512, 1, SWIGLU, max_stages=2000)
+    _, _, _, pair = _run(env, X, W, T, 512, 1, SWIGLU, max_stages=4000)
+    assert torch.equal(pair[:T], single[:T])
+    Wv = W.view(N // 2, 2, K)
+    gt = _ref(torch, X, Wv[:, 0], T)
+    ut = _ref(torch, X, Wv[:, 1], T)
+    want = torch.nn.functional.silu(gt) * ut
+    # bf16 output: 2^-8 relative, plus tanh.approx SiLU (~2^-11)
+    assert torch.allclose(pair[:T].float(), want, atol=2e-2, rtol=1e-2)
+
+
+@pytest.mark.parametrize("T", [20, 256])
+def test_lm_head_argmax_at_128k_vocab(env, T):
+    """Greedy lm_head at V = 128256, K = 4096 (the 8B target's head: several
+    256-row tiles per CTA) against the fp32 argmax."""
+    torch = env[0]
+    V, K = 128256, 4096
+    g = torch.Generator(device="cuda").manual_seed(V + T)
+    X = torch.randn(256, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(V, K, device="cuda", generator=g) * 0.02).bfloat16()
+    _, av, ai, _ = _run(env, X, W, T, 256, 1, ARGMAX, max_stages=2000)
+    idx = ai[:, :T].gather(0, av[:, :T].argmax(0)[None]).squeeze(0).long()
+    logits = _ref(torch, X, W, T)
+    top2 = logits.topk(2, dim=1).values
+    clear = (top2[:, 0] - top2[:, 1]) > 1e-2
+    assert torch.equal(idx[clear], logits.argmax(1)[clear])
+    assert clear.float().mean().item() > 0.8

@@ -1,0 +1,136 @@
+"""Model-mode parity at the BASELINE shapes (configs 2 and 5), not just the
+tiny / small test models.
+
+* C2 pair (Llama-3.1-8B-shape target, Llama-3.2-1B-shape draft): a verify-
+  shaped forward (gamma + 1 = 5 new rows per request, 8 requests) through the
+  engine exactly as the decode loop runs it — CTA-pair gate/up GEMM
+  (cta_group::2, selected because 2F/256 = 112 tiles), split-K q/k/v / o /
+  down, the 128,256-vocab greedy lm_head with several tiles per CTA — against
+  the fp32 restatement `oracle/model_ref.py` with full-strength transformer
+  branches (branch_scale 1.0).
+* C2 losslessness: AR, ordinary, parallel and SPECTRE (hybrid) commit the
+  same greedy stream at the 8B/1B shapes (draft noise alpha 0.8, so every
+  protocol path — rejections, rollbacks, PADDED rounds — is taken).
+* C5 pair (Qwen2.5-32B-shape target, Qwen2.5-0.5B-shape draft): one verify-
+  shaped forward (gamma + 1 = 7 rows) of each model against the restatement.
+
+Tolerances (stated, as in test_gpu_model.py): the final hidden state within
+|dx| <= X_RTOL * rms(x) on average (bf16 storage at the kernels' rounding
+points, fp32 accumulation in a different order); greedy tokens identical
+wherever the fp32 top-2 logit margin exceeds MARGIN.
+"""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+MARGIN = 0.05
+X_RTOL = 3e-2
+
+
+@pytest.fixture(scope="module")
+def M():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2605_08151_b200 import model
+    return model
+
+
+def _free():
+    import gc
+
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def _verify_shaped_forward(eng, which, prompts, rows):
+    """Feed each request's prompt through the forward `rows` tokens at a time
+    (the packed ragged batch of a verify pass: [bonus, gamma candidates])."""
+    import torch
+    n, P = prompts.shape
+    outs, xs = [], []
+    for c0 in range(0, P, rows):
+        cs = min(rows, P - c0)
+        tok = prompts[:, c0:c0 + cs].reshape(-1)
+        pos = torch.arange(c0, c0 + cs, device="cuda").repeat(n)
+        slot = torch.arange(n, device="cuda").repeat_interleave(cs)
+        q_off = torch.arange(n, device="cuda") * cs
+        n_new = torch.full((n,), cs, device="cuda")
+        pos0 = torch.full((n,), c0, device="cuda")
+        o, x = eng.forward(which, tok, pos, slot, q_off, n_new, pos0, want_x=True)
+        outs.append(o.view(n, cs))
+        xs.append(x.view(n, cs, -1))
+    return torch.cat(outs, 1), torch.cat(xs, 1)
+
+
+def _check_vs_reference(weights, prompts, toks, xs):
+    import torch
+    from oracle.model_ref import reference_forward
+    clear_frac = []
+    for r in range(prompts.shape[0]):
+        x_ref, logits = reference_forward(weights, prompts[r])
+        dx = (xs[r].float() - x_ref).abs()
+        rms = x_ref.pow(2).mean().sqrt().item()
+        assert dx.mean().item() <= X_RTOL * x_ref.abs().mean().item(), (r, dx.mean().item())
+        assert dx.max().item() <= X_RTOL * rms * 16, (r, dx.max().item(), rms)
+        top2 = logits.topk(2, -1).values
+        clear = (top2[:, 0] - top2[:, 1]) > MARGIN
+        assert torch.equal(toks[r][clear].long(), logits.argmax(-1)[clear]), r
+        clear_frac.append(clear.float().mean().item())
+        del logits
+    assert sum(clear_frac) / len(clear_frac) > 0.5
+
+
+def test_c2_verify_forward_vs_fp32_reference(M):
+    n, P, gamma = 8, 20, 4
+    pair = M.build_pair(M.LLAMA_31_8B, M.LLAMA_32_1B, n_req=n, ctx_cap=128, seed=21,
+                        target_branch=1.0, draft_branch=1.0)
+    spec = M.DecodeSpec(n_req=n, gamma=gamma, output_len=32, prompt_len=P, seed=21)
+    eng = M.SpectreEngine(pair, spec, "hybrid")
+    prompts = M.synthetic_prompts(n, P, M.LLAMA_31_8B.vocab, seed=21)
+    toks, xs = _verify_shaped_forward(eng, 0, prompts, gamma + 1)
+    _check_vs_reference(pair.target, prompts, toks, xs)
+    # the draft's decode shape: one new token per request
+    toks, xs = _verify_shaped_forward(eng, 1, prompts[:, :8], 1)
+    _check_vs_reference(pair.draft, prompts[:, :8], toks, xs)
+    eng.close()
+    del eng, pair
+    _free()
+
+
+def test_c2_speculative_decoding_is_lossless(M):
+    import torch
+    n = 8
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=64, prompt_len=32, alpha=0.8, seed=4)
+    pair = M.build_pair(M.LLAMA_31_8B, M.LLAMA_32_1B, n_req=n, ctx_cap=spec.ctx_cap(), seed=4,
+                        target_branch=0.004, draft_branch=0.004)
+    ar = M.decode(pair, spec, "ar")
+    assert (ar.committed_pos == spec.output_len).all()
+    timelines = {}
+    for v in ("ordinary", "parallel", "hybrid"):
+        got = M.decode(pair, spec, v, use_graph=True)
+        assert got.graph == 1, got.extra
+        assert torch.equal(got.committed, ar.committed), v
+        timelines[v] = got.report.mode_timeline
+    assert set(timelines["ordinary"]) == {"O"}
+    assert set(timelines["parallel"]) == {"P"}
+    del pair
+    _free()
+
+
+def test_c5_qwen_forward_vs_fp32_reference(M):
+    n, P, gamma = 4, 14, 6
+    pair = M.build_pair(M.QWEN_25_32B, M.QWEN_25_05B, n_req=n, ctx_cap=128, seed=23,
+                        target_branch=1.0, draft_branch=1.0)
+    spec = M.DecodeSpec(n_req=n, gamma=gamma, output_len=32, prompt_len=P, seed=23)
+    eng = M.SpectreEngine(pair, spec, "hybrid")
+    prompts = M.synthetic_prompts(n, P, M.QWEN_25_32B.vocab, seed=23)
+    toks, xs = _verify_shaped_forward(eng, 0, prompts, gamma + 1)
+    _check_vs_reference(pair.target, prompts, toks, xs)
+    toks, xs = _verify_shaped_forward(eng, 1, prompts, 1)
+    _check_vs_reference(pair.draft, prompts, toks, xs)
+    eng.close()
+    del eng, pair
+    _free()

@@ -109,9 +109,18 @@ def test_device_loop_draft_model_matches_reference(pkg, golden_runs_draft_model,
     test_device_decode_loop_matches_reference(pkg, golden_runs_draft_model, idx)
 
 
+@pytest.mark.parametrize("idx", range(24))
+def test_device_loop_conservative_matches_reference(pkg, golden_runs_conservative, idx):
+    """a10: conservative parallel rounds on the device loop (the commit waits
+    for the replies; simulated clock in IEEE doubles, no FMA)."""
+    test_device_decode_loop_matches_reference(pkg, golden_runs_conservative, idx)
+
+
 def test_device_loop_outside_domain_refused(pkg):
     with pytest.raises(pkg.OutsideDeviceDomain):
         pkg.run(pkg.SimConfig(batch_size=4, n_requests=4, output_len=8, drop_prob=0.1), "hybrid")
+    with pytest.raises(pkg.OutsideDeviceDomain):   # conservative replies miss the deadline
+        pkg.run(pkg.SimConfig(batch_size=4, n_requests=4, output_len=8, t_draft=0.03), "parallel")
 
 
 def test_device_loop_large_batch_against_oracle(pkg):

@@ -79,6 +79,14 @@ def test_lockstep_matches_reference_draft_model(golden_runs_draft_model, idx):
     test_lockstep_matches_reference_run(golden_runs_draft_model, idx)
 
 
+@pytest.mark.parametrize("idx", range(24))
+def test_lockstep_matches_reference_conservative(golden_runs_conservative, idx):
+    """a10: conservative parallel rounds (gamma * T_D^mix > T_T, sim.py:143-146,
+    599-606) — the commit waits for the replies; conservative flags in the
+    trace and the report's conservative_rounds equal the reference's."""
+    test_lockstep_matches_reference_run(golden_runs_conservative, idx)
+
+
 def test_verify_semantics():
     # /root/reference/pkg/tests/test_oracle.py:119-178
     cand = [L.reference_token(0, 1, i) for i in range(4)]
@@ -96,5 +104,11 @@ def test_out_of_domain_is_refused():
         L.run(dict(batch_size=4, n_requests=4, output_len=8, drop_prob=0.1), "hybrid")
     with pytest.raises(L.OutOfDomain):
         L.run(dict(batch_size=4, n_requests=4, output_len=8, gamma=1), "ordinary")
+    # contention makes this round's T_D^mix exceed the last reply's: the
+    # (non-conservative) parallel replies would land after the commit
     with pytest.raises(L.OutOfDomain):
-        L.run(dict(batch_size=4, n_requests=4, output_len=8, gamma=12), "parallel")
+        L.run(dict(batch_size=8, n_requests=8, output_len=16, gamma=8, qps=1e6,
+                   t_draft_slope=0.0002), "parallel")
+    # conservative round whose replies miss the reply deadline (timeouts)
+    with pytest.raises(L.OutOfDomain):
+        L.run(dict(batch_size=4, n_requests=4, output_len=8, t_draft=0.03), "parallel")
