@@ -13,16 +13,6 @@ static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 // SPECTRE_PDL=0 disables programmatic dependent launch (A/B measurements).
-bool& no_grid_sync_ref() {
-  static thread_local bool v = false;
-  return v;
-}
-
-int& cta_cap_ref() {
-  static thread_local int cap = 0;
-  return cap;
-}
-
 bool pdl_enabled() {
   static const bool on = [] {
     const char* v = getenv("SPECTRE_PDL");

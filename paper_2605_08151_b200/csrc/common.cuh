@@ -50,32 +50,6 @@ __device__ __forceinline__ void pdl_trigger() {
 
 bool pdl_enabled();
 
-// SM budget for the persistent / grid-stride kernels launched by this host
-// thread (0: whole GPU).  Parallel rounds run the draft and the target
-// concurrently with disjoint CTA budgets so they co-reside instead of
-// time-slicing the SMs; every kernel honouring it has a result independent
-// of its grid size.
-int& cta_cap_ref();
-inline int cap_grid(int g) {
-  const int c = cta_cap_ref();
-  return (c > 0 && g > c) ? c : g;
-}
-// Set while capturing/launching work that runs CONCURRENTLY with another
-// stream's kernels (parallel rounds): kernels with an in-kernel grid barrier
-// (fused split-K reductions) would deadlock if two of them each held part of
-// the GPU, so they fall back to separate reduction kernels.
-bool& no_grid_sync_ref();
-struct NoGridSyncGuard {
-  bool prev;
-  NoGridSyncGuard() : prev(no_grid_sync_ref()) { no_grid_sync_ref() = true; }
-  ~NoGridSyncGuard() { no_grid_sync_ref() = prev; }
-};
-struct CtaCapGuard {
-  int prev;
-  explicit CtaCapGuard(int c) : prev(cta_cap_ref()) { cta_cap_ref() = c; }
-  ~CtaCapGuard() { cta_cap_ref() = prev; }
-};
-
 // Every kernel uses the same (maximum) shared-memory carveout so consecutive
 // kernels never force an L1/shared reconfiguration of the SMs.
 cudaError_t ensure_carveout(const void* kern);

@@ -8,9 +8,8 @@
 //                             ├─► IF(parallel){ fork: draft speculation (γ steps) ∥ verify; join }
 //                             └─► IF(ar){ verify }
 //                                        ─► accept (rejection-sampling pre-pass when T > 0)
-// In parallel rounds the draft and the target run with disjoint CTA budgets
-// (par_draft_ctas + par_target_ctas <= SMs) so their persistent kernels
-// co-reside on different SMs instead of time-slicing the GPU.
+// In parallel rounds the draft and the target are forked onto two streams and
+// joined before the accept.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -25,8 +24,6 @@
 
 namespace spectre {
 
-int launch_attention(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, int hd,
-                     int rows_per_req, cudaStream_t s);
 int launch_attention_w(const CUtensorMap& tk32, const CUtensorMap& tv32, const AttnArgs& a,
                        int hd, int rows_per_req, cudaStream_t s);
 int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void* E,
@@ -91,16 +88,9 @@ static int prefill_chunk(int n_req) {
   return std::max(1, std::min(16, rows / std::max(1, n_req)));
 }
 
-static int jobs_per_cta() {
-  const char* v = getenv("SPECTRE_JOBS_PER_CTA");
-  const int j = v ? atoi(v) : 1;
-  return j < 1 ? 1 : (j > 4 ? 4 : j);
-}
-
 static int pick_splits(int n_tiles, int k_iters, int ctas = 148) {
-  // one wave of CTAs x jobs per CTA: with two or more jobs a CTA's epilogue
-  // overlaps its next job's mainloop (double-buffered TMEM)
-  int s = ctas * jobs_per_cta() / n_tiles;
+  // one wave of CTAs, one split-K job each (two jobs per CTA measured slower)
+  int s = ctas / n_tiles;
   if (s > 12) s = 12;     // partial traffic grows with s (consumers unroll <= 12)
   if (s < 1) s = 1;
   while (s > 1 && k_iters / s < 3) --s;
@@ -115,16 +105,11 @@ struct ModelRT {
   int sp_qkv = 1, sp_o = 1, sp_d = 1;
   int tr_qkv = 256, tr_o = 256, tr_d = 256;   // weight rows per tile, per GEMM
   int tile_rows = 256;   // weight rows per GEMM CTA (128 for small-T models)
-  long long pf_cap = 0;   // L2 prefetch of the next GEMM's weights (bytes; measured: off)
   bool half_gemm = false; // decode GEMMs in the half-SM config (2 CTAs per SM, 128-row tiles)
   int attn_chunk = 128;
   float* h = nullptr;
   __nv_bfloat16 *x = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
   float *part = nullptr, *att_o = nullptr, *att_ml = nullptr, *amax_v = nullptr;
-  int* gbar = nullptr;        // [2] grid barrier of this model's fused-post GEMMs
-  bool fuse_post = false;     // split-K reductions fused into the GEMMs (gemm_post.cuh; measured slower)
-  float* sk_part = nullptr;   // stream-K segment partials (SwiGLU / lm_head GEMMs)
-  int* sk_flag = nullptr;
   int sampling = 0;           // temperature > 0: lm_head writes fp32 logits
   float inv_t = 1.f;
   uint64_t seed = 0;
@@ -133,9 +118,8 @@ struct ModelRT {
   int* att_cnt = nullptr;
   int* amax_i = nullptr;
   float2* rope = nullptr;
-  CUtensorMap tm_k{}, tm_v{};   // whole K / V cache as [L*slots*n_kv*ctx_cap][hd] rows
-  CUtensorMap tm_k32{}, tm_v32{};   // same, 32-key boxes (warp-per-item attention)
-  bool attn_warp = true;            // warp-per-item attention (SPECTRE_ATTN_WARP=0: CTA items)
+  CUtensorMap tm_k32{}, tm_v32{};   // whole K / V cache as [L*slots*n_kv*ctx_cap][hd] rows,
+                                    // 32-key boxes (warp-per-item attention)
   BatchDev bt{};
   std::vector<GemmPlan> pq, po, pgu, pd;
   GemmPlan plm{};
@@ -161,13 +145,6 @@ struct ModelRT {
     sp_qkv = pick_splits((nqkv() + tr_qkv - 1) / tr_qkv, d / 64, ctas);
     sp_o = pick_splits((d + tr_o - 1) / tr_o, qd / 64, ctas);
     sp_d = pick_splits((d + tr_d - 1) / tr_d, dm.ffn / 64, ctas);
-    if (half_gemm)
-      if (const char* v = getenv("SPECTRE_DRAFT_SPLIT_CAP")) {   // measured: caps 8/6/4 slower
-        const int cap = std::max(1, atoi(v));
-        sp_qkv = std::min(sp_qkv, cap);
-        sp_o = std::min(sp_o, cap);
-        sp_d = std::min(sp_d, cap);
-      }
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
     attn_chunk = attn_chunk_default(n_req * dm.n_kv_heads, ctx_cap);
     split_max = (ctx_cap + attn_chunk - 1) / attn_chunk;
@@ -191,9 +168,6 @@ struct ModelRT {
     amax_v = b.take<float>((size_t)n_blocks * R);
     amax_i = b.take<int>((size_t)n_blocks * R);
     rope = b.take<float2>((size_t)ctx_cap * dm.head_dim / 2);
-    sk_part = b.take<float>(gemm_sk_part_floats());
-    gbar = b.take<int>(2);
-    sk_flag = b.take<int>(gemm_sk_grid());
     bt.tok = b.take<int>(R);
     bt.pos = b.take<int>(R);
     bt.slot = b.take<int>(R);
@@ -221,23 +195,15 @@ struct ModelRT {
       // SwiGLU needs full K per tile: 128-row tiles when they fit one wave
       // (draft), else 256-row tiles (two accumulators share every X stage)
       const bool gu128 = (2 * F) / 128 <= gemm_sk_grid();
-      static const bool gu_sk = [] {   // stream-K SwiGLU (owner fix-up) for 256-row tiles
-        const char* v = getenv("SPECTRE_GU_SK");
-        return v && atoi(v) != 0;
-      }();
-      if (gu_sk && !gu128)
-        TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
-                      1, 0, 0, 256, sk_part, sk_flag));
-      else
-        TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
-                      1, 0, 0, gu128 ? 128 : 256));
+      TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
+                    1, 0, 0, gu128 ? 128 : 256));
       TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
                     0, 0, tr_d));
       static const bool gu_pair = [] {   // CTA pairs (cta_group::2) for the 256-row SwiGLU
         const char* v = getenv("SPECTRE_GU_PAIR");   // tiles: half the token tile per CTA,
         return v ? atoi(v) != 0 : true;              // measured 68.7 -> 66.4 us (bit-identical)
       }();
-      if (gu_pair && !gu128 && !half_gemm && !(gu_sk && !gu128) &&
+      if (gu_pair && !gu128 && !half_gemm &&
           (2 * F / 256) % 2 == 0 && 2 * F / 256 <= gemm_sk_grid())
         TRY(gemm_set_pair(&pgu[l]));
       if (half_gemm) {
@@ -253,67 +219,14 @@ struct ModelRT {
       TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kPartial, 1, 0, 0, 256));
       TRY(gemm_set_outputs(&plm, logits, nullptr, nullptr, nullptr, 0));
     } else {
-      // whole tiles per CTA (no stream-K): logits independent of the CTA budget
-      static const int lm_tile = [] {
-        const char* v = getenv("SPECTRE_LM_TILE");
-        return (v && atoi(v) == 128) ? 128 : 256;
-      }();
-      TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, lm_tile));
+      // whole 256-row tiles per CTA (no stream-K): logits independent of the
+      // CTA budget (128-row tiles measured neutral)
+      TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0, 256));
       TRY(gemm_set_outputs(&plm, nullptr, amax_v, amax_i, nullptr, 0));
     }
-    // each GEMM prefetches the next GEMM's weights into L2 (capped: the
-    // next kernel's working set must not push them out before use)
-    if (const char* v = getenv("SPECTRE_L2_PREFETCH_MB")) pf_cap = (long long)atoi(v) << 20;
-    auto link = [&](GemmPlan& p, const void* w, long long bytes) {
-      p.args.pf_ptr = pf_cap > 0 ? w : nullptr;
-      p.args.pf_bytes = std::min(bytes, pf_cap) & ~15ll;
-    };
-    if (const char* v = getenv("SPECTRE_FUSE_POST")) fuse_post = atoi(v) != 0;
-    if (fuse_post) {
-      const size_t kv_layer = (size_t)n_req * dm.n_kv_heads * ctx_cap * dm.head_dim;
-      auto* kc = reinterpret_cast<__nv_bfloat16*>(w.k_cache);
-      auto* vc = reinterpret_cast<__nv_bfloat16*>(w.v_cache);
-      for (int l = 0; l < L; ++l) {
-        GemmPost& r = pq[l].args.post;
-        r.kind = kPostRope;
-        r.gbar = gbar;
-        r.tok_pos = bt.pos;
-        r.tok_slot = bt.slot;
-        r.rope = rope;
-        r.q = q;
-        r.kc = kc + l * kv_layer;
-        r.vc = vc + l * kv_layer;
-        r.n_q = dm.n_q_heads;
-        r.n_kv = dm.n_kv_heads;
-        r.hd = dm.head_dim;
-        r.ctx_cap = ctx_cap;
-        for (int which = 0; which < 2; ++which) {
-          GemmPost& z = which == 0 ? po[l].args.post : pd[l].args.post;
-          z.kind = kPostResid;
-          z.gbar = gbar;
-          z.h = h;
-          z.x = x;
-          z.eps = dm.rms_eps;
-          z.w = which == 0 ? w.mlp_norm + (size_t)l * d
-                           : (l + 1 < L ? w.attn_norm + (size_t)(l + 1) * d : w.final_norm);
-        }
-      }
-    }
-    for (int l = 0; l < L; ++l) {
-      link(pq[l], bf(w.wo) + (size_t)l * d * qd, (long long)d * qd * 2);
-      link(po[l], bf(w.wgu) + (size_t)l * 2 * F * d, (long long)2 * F * d * 2);
-      link(pgu[l], bf(w.wd) + (size_t)l * d * F, (long long)d * F * 2);
-      if (l + 1 < L)
-        link(pd[l], bf(w.wqkv) + (size_t)(l + 1) * nqkv() * d, (long long)nqkv() * d * 2);
-      else
-        link(pd[l], w.lm_head, (long long)dm.vocab * d * 2);
-    }
     const uint64_t kv_rows = (uint64_t)L * n_req * dm.n_kv_heads * ctx_cap;
-    TRY(make_tmap_bf16(&tm_k, w.k_cache, dm.head_dim, kv_rows, 64, 64));
-    TRY(make_tmap_bf16(&tm_v, w.v_cache, dm.head_dim, kv_rows, 64, 64));
     TRY(make_tmap_bf16(&tm_k32, w.k_cache, dm.head_dim, kv_rows, 32, 64));
     TRY(make_tmap_bf16(&tm_v32, w.v_cache, dm.head_dim, kv_rows, 32, 64));
-    if (const char* v = getenv("SPECTRE_ATTN_WARP")) attn_warp = atoi(v) != 0;
     plm.args.t_dev = bt.t_dev;
     return SPECTRE_OK;
   }
@@ -355,23 +268,18 @@ struct ModelRT {
     TRY(launch_embed_rmsnorm(bt.tok, bt.t_dev, rows_cap, w.embed, w.attn_norm, h, x, d, eps, s));
     for (int l = 0; l < L; ++l) {
       TRY(gemm_run(pq[l], s));
-      const bool fused = fuse_post && !no_grid_sync_ref();
-      if (!fused)
-        TRY(launch_qkv_rope_kv(part, sp_qkv, rows_cap, bt.t_dev, rows_cap, bt.pos, bt.slot,
+      TRY(launch_qkv_rope_kv(part, sp_qkv, rows_cap, bt.t_dev, rows_cap, bt.pos, bt.slot,
                                rope, q, kc + l * kv_layer, vc + l * kv_layer, dm.n_q_heads,
                                dm.n_kv_heads, hd, ctx_cap, s));
       a.layer_row0 = l * n_req * dm.n_kv_heads * ctx_cap;
-      if (attn_warp) TRY(launch_attention_w(tm_k32, tm_v32, a, hd, rows, s));
-      else TRY(launch_attention(tm_k, tm_v, a, hd, rows, s));
+      TRY(launch_attention_w(tm_k32, tm_v32, a, hd, rows, s));
       TRY(gemm_run(po[l], s));
-      if (!fused)
-        TRY(launch_residual_rmsnorm(part, sp_o, rows_cap, bt.t_dev, rows_cap,
+      TRY(launch_residual_rmsnorm(part, sp_o, rows_cap, bt.t_dev, rows_cap,
                                     w.mlp_norm + (size_t)l * d, h, x, d, eps, s));
       TRY(gemm_run(pgu[l], s));
       TRY(gemm_run(pd[l], s));
       const float* next = (l + 1 < L) ? w.attn_norm + (size_t)(l + 1) * d : w.final_norm;
-      if (!fused)
-        TRY(launch_residual_rmsnorm(part, sp_d, rows_cap, bt.t_dev, rows_cap, next, h, x, d, eps,
+      TRY(launch_residual_rmsnorm(part, sp_d, rows_cap, bt.t_dev, rows_cap, next, h, x, d, eps,
                                     s));
     }
     if (!head) {
@@ -386,7 +294,7 @@ struct ModelRT {
         TRY(launch_sample_rows(logits, dm.vocab, bt.t_dev, rows_cap, bt.pos, bt.slot, inv_t, seed,
                                lstat, bt.out_tok, s));
     } else {
-      TRY(launch_argmax_reduce(amax_v, amax_i, cap_grid(plm.grid) * 8, rows_cap, bt.t_dev, rows_cap,
+      TRY(launch_argmax_reduce(amax_v, amax_i, (plm.grid) * 8, rows_cap, bt.t_dev, rows_cap,
                                bt.out_tok, nullptr, s));
     }
     if (out_x)
@@ -410,7 +318,6 @@ struct Engine {
   int graph_failed = 0;
   int* mode_host = nullptr;  // pinned
   int warmed = 0;
-  int par_draft_ctas = 0, par_target_ctas = 0;   // parallel-round CTA budgets (0: whole GPU)
   int device = 0;
   int attached = 0;           // layout-only view of a peer process's engine (IPC)
   cudaStream_t s_cap2 = nullptr;
@@ -538,8 +445,6 @@ struct Engine {
     st.sampling = c.temperature > 0.0 ? 1 : 0;
     st.breaker_threshold = c.breaker_threshold > 0 ? c.breaker_threshold : 3;
     st.breaker_cooldown = c.breaker_cooldown > 0 ? c.breaker_cooldown : 5;
-    if (const char* v = getenv("SPECTRE_PAR_DRAFT_CTAS")) par_draft_ctas = atoi(v);
-    if (const char* v = getenv("SPECTRE_PAR_TARGET_CTAS")) par_target_ctas = atoi(v);
     qwin = 4 * c.gamma + 4;   // > every candidate-to-speculation position gap
     for (ModelRT* m : {&tgt, &drf}) {
       m->sampling = st.sampling;
@@ -585,20 +490,14 @@ struct Engine {
     return SPECTRE_OK;
   }
 
-  // draft speculation on `sd` concurrent with the verify on `s`, disjoint CTA budgets
+  // draft speculation on `sd` concurrent with the verify on `s` (disjoint CTA
+  // budgets for the two measured slower: both phases share HBM bandwidth)
   int parallel_phase(cudaStream_t s, cudaStream_t sd) {
-    NoGridSyncGuard concurrent;   // draft and target kernels overlap on two streams
     SPECTRE_CUDA_TRY(cudaEventRecord(ev_fork, s));
     SPECTRE_CUDA_TRY(cudaStreamWaitEvent(sd, ev_fork, 0));
-    {
-      CtaCapGuard g(par_draft_ctas);
-      TRY(draft_phase('P', sd));
-    }
+    TRY(draft_phase('P', sd));
     SPECTRE_CUDA_TRY(cudaEventRecord(ev_join, sd));
-    {
-      CtaCapGuard g(par_target_ctas);
-      TRY(verify_phase(s));
-    }
+    TRY(verify_phase(s));
     SPECTRE_CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
     return SPECTRE_OK;
   }

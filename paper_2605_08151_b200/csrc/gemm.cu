@@ -114,10 +114,8 @@ static int launch_one(const GemmPlan& p, cudaStream_t s) {
                                           Cfg::kSmem));
     configured = true;
   }
-  if (p.args.stream_k && cap_grid(p.grid) != p.grid)
-    return arg_fail("gemm: stream-K plans need the whole grid");
   if (kPair) {
-    if (kHalf || cap_grid(p.grid) != p.grid) return arg_fail("gemm: pair plans need the whole grid");
+    if (kHalf) return arg_fail("gemm: pair plans use the full config");
     if (getenv("SPECTRE_GEMM_PAIR_DBG")) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(p.grid);
@@ -143,7 +141,7 @@ static int launch_one(const GemmPlan& p, cudaStream_t s) {
     }
     return SPECTRE_OK;
   }
-  SPECTRE_LAUNCH_PDL("gemm_bf16_swapab", kern, dim3(cap_grid(p.grid)), dim3(Cfg::kThreads),
+  SPECTRE_LAUNCH_PDL("gemm_bf16_swapab", kern, dim3(p.grid), dim3(Cfg::kThreads),
                      Cfg::kSmem, s, p.tmap_w, p.tmap_x, p.tmap_out, p.tmap_sk, p.args);
   return SPECTRE_OK;
 }
@@ -154,7 +152,7 @@ static int num_sms();
 // 256-row tile (full K), the grid is an even number of CTAs in clusters of 2.
 int gemm_set_pair(GemmPlan* p) {
   if (p->half || p->bk != 64 || p->epi != kSwiGLU || p->args.tile_rows != 256 || p->args.splits != 1 ||
-      p->args.stream_k || p->args.post.kind != kPostNone || p->n_tiles % 2 ||
+      p->args.stream_k || p->n_tiles % 2 ||
       p->n_tiles > num_sms())
     return arg_fail("gemm_set_pair: one 256-row tile per CTA, BK 64, no split / stream-K");
   p->grid = p->n_tiles;
@@ -220,14 +218,6 @@ int gemm_plan(GemmPlan* p, const void* W, int N, int K, const void* X, int rows_
   return SPECTRE_OK;
 }
 
-static int l2_ahead_default() {
-  static const int v = [] {
-    const char* e = getenv("SPECTRE_GEMM_L2_AHEAD");   // k-steps; 0 = off
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 static int ksub_env() {
   static const int v = [] {
     const char* e = getenv("SPECTRE_GEMM_KSUB");   // k blocks per stage override (1 / 2)
@@ -243,17 +233,11 @@ int gemm_run(const GemmPlan& p0, cudaStream_t s) {
     const char* e = getenv("SPECTRE_GEMM_KSUBMAX");
     return e ? atoi(e) : 0;
   }();
-  if (l2_ahead_default() != p0.args.l2_ahead || (ksub_env() && ksub_env() != p0.args.ksub) ||
+  if ((ksub_env() && ksub_env() != p0.args.ksub) ||
       (ksub_max_env && ksub_max_env != p0.args.ksub_max)) {
     stripped = p0;
-    stripped.args.l2_ahead = l2_ahead_default();
     if (ksub_env()) stripped.args.ksub = ksub_env();
     if (ksub_max_env) stripped.args.ksub_max = ksub_max_env;
-    pp = &stripped;
-  }
-  if (p0.args.post.kind != kPostNone && no_grid_sync_ref()) {   // concurrent: no grid barrier
-    if (pp != &stripped) stripped = p0;
-    stripped.args.post.kind = kPostNone;
     pp = &stripped;
   }
   const GemmPlan& p = *pp;

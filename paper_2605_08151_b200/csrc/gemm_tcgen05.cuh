@@ -42,7 +42,6 @@
 #include <cstdint>
 
 #include "common.cuh"
-#include "gemm_post.cuh"
 #include "ptx.cuh"
 
 namespace spectre {
@@ -92,10 +91,6 @@ struct GemmArgs {
   int* sk_flag;             // stream-K: [grid] segment-ready flags (self-resetting)
   unsigned long long* dbg;  // diagnostics: per-CTA [8] globaltimer stamps (nullptr: off)
   int diag;                 // diagnostics (timing only): 1 skip MMAs, 2 skip epilogue math
-  const void* pf_ptr;       // next GEMM's weights: prefetched into L2 while this one runs
-  long long pf_bytes;       //   (static data, so issued before griddepcontrol.wait)
-  GemmPost post;            // fused split-K reduction phase (gemm_post.cuh)
-  int l2_ahead;             // producer L2-prefetches weight boxes this many k-steps ahead
   int ksub;                 // 1: one BK block per stage; 0: two when >= 2 such stages fit
   int ksub_max;             // most BK blocks per stage (0: 4)
   int pair;                 // launched as CTA pairs (cluster 2): M=256 cta_group::2 MMAs
@@ -285,7 +280,9 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tmem_full[b], 1);
-      mbar_init(&tmem_empty[b], kEpiThreads);
+      // pair: both CTAs' epilogues arrive on the leader's barrier (the leader
+      // issues every MMA into both TMEMs)
+      mbar_init(&tmem_empty[b], (kPair && pair) ? 2 * kEpiThreads : kEpiThreads);
     }
     fence_barrier_init();
   }
@@ -300,25 +297,12 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   const uint32_t tmem_base = *tmem_slot;
 
   const bool producer = (warp == 0 && lane == 0);
-  if (a.pf_ptr && a.pf_bytes > 0 && warp >= 2) {
-    // this CTA's share of the next GEMM's weights, one bulk prefetch per thread
-    const long long share = (a.pf_bytes / gridDim.x + 4095) & ~4095ll;
-    const long long c0 = share * blockIdx.x;
-    const long long per = (share / kEpiThreads + 15) & ~15ll;
-    const long long b0 = c0 + per * (threadIdx.x - 64);
-    const long long b1 = min(min(b0 + per, c0 + share), a.pf_bytes);
-    if (b1 > b0)
-      prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(a.pf_ptr) + b0, (uint32_t)(b1 - b0));
-  }
   if (!producer) {  // everyone but the TMA lane waits for the previous kernel now
     pdl_wait();
     pdl_trigger();
   }
   GemmSched sched;
   sched.init(a, T, BK, Cfg::kPass);
-  // pair mode: the leader's issuer waits only on its own tmem_empty, so a
-  // pair CTA may own at most one job (gemm_set_pair: one tile per CTA)
-  if (kPair && pair && sched.n_tiles * sched.splits > sched.G) __trap();
   if (a.dbg && threadIdx.x == 64) a.dbg[blockIdx.x * 8 + 0] = gtimer();
   const bool no_work = (T == 0);
 
@@ -380,11 +364,6 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
           const int s = g % stages;
           const int nk = min(ksub, j.k1 - k);
           uint8_t* st = pipe + s * stage_bytes;
-          // L2 prefetch one ring ahead: the smem ring then refills from L2
-          // instead of waiting a full HBM round trip per slot
-          if (a.l2_ahead > 0 && k + a.l2_ahead < j.k1)
-            for (int b = 0; b < j.boxes; ++b)
-              tma_prefetch_2d(&tmap_w, (k + a.l2_ahead) * BK, n0 + b * 128);
           if (g >= pre) {
             if (g >= stages) {
               const long long t_w = a.stall ? clock64() : 0;
@@ -713,7 +692,12 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       }
       if (a.dbg && etid == 0 && jn < 5) a.dbg[blockIdx.x * 8 + 1 + jn] = gtimer() | ((unsigned long long)j.role << 62);
       tc_fence_before();
-      mbar_arrive(&tmem_empty[buf]);
+      if (kPair && pair) {
+        if (leader) mbar_arrive(&tmem_empty[buf]);
+        else mbar_arrive_cluster(mapa_shared(&tmem_empty[buf], 0));
+      } else {
+        mbar_arrive(&tmem_empty[buf]);
+      }
       if (j.role == 2) {
         // make the segment partial visible, then flag it (one thread, after all 256)
         if (issuer) {
@@ -752,14 +736,6 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   }
   tc_fence_before();
   __syncthreads();
-  if (kEpi == kPartial && a.post.kind != kPostNone) {
-    // every CTA's partials are in global memory: reduce them in this grid
-    // 40 floats in the (dynamic) barrier area, past the mbarriers and the TMEM slot
-    float* post_sh = reinterpret_cast<float*>(smem + kPipeB + kStageOutB + 512);
-    post_grid_sync(a.post.gbar);
-    if (a.post.kind == kPostRope) post_rope(a.post, a.part, a.splits, a.rows_cap, T);
-    else post_resid(a.post, a.part, a.splits, a.rows_cap, T, a.N, post_sh);
-  }
   if (kPair) cluster_sync();   // the leader's MMAs and both epilogues are done with both TMEMs
   if (warp == 1) {
     tc_fence_after();

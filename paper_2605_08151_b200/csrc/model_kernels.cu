@@ -492,7 +492,7 @@ static int resid_ctas_per_sm() {
 }
 int launch_embed_rmsnorm(const int* tok, const int* t_dev, int t_cap, const void* E,
                          const float* w, float* h, void* x, int d, float eps, cudaStream_t s) {
-  SPECTRE_LAUNCH_PDL("k_embed_rmsnorm", k_embed_rmsnorm, dim3(cap_grid(std::min(t_cap, 2 * kSms))), dim3(256), 0, s, tok, t_dev,
+  SPECTRE_LAUNCH_PDL("k_embed_rmsnorm", k_embed_rmsnorm, dim3((std::min(t_cap, 2 * kSms))), dim3(256), 0, s, tok, t_dev,
                      reinterpret_cast<const __nv_bfloat16*>(E), w, h,
                      reinterpret_cast<__nv_bfloat16*>(x), d, eps);
   return SPECTRE_OK;
@@ -514,7 +514,7 @@ int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const i
   const int threads = nv < 512 ? ((nv + 31) / 32) * 32 : 512;
   const int vec = (nv + threads - 1) / threads;
   auto* xb = reinterpret_cast<__nv_bfloat16*>(x);
-  const dim3 grid(cap_grid(std::min(t_cap, resid_ctas_per_sm() * kSms)));
+  const dim3 grid((std::min(t_cap, resid_ctas_per_sm() * kSms)));
   if (vec <= 1)
     SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<1>, grid, dim3(threads),
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
@@ -546,7 +546,7 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
     const int quads = pairs / 4;
     if (splits <= 4)
       SPECTRE_LAUNCH_PDL("k_qkv_rope_kv4", k_qkv_rope_kv4<4>,
-                       dim3(cap_grid(std::min(t_cap * ((quads + 127) / 128),
+                       dim3((std::min(t_cap * ((quads + 127) / 128),
                                               (rope_ctas_per_sm() ? rope_ctas_per_sm() : 8) * kSms))),
                        dim3(128), 0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
                        reinterpret_cast<const float2*>(rope), reinterpret_cast<__nv_bfloat16*>(q),
@@ -554,7 +554,7 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
                        n_q, n_kv, hd, ctx_cap);
     else
       SPECTRE_LAUNCH_PDL("k_qkv_rope_kv4", k_qkv_rope_kv4<kMaxSplits>,
-                       dim3(cap_grid(std::min(t_cap * ((quads + 127) / 128),
+                       dim3((std::min(t_cap * ((quads + 127) / 128),
                                               (rope_ctas_per_sm() ? rope_ctas_per_sm() : 8) * kSms))),
                        dim3(128), 0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
                        reinterpret_cast<const float2*>(rope), reinterpret_cast<__nv_bfloat16*>(q),
@@ -563,7 +563,7 @@ int launch_qkv_rope_kv(const float* part, int splits, int rows_cap, const int* t
     return SPECTRE_OK;
   }
   SPECTRE_LAUNCH_PDL("k_qkv_rope_kv", k_qkv_rope_kv,
-                     dim3(cap_grid(std::min(t_cap * ((pairs + 127) / 128),
+                     dim3((std::min(t_cap * ((pairs + 127) / 128),
                                             (rope_ctas_per_sm() ? rope_ctas_per_sm() : 24) * kSms))),
                      dim3(128),
                      0, s, part, splits, rows_cap, t_dev, tok_pos, tok_slot,
@@ -582,11 +582,11 @@ int launch_argmax_reduce(const float* val, const int* idx, int n_tiles, int rows
   }();
   if (rows) {
     SPECTRE_LAUNCH_PDL("k_argmax_reduce_rows", k_argmax_reduce_rows,
-                       dim3(cap_grid(std::min((t_cap + 31) / 32, kSms))), dim3(1024), 0, s, val,
+                       dim3((std::min((t_cap + 31) / 32, kSms))), dim3(1024), 0, s, val,
                        idx, n_tiles, rows_cap, t_dev, out_tok, out_val);
     return SPECTRE_OK;
   }
-  SPECTRE_LAUNCH_PDL("k_argmax_reduce", k_argmax_reduce, dim3(cap_grid(std::min(t_cap, 2 * kSms))), dim3(256), 0, s, val, idx,
+  SPECTRE_LAUNCH_PDL("k_argmax_reduce", k_argmax_reduce, dim3((std::min(t_cap, 2 * kSms))), dim3(256), 0, s, val, idx,
                      n_tiles, rows_cap, t_dev, out_tok, out_val);
   return SPECTRE_OK;
 }

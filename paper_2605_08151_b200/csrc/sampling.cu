@@ -221,8 +221,37 @@ __global__ void __launch_bounds__(kSampThreads) k_accept_sample(
   const float* lp = logits + (size_t)(row0 + a) * V;
   const float2 ts = tstat[row0 + a];
   const double u2 = u53s(mix64(s.seed, kStreamResample, (uint64_t)b, (uint64_t)(pos + a)));
+  // Parallel rounds: the draft's fresh speculation starts AT the bonus position
+  // (its head token is a proposal for the token this round emits).  It goes
+  // through the same min(1, p/q) test instead of being matched against an
+  // independently sampled bonus (probability sum_x p(x) q(x), ~0 at V = 128k);
+  // accepted, it is the bonus and the rest of the segment stays cached;
+  // rejected, the bonus is drawn from norm(max(0, p - q)) — whose weight at the
+  // head token is 0, so k_accept's reuse rule (head == bonus) then discards the
+  // segment.  The emitted token is distributed as p either way.
+  bool head = false;
+  if (a == m) {
+    const bool fresh = s.r_serial[b] == s.q_serial[b] && s.r_round[b] == s.q_round[b];
+    if (s.ctrl->mode == 'P' && fresh && s.gen_count[b] > 0 && s.gen_done[b] > 0 &&
+        s.gen_start[b] == pos + a) {
+      const int x = (int)s.hist[(size_t)b * s.hist_cap + s.gen_start[b]];
+      const float p = __expf(lp[x] * inv_t - ts.x) / ts.y;
+      const int slot = (pos + a) % W;
+      const float2 qs = qstat[b * W + slot];
+      const float q = __expf(qstore[((size_t)b * W + slot) * V + x] * inv_t - qs.x) / qs.y;
+      const double u = u53s(mix64(s.seed, kStreamAccept, (uint64_t)b, (uint64_t)(pos + a)));
+      if (u * (double)q < (double)p) {
+        if (threadIdx.x == 0) {
+          out_a[b] = a;
+          out_bonus[b] = x;
+        }
+        return;
+      }
+      head = true;   // rejected: residual resample against the head's q
+    }
+  }
   int y;
-  if (a < m) {   // resample from norm(max(0, p - q)) at the rejected position
+  if (a < m || head) {   // resample from norm(max(0, p - q)) at the rejected position
     const int slot = (pos + a) % W;
     const float* lq = qstore + ((size_t)b * W + slot) * V;
     const float2 qs = qstat[b * W + slot];
@@ -258,7 +287,7 @@ __global__ void __launch_bounds__(kSampThreads) k_accept_sample(
 int launch_sample_rows(const float* logits, int V, const int* t_dev, int t_cap,
                        const int* tok_pos, const int* tok_slot, float inv_t, uint64_t seed,
                        float2* stats, int* out_tok, cudaStream_t s) {
-  SPECTRE_LAUNCH_PDL("k_sample_rows", k_sample_rows, dim3(cap_grid(t_cap < 296 ? t_cap : 296)),
+  SPECTRE_LAUNCH_PDL("k_sample_rows", k_sample_rows, dim3((t_cap < 296 ? t_cap : 296)),
                      dim3(kSampThreads), 0, s, logits, V, t_dev, tok_pos, tok_slot, inv_t, seed,
                      stats, out_tok);
   return SPECTRE_OK;

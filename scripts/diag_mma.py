@@ -8,7 +8,8 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch  # noqa: F401
 from paper_2605_08151_b200 import _native
-L = _native.lib()
+from diagnostics import lib as _diag_lib  # noqa: E402
+L = _diag_lib()
 L.spectre_diag_mma.argtypes = [C.c_int32] * 5 + [C.POINTER(C.c_uint64), C.c_void_p]
 for n in (64, 256):
     for nmma in (1, 4, 8, 16):

@@ -7,7 +7,8 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch
 from paper_2605_08151_b200 import _native
-L = _native.lib()
+from diagnostics import lib as _diag_lib  # noqa: E402
+L = _diag_lib()
 K = 4096
 buf = torch.empty(4 << 30, dtype=torch.uint8, device="cuda")
 X = torch.randn(256, K, device="cuda").bfloat16()

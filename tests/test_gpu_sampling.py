@@ -39,9 +39,16 @@ def _copy_target_into_draft(pair):
 
 
 def test_sampling_is_deterministic(M):
+    """Same seed, same stream.  The committed stream at T > 0 depends on the
+    round modes (a parallel round proposes a token where an ordinary round
+    samples the bonus), so this uses the reference controller, whose mode
+    sequence is a function of the protocol state alone; the measured-time
+    controllers choose modes from device timers (distributionally lossless
+    either way: the PIT tests)."""
     import torch
     pair = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=8, ctx_cap=256, seed=4)
-    spec = M.DecodeSpec(n_req=8, gamma=4, output_len=48, prompt_len=16, seed=4, temperature=1.0)
+    spec = M.DecodeSpec(n_req=8, gamma=4, output_len=48, prompt_len=16, seed=4, temperature=1.0,
+                        controller="reference")
     a = M.decode(pair, spec, "hybrid")
     b = M.decode(pair, spec, "hybrid")
     assert (a.committed_pos == spec.output_len).all()
@@ -96,3 +103,43 @@ def test_committed_tokens_follow_target_distribution(M, variant):
     if variant != "ar":
         # the draft is a different model: rejections and resamples really happen
         assert res.report.content_mean_accepted_length < spec.gamma
+
+
+def test_parallel_head_token_is_rejection_sampled(M):
+    """Parallel rounds: the draft's speculation starts at the bonus position, and
+    its head token is accepted with min(1, p/q) (not exact-matched against an
+    independently sampled bonus).  With the draft identical to the target,
+    p == q, so every head is accepted: after the switch-over round no request
+    is ever PADDED again and every round commits gamma tokens per request."""
+    pair = M.build_pair(M.TINY_TARGET, M.TINY_TARGET, n_req=8, ctx_cap=256, seed=6)
+    _copy_target_into_draft(pair)
+    spec = M.DecodeSpec(n_req=8, gamma=4, output_len=64, prompt_len=16, seed=6, temperature=1.0)
+    res = M.decode(pair, spec, "parallel")
+    tr = res.trace
+    assert tr["n_padded"][0] == spec.n_req          # the switch-over round
+    assert tr["n_padded"][1:].sum() == 0
+    assert res.report.mean_accepted_length > spec.gamma - 0.5
+
+
+
+
+@pytest.mark.parametrize("variant", ["ar", "parallel", "hybrid"])
+def test_committed_tokens_follow_target_distribution_128k_vocab(M, variant):
+    """The PIT test at the headline vocabulary (V = 128,256): the sampler's
+    fp32 chunked inverse CDF over 128k entries, the residual resample and the
+    parallel head-token test are exact in distribution at full width."""
+    import dataclasses
+
+    from scipy import stats
+    tgt = dataclasses.replace(M.SMALL_TARGET, name="small-128k", vocab=128256)
+    drf = dataclasses.replace(M.SMALL_DRAFT, name="small-draft-128k", vocab=128256)
+    n = 64
+    pair = M.build_pair(tgt, drf, n_req=n, ctx_cap=128, seed=12, target_branch=1.0,
+                        draft_branch=0.5)
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=K_TOKENS + 8, prompt_len=12, seed=12,
+                        temperature=1.0)
+    res = M.decode(pair, spec, variant)
+    assert (res.committed_pos == spec.output_len).all()
+    pit = _pit_values(M, pair, spec, res, np.random.default_rng(1))
+    p = stats.kstest(pit, "uniform").pvalue
+    assert p > KS_PVALUE, (variant, p)
