@@ -240,6 +240,11 @@ typedef struct SpectreDecodeConfig {
                                  missing draft reply disable speculation ... */
   int32_t breaker_cooldown;   /* ... for this many rounds.  <= 0: defaults 3 / 5
                                  (core.py:93-94) */
+  int32_t draft_prompt_keep;  /* draft prompt compression (draft_engine.py:123-131,
+                                 StreamingLLM head/tail retention): the draft model
+                                 sees only the first and the last `keep` prompt
+                                 tokens, re-indexed to positions 0 .. 2 keep - 1;
+                                 0 (or 2 keep >= prompt_len): the whole prompt */
 } SpectreDecodeConfig;
 
 #define SPECTRE_ROLE_BOTH 0

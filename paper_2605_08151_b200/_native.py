@@ -112,7 +112,7 @@ class DecodeConfig(C.Structure):
                 ("t_target", C.c_double), ("t_draft", C.c_double), ("ema_decay", C.c_double),
                 ("fixed_threshold_l", C.c_double), ("temperature", C.c_double),
                 ("role", C.c_int32), ("breaker_threshold", C.c_int32),
-                ("breaker_cooldown", C.c_int32)]
+                ("breaker_cooldown", C.c_int32), ("draft_prompt_keep", C.c_int32)]
 
 
 TRACE_FIELDS = ("mode", "participants", "delta", "n_roll", "content_sum", "content_n",

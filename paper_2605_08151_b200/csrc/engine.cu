@@ -325,6 +325,7 @@ struct Engine {
   int qwin = 0;               // slots per request (positions mod qwin)
   float* qstore = nullptr;    // [n_req][qwin][vocab] draft logits
   float2* qstat = nullptr;    // [n_req][qwin] (max, sum exp)
+  int* dprompts = nullptr;    // [n_req][dprompt_len] compressed prompts (draft side)
 
   ~Engine() {
     if (exec_loop) cudaGraphExecDestroy(exec_loop);
@@ -376,6 +377,7 @@ struct Engine {
     st.hist = b.take<uint64_t>((size_t)n * st.hist_cap);
     st.cached_tok = b.take<uint64_t>((size_t)n * G);
     st.cand_tok = b.take<uint64_t>((size_t)n * G);
+    if (st.dprompt_len < cfg.prompt_len) dprompts = b.take<int>((size_t)n * st.dprompt_len);
     st.ctrl = b.take<CtrlDev>(1);
     const int R = cfg.max_rounds;
     st.trace.mode = b.take<int>(R);
@@ -428,6 +430,8 @@ struct Engine {
     st.gamma = c.gamma;
     st.out_len = c.output_len;
     st.prompt_len = c.prompt_len;
+    st.dprompt_len = (c.draft_prompt_keep > 0 && 2 * c.draft_prompt_keep < c.prompt_len)
+                         ? 2 * c.draft_prompt_keep : c.prompt_len;
     st.vocab = d.vocab;
     st.variant = c.variant;
     st.controller = c.controller;
@@ -717,13 +721,22 @@ extern "C" int spectre_engine_prefill(void* engine, const int32_t* prompts, void
   auto* e = reinterpret_cast<Engine*>(engine);
   if (!e || !prompts || e->attached) return arg_fail("spectre_engine_prefill");
   cudaStream_t s = as_stream(stream);
-  const int P = e->cfg.prompt_len, cs = e->prefill_cs;
+  const int cs = e->prefill_cs;
   for (ModelRT* m : {&e->drf, &e->tgt}) {
     if ((m == &e->drf && e->cfg.role == SPECTRE_ROLE_TARGET) ||
         (m == &e->tgt && e->cfg.role == SPECTRE_ROLE_DRAFT))
       continue;   // disaggregated: this side holds only one model
+    // the draft prefills its (possibly compressed) prompt view
+    const int* src = prompts;
+    int P = e->cfg.prompt_len;
+    if (m == &e->drf && e->dprompts) {
+      TRY(launch_compress_prompts(prompts, P, e->cfg.draft_prompt_keep, e->cfg.n_req, e->dprompts,
+                                  s));
+      src = e->dprompts;
+      P = e->st.dprompt_len;
+    }
     for (int c0 = 0; c0 < P; c0 += cs) {
-      TRY(launch_prefill_batch(prompts, P, e->cfg.n_req, c0, cs, m->bt, s));
+      TRY(launch_prefill_batch(src, P, e->cfg.n_req, c0, cs, m->bt, s));
       // only the target's prediction at the last prompt position is read
       // (admission commits it as output token 0)
       TRY(m->forward(cs, s, nullptr, true, m == &e->tgt && c0 + cs >= P));

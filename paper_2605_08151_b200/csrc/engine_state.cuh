@@ -68,6 +68,7 @@ struct RoundTraceDev {
 
 struct DecodeStateDev {
   int n_req, gamma, out_len, prompt_len, vocab, variant, controller, r_kind, max_rounds;
+  int dprompt_len;   // prompt tokens the draft model sees (compression, draft_engine.py:123-131)
   int has_fixed_l;
   int hist_cap;      // draft history capacity (output positions)
   uint64_t seed;
@@ -109,6 +110,8 @@ struct DecodeStateDev {
 };
 
 // launchers (model_protocol.cu)
+int launch_compress_prompts(const int* prompts, int P, int keep, int n_req, int* out,
+                            cudaStream_t s);
 int launch_prefill_batch(const int* prompts, int prompt_len, int n_req, int c0, int cs,
                          const BatchDev& bt, cudaStream_t s);
 int launch_admit(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);

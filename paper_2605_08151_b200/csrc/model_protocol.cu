@@ -271,11 +271,11 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_prep(DecodeStateDev s, 
   if (b < s.n_req) {
     bt.q_off[b] = off;
     bt.n_new[b] = n_new;
-    bt.pos0[b] = s.prompt_len + kvd;
+    bt.pos0[b] = s.dprompt_len + kvd;
     const uint64_t* h = s.hist + (size_t)b * s.hist_cap;
     for (int j = 0; j < n_new; ++j) {
       bt.tok[off + j] = (int)h[kvd + j];
-      bt.pos[off + j] = s.prompt_len + kvd + j;
+      bt.pos[off + j] = s.dprompt_len + kvd + j;
       bt.slot[off + j] = b;
     }
   }
@@ -316,10 +316,10 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_append(DecodeStateDev s
     bt.q_off[b] = off;
     bt.n_new[b] = n_new;
     const int hl = s.hist_len[b];
-    bt.pos0[b] = s.prompt_len + hl - 1;
+    bt.pos0[b] = s.dprompt_len + hl - 1;
     if (n_new) {
       bt.tok[off] = (int)s.hist[(size_t)b * s.hist_cap + hl - 1];
-      bt.pos[off] = s.prompt_len + hl - 1;
+      bt.pos[off] = s.dprompt_len + hl - 1;
       bt.slot[off] = b;
     }
   }
@@ -607,6 +607,24 @@ int launch_set_round_limit(const DecodeStateDev& st, int extra, cudaStream_t s) 
   SPECTRE_LAUNCH_PDL("k_set_round_limit", k_set_round_limit, dim3(1), dim3(1), 0, s, st, extra);
   return SPECTRE_OK;
 }
+// Draft prompt compression (draft_engine.py:123-131): keep the first and the
+// last `keep` tokens of every prompt, contiguous (StreamingLLM-style re-indexing).
+__global__ void k_compress_prompts(const int* __restrict__ prompts, int P, int keep, int n_req,
+                                   int* __restrict__ out) {
+  const int Pd = 2 * keep;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_req * Pd; i += gridDim.x * blockDim.x) {
+    const int b = i / Pd, j = i % Pd;
+    out[i] = prompts[(size_t)b * P + (j < keep ? j : P - Pd + j)];
+  }
+}
+
+int launch_compress_prompts(const int* prompts, int P, int keep, int n_req, int* out,
+                            cudaStream_t s) {
+  k_compress_prompts<<<(n_req * 2 * keep + 255) / 256, 256, 0, s>>>(prompts, P, keep, n_req, out);
+  SPECTRE_LAUNCH_CHECK("k_compress_prompts");
+  return SPECTRE_OK;
+}
+
 int launch_prefill_batch(const int* prompts, int prompt_len, int n_req, int c0, int cs,
                          const BatchDev& bt, cudaStream_t s) {
   SPECTRE_LAUNCH_PDL("k_prefill_batch", k_prefill_batch, dim3((n_req + 255) / 256), dim3(256), 0, s,

@@ -184,6 +184,21 @@ class DecodeSpec:
     temperature: float = 0.0        # 0: greedy; > 0: speculative rejection sampling (config 3)
     breaker_threshold: int = 3      # circuit breaker (core.py:93-94, target_engine.py:337-380)
     breaker_cooldown: int = 5
+    compression_p: float = 1.0      # draft prompt compression (core.py compression_p,
+                                    # draft_engine.py:123-131): keep floor(p*S/2) head and
+                                    # tail prompt tokens in the draft's KV cache
+
+    def draft_prompt_keep(self) -> int:
+        """compress_prompt (draft_engine.py:123-131): keep = int((p / 2) * S); no
+        compression when 2 * keep >= S."""
+        if not 0.0 <= self.compression_p <= 1.0:
+            raise ValueError(f"compression_p must be in [0, 1], got {self.compression_p}")
+        keep = int((self.compression_p / 2.0) * self.prompt_len)
+        if 2 * keep >= self.prompt_len:
+            return 0
+        if keep == 0:
+            raise ValueError("compression_p keeps no prompt token for the draft")
+        return keep
 
     def __post_init__(self):
         if self.temperature > 0 and self.alpha < 1.0:
@@ -228,7 +243,8 @@ class SpectreEngine:
             fixed_threshold_l=float(spec.fixed_threshold_l or 0.0),
             temperature=float(spec.temperature), role=ROLES[role],
             breaker_threshold=int(spec.breaker_threshold),
-            breaker_cooldown=int(spec.breaker_cooldown))
+            breaker_cooldown=int(spec.breaker_cooldown),
+            draft_prompt_keep=spec.draft_prompt_keep())
         self.role = role
         self._tdims = pair.target.spec.dims()
         self._ddims = pair.draft.spec.dims()

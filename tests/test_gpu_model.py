@@ -181,3 +181,45 @@ def test_long_context_batch_invariance(M, which, attn_split, monkeypatch):
         tok, x = _forward_chunks(eng, which, prompts, chunk)
         assert torch.equal(tok, ref_tok), chunk
         assert torch.equal(x, ref_x), chunk
+
+
+def test_draft_prompt_compression_kv_and_losslessness(M):
+    """Model-mode draft prompt compression (draft_engine.py:123-131, StreamingLLM
+    head/tail retention): the draft's KV cache after prefill is exactly that of
+    the compressed prompt (first and last keep tokens, re-indexed to positions
+    0 .. 2 keep - 1), the target is untouched, and speculative decoding stays
+    lossless."""
+    import torch
+    n, P = 8, 40
+    pair = M.build_pair(M.SMALL_TARGET, M.SMALL_DRAFT, n_req=n, ctx_cap=256, seed=17)
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=64, prompt_len=P, seed=17,
+                        compression_p=0.5)
+    keep = spec.draft_prompt_keep()
+    assert keep == 10
+    prompts = M.synthetic_prompts(n, P, M.SMALL_TARGET.vocab, seed=17)
+    eng = M.SpectreEngine(pair, spec, "ordinary")
+    eng.prefill(prompts)
+    torch.cuda.synchronize()
+    kd = pair.draft.k_cache[:, :, :, :2 * keep].clone()
+    vd = pair.draft.v_cache[:, :, :, :2 * keep].clone()
+    kt = pair.target.k_cache[:, :, :, :P].clone()
+    eng.close()
+    comp = torch.cat([prompts[:, :keep], prompts[:, P - keep:]], 1).contiguous()
+    ref_spec = M.DecodeSpec(n_req=n, gamma=4, output_len=64, prompt_len=2 * keep, seed=17)
+    ref = M.SpectreEngine(pair, ref_spec, "ordinary")
+    ref.prefill(comp)
+    torch.cuda.synchronize()
+    assert torch.equal(pair.draft.k_cache[:, :, :, :2 * keep], kd)
+    assert torch.equal(pair.draft.v_cache[:, :, :, :2 * keep], vd)
+    ref.close()
+    # the target saw the whole prompt
+    full = M.SpectreEngine(pair, M.DecodeSpec(n_req=n, gamma=4, output_len=64, prompt_len=P,
+                                              seed=17), "ordinary")
+    full.prefill(prompts)
+    torch.cuda.synchronize()
+    assert torch.equal(pair.target.k_cache[:, :, :, :P], kt)
+    full.close()
+    ar = M.decode(pair, spec, "ar", prompts=prompts)
+    for v in ("ordinary", "parallel", "hybrid"):
+        got = M.decode(pair, spec, v, prompts=prompts)
+        assert torch.equal(got.committed, ar.committed), v
