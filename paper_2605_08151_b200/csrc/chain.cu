@@ -1,0 +1,663 @@
+// chain.cu — the draft model's decode step as few persistent launches.
+//
+// Everything between two attention launches of the draft runs as ONE kernel
+// ("chain"): o-projection -> residual + RMSNorm -> gate/up + SwiGLU -> down ->
+// residual + RMSNorm -> next layer's q/k/v -> RoPE + KV write (the first chain
+// of a step starts with embedding + RMSNorm, the last one ends at the final
+// norm).  Per layer that is 2 launches (chain + attention) instead of 8.
+//
+// Why: at the draft's decode shape (T = B = 64 tokens) every weight-streaming
+// GEMM launch costs ~5 us of body (weights at ~5.3 TB/s, then the epilogue)
+// plus ~5 us of launch / drain (scripts/time_draft_gemms.py: back-to-back
+// split-K launches run at 10.7-13.5 us for 8-34 MB), and the glue kernels add
+// their own turnovers.  Inside a chain the weight stream never stops: weights
+// are static, so the TMA producer warp walks ALL of the chain's GEMM jobs
+// ahead of the math, limited only by its shared-memory ring; only the
+// activation loads wait for the phase barrier that publishes their producer's
+// output.
+//
+// One CTA per SM (grid = SMs, all co-resident), 12 warps:
+//   warp 0  weight producer (TMA, evict-first), runs across phase boundaries
+//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer
+//   warp 2  activation producer (TMA), waits on the phase barriers
+//   warps 4-11  epilogue (tcgen05.ld -> split-K partial / SwiGLU stores) and
+//           the glue phases (residual + RMSNorm, RoPE, embedding) in between
+// Phase barrier: one monotonic arrival counter per chain launch (each CTA
+// arrives once per phase after its results are globally visible; the last
+// arrival of the last phase resets it for the next launch).
+//
+// Arithmetic: GEMMs are 128-row weight tiles, K split into fixed ranges that
+// depend only on (N, K, splits) — never on T — and the reductions (split sum in
+// split order, per-row RMS over a fixed tree) are per row, so every token's
+// result is independent of the batch composition (batch invariance).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "chain.h"
+#include "common.cuh"
+#include "gemm.h"
+#include "model_kernels.cuh"
+#include "ptx.cuh"
+
+namespace spectre {
+
+#define CHAIN_TRY(x)             \
+  do {                           \
+    if (int _r = (x)) return _r; \
+  } while (0)
+
+constexpr int kChainThreads = 384;
+constexpr int kChainEpiThreads = 256;          // warps 4..11
+constexpr int kChainMaxPhases = 8;
+constexpr int kChainWStages = 8;               // 16 KB weight boxes (128 rows x 64 k)
+constexpr int kChainXStages = 4;               // up to 128 tokens x 64 k (16 KB)
+constexpr int kChainPass = 128;                // tokens per MMA pass
+constexpr int kChainWBox = 128 * 128;
+constexpr int kChainXStage = kChainPass * 128;
+constexpr int kChainStageOut = 2 * 16384;
+constexpr int kChainSmem = 1024 + kChainWStages * kChainWBox + kChainXStages * kChainXStage +
+                           kChainStageOut + 1024;
+static_assert(kChainSmem <= 232448, "chain smem");
+
+struct ChainGemm {
+  int N, K, splits, tiles, kb;   // kb: K / 64
+  int epi;                       // kPhGemmPartial / kPhGemmSwiGLU
+};
+
+struct ChainArgs {
+  int n_phase;
+  int n_gemm;
+  int t_pre_wait;                // 1: the row count was written launches back (read it
+                                 // before griddepcontrol.wait); 0: by the predecessor
+  int kind[kChainMaxPhases];
+  int gemm[kChainMaxPhases];     // GEMM phases: slot 0..3
+  float* resid_part;             // per-resid-phase source: the shared split-K buffer
+  int resid_splits[kChainMaxPhases];
+  const float* norm_w[kChainMaxPhases];
+  ChainGemm g[4];
+  int rows_cap, d, n_q, n_kv, hd, ctx_cap;
+  float eps;
+  const int* t_dev;
+  const int* tok;
+  const __nv_bfloat16* embed;
+  float* h;
+  __nv_bfloat16* x;
+  const int* tok_pos;
+  const int* tok_slot;
+  const float2* rope;
+  __nv_bfloat16* q;
+  __nv_bfloat16* kc;             // this chain's RoPE layer bases
+  __nv_bfloat16* vc;
+  int rope_splits;
+  unsigned* bar;                 // phase arrival counter (self-resetting)
+};
+
+struct ChainJob {
+  int tile, k0, k1, split, t0, nt;
+};
+
+// Jobs of GEMM slot `g` owned by CTA c of G: units (pass, split, tile), tile fastest.
+struct ChainSched {
+  int units, c, G, T;
+  __device__ __forceinline__ void init(const ChainGemm& g, int T_, int c_, int G_) {
+    T = T_;
+    c = c_;
+    G = G_;
+    const int passes = (T + kChainPass - 1) / kChainPass;
+    units = g.tiles * g.splits * passes;
+  }
+  __device__ __forceinline__ bool get(const ChainGemm& g, int i, ChainJob& j) const {
+    const int u = c + i * G;
+    if (u >= units) return false;
+    const int per_pass = g.tiles * g.splits;
+    const int pass = u / per_pass;
+    const int r = u % per_pass;
+    j.tile = r % g.tiles;
+    j.split = r / g.tiles;
+    j.k0 = (int)((long long)g.kb * j.split / g.splits);
+    j.k1 = (int)((long long)g.kb * (j.split + 1) / g.splits);
+    j.t0 = pass * kChainPass;
+    j.nt = min(kChainPass, T - j.t0);
+    return true;
+  }
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void chain_wait_phase(const unsigned* bar, unsigned target) {
+  while (ld_acquire_u32(bar) < target) {
+  }
+}
+
+// fixed-tree sum over the 256 epilogue threads (named barrier 1)
+__device__ __forceinline__ float chain_block_sum(float v, float* sh, int et) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((et & 31) == 0) sh[et >> 5] = v;
+  asm volatile("bar.sync 1, %0;" ::"n"(kChainEpiThreads) : "memory");
+  float r = 0.f;
+#pragma unroll
+  for (int w = 0; w < kChainEpiThreads / 32; ++w) r += sh[w];
+  asm volatile("bar.sync 1, %0;" ::"n"(kChainEpiThreads) : "memory");
+  return r;
+}
+
+// x[t] = bf16(h[t] * rsqrt(mean(h[t]^2) + eps) * w), h[t] = src (+ sum of split partials)
+__device__ void chain_norm_rows(const ChainArgs& a, int T, int phase, int et, float* sh) {
+  const int d = a.d;
+  const bool embed = a.kind[phase] == kPhEmbed;
+  const float* w = a.norm_w[phase];
+  const int splits = a.resid_splits[phase];
+  const size_t sstride = (size_t)a.rows_cap * d;
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
+    float v[16];   // d <= 4096: 16 values per thread
+    float ss = 0.f;
+    const __nv_bfloat16* e = embed ? a.embed + (size_t)a.tok[t] * d : nullptr;
+    float* hr = a.h + (size_t)t * d;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int i = et + j * kChainEpiThreads;
+      float acc = 0.f;
+      if (i < d) {
+        if (embed) {
+          acc = __bfloat162float(e[i]);
+        } else {
+          acc = hr[i];
+          const float* p = a.resid_part + (size_t)t * d + i;
+          for (int s = 0; s < splits; ++s) acc += __ldcg(p + s * sstride);
+        }
+        hr[i] = acc;
+        ss += acc * acc;
+      }
+      v[j] = acc;
+    }
+    ss = chain_block_sum(ss, sh, et);
+    const float r = rsqrtf(ss / (float)d + a.eps);
+    __nv_bfloat16* xr = a.x + (size_t)t * d;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int i = et + j * kChainEpiThreads;
+      if (i < d) xr[i] = __float2bfloat16_rn(v[j] * r * w[i]);
+    }
+  }
+}
+
+// RoPE (rotate-half pairs (i, i + hd/2)) on the summed q/k/v partials; q to
+// the q buffer, k / v into the KV cache at (slot, position).
+__device__ void chain_rope(const ChainArgs& a, int T, int et) {
+  const int half = a.hd / 2;
+  const int heads = a.n_q + 2 * a.n_kv;
+  const int N = heads * a.hd;
+  const int n_pairs = heads * half;
+  const size_t sstride = (size_t)a.rows_cap * N;
+  const int items = T * n_pairs;
+  for (int it = blockIdx.x * kChainEpiThreads + et; it < items;
+       it += gridDim.x * kChainEpiThreads) {
+    const int t = it / n_pairs;
+    const int c = it % n_pairs;
+    const int head = c / half, i = c % half;
+    const float* p0 = a.resid_part + (size_t)t * N + head * a.hd + i;
+    float x0 = 0.f, x1 = 0.f;
+    for (int s = 0; s < a.rope_splits; ++s) {
+      x0 += __ldcg(p0 + s * sstride);
+      x1 += __ldcg(p0 + s * sstride + half);
+    }
+    const int pos = a.tok_pos[t];
+    if (head < a.n_q + a.n_kv) {
+      const float2 cs = a.rope[(size_t)pos * half + i];
+      const float ra = x0 * cs.x - x1 * cs.y;
+      const float rb = x1 * cs.x + x0 * cs.y;
+      if (head < a.n_q) {
+        __nv_bfloat16* dst = a.q + ((size_t)t * a.n_q + head) * a.hd;
+        dst[i] = __float2bfloat16_rn(ra);
+        dst[i + half] = __float2bfloat16_rn(rb);
+      } else {
+        const size_t off =
+            (((size_t)a.tok_slot[t] * a.n_kv + (head - a.n_q)) * a.ctx_cap + pos) * a.hd;
+        a.kc[off + i] = __float2bfloat16_rn(ra);
+        a.kc[off + i + half] = __float2bfloat16_rn(rb);
+      }
+    } else {
+      const size_t off =
+          (((size_t)a.tok_slot[t] * a.n_kv + (head - a.n_q - a.n_kv)) * a.ctx_cap + pos) * a.hd;
+      a.vc[off + i] = __float2bfloat16_rn(x0);
+      a.vc[off + i + half] = __float2bfloat16_rn(x1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kChainThreads, 1)
+k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtensorMap tw1,
+        const __grid_constant__ CUtensorMap tw2, const __grid_constant__ CUtensorMap tw3,
+        const __grid_constant__ CUtensorMap tx0, const __grid_constant__ CUtensorMap tx1,
+        const __grid_constant__ CUtensorMap tx2, const __grid_constant__ CUtensorMap tx3,
+        const __grid_constant__ CUtensorMap to0, const __grid_constant__ CUtensorMap to1,
+        const __grid_constant__ CUtensorMap to2, const __grid_constant__ CUtensorMap to3,
+        ChainArgs a) {
+  using namespace ptx;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* wring = smem;
+  uint8_t* xring = wring + kChainWStages * kChainWBox;
+  uint8_t* stage_out = xring + kChainXStages * kChainXStage;
+  uint64_t* w_full = reinterpret_cast<uint64_t*>(stage_out + kChainStageOut);
+  uint64_t* w_empty = w_full + kChainWStages;
+  uint64_t* x_full = w_empty + kChainWStages;
+  uint64_t* x_empty = x_full + kChainXStages;
+  uint64_t* tmem_full = x_empty + kChainXStages;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  float* sh = reinterpret_cast<float*>(tmem_slot + 4);   // 8 floats (block sums)
+
+  const CUtensorMap* tw[4] = {&tw0, &tw1, &tw2, &tw3};
+  const CUtensorMap* tx[4] = {&tx0, &tx1, &tx2, &tx3};
+  const CUtensorMap* to[4] = {&to0, &to1, &to2, &to3};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x, c = blockIdx.x;
+  auto row_count = [&]() {
+    const int t = *a.t_dev;
+    return t < 0 ? 0 : (t > a.rows_cap ? a.rows_cap : t);
+  };
+  // mid-step chains: the row count comes from the step's batch kernel, several
+  // launches back (the preceding attention released this grid only after its
+  // own wait); the first chain of a step follows the batch kernel directly
+  int T = a.t_pre_wait ? row_count() : -1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kChainWStages; ++s) {
+      mbar_init(&w_full[s], 1);
+      mbar_init(&w_empty[s], 1);
+    }
+    for (int s = 0; s < kChainXStages; ++s) {
+      mbar_init(&x_full[s], 1);
+      mbar_init(&x_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], kChainEpiThreads);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- weight producer: every GEMM job of the chain, in order
+    if (lane == 0) {
+      for (int s = 0; s < a.n_gemm; ++s) prefetch_tmap(tw[s]);
+      const uint64_t pol = policy_evict_first();
+      int gw = 0;
+      bool waited = false;
+      if (T < 0) {
+        pdl_wait();
+        pdl_trigger();
+        waited = true;
+        T = row_count();
+      }
+      for (int p = 0; p < a.n_phase && T > 0; ++p) {
+        if (a.kind[p] != kPhGemmPartial && a.kind[p] != kPhGemmSwiGLU) continue;
+        const ChainGemm& g = a.g[a.gemm[p]];
+        ChainSched sc;
+        sc.init(g, T, c, G);
+        ChainJob j;
+        for (int i = 0; sc.get(g, i, j); ++i) {
+          for (int kb = j.k0; kb < j.k1; ++kb, ++gw) {
+            const int s = gw % kChainWStages;
+            if (gw >= kChainWStages) {
+              if (!waited) {   // the first ring's worth streams before the predecessor ends
+                pdl_wait();
+                pdl_trigger();
+                waited = true;
+              }
+              mbar_wait(&w_empty[s], ((uint32_t)(gw / kChainWStages) - 1u) & 1u);
+            }
+            mbar_arrive_expect_tx(&w_full[s], kChainWBox);
+            tma_load_2d(wring + s * kChainWBox, tw[a.gemm[p]], &w_full[s], kb * 64, j.tile * 128,
+                        pol);
+          }
+        }
+      }
+      if (!waited) {
+        pdl_wait();
+        pdl_trigger();
+      }
+    } else {
+      pdl_wait();
+      pdl_trigger();
+    }
+    __syncwarp();
+  } else if (warp == 2) {
+    // ---------------- activation producer: waits for each phase's inputs
+    pdl_wait();
+    pdl_trigger();
+    if (T < 0) T = row_count();
+    if (lane == 0 && T > 0) {
+      for (int s = 0; s < a.n_gemm; ++s) prefetch_tmap(tx[s]);
+      const uint64_t pol = policy_evict_last();
+      int gx = 0;
+      for (int p = 0; p < a.n_phase; ++p) {
+        if (a.kind[p] != kPhGemmPartial && a.kind[p] != kPhGemmSwiGLU) continue;
+        const ChainGemm& g = a.g[a.gemm[p]];
+        ChainSched sc;
+        sc.init(g, T, c, G);
+        ChainJob j;
+        // only CTAs with jobs wait: a CTA's own epilogue cannot finish a phase it
+        // has jobs in before this wait passed, so no waiter can outlive the
+        // counter reset at the end of the chain
+        if (p > 0 && sc.get(g, 0, j)) {
+          chain_wait_phase(a.bar, (unsigned)(G * p));
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        for (int i = 0; sc.get(g, i, j); ++i) {
+          const int boxes = (j.nt + 63) >> 6;
+          for (int kb = j.k0; kb < j.k1; ++kb, ++gx) {
+            const int s = gx % kChainXStages;
+            if (gx >= kChainXStages)
+              mbar_wait(&x_empty[s], ((uint32_t)(gx / kChainXStages) - 1u) & 1u);
+            mbar_arrive_expect_tx(&x_full[s], (uint32_t)boxes * 8192u);
+            for (int b = 0; b < boxes; ++b)
+              tma_load_2d(xring + s * kChainXStage + b * 8192, tx[a.gemm[p]], &x_full[s], kb * 64,
+                          j.t0 + b * 64, pol);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    pdl_wait();
+    pdl_trigger();
+    if (T < 0) T = row_count();
+    int gw = 0, gx = 0, jn = 0;
+    for (int p = 0; p < a.n_phase && T > 0; ++p) {
+      if (a.kind[p] != kPhGemmPartial && a.kind[p] != kPhGemmSwiGLU) continue;
+      const ChainGemm& g = a.g[a.gemm[p]];
+      ChainSched sc;
+      sc.init(g, T, c, G);
+      ChainJob j;
+      for (int i = 0; sc.get(g, i, j); ++i, ++jn) {
+        const int buf = jn & 1;
+        const uint32_t acc = tmem_base + (uint32_t)(buf * kChainPass);
+        const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)((j.nt + 15) & ~15));
+        if (jn >= 2) {
+          mbar_wait(&tmem_empty[buf], ((uint32_t)(jn >> 1) - 1u) & 1u);
+          tc_fence_after();
+        }
+        for (int kb = j.k0; kb < j.k1; ++kb, ++gw, ++gx) {
+          const int sw = gw % kChainWStages, sx = gx % kChainXStages;
+          mbar_wait(&w_full[sw], (uint32_t)(gw / kChainWStages) & 1u);
+          mbar_wait(&x_full[sx], (uint32_t)(gx / kChainXStages) & 1u);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t wa = smem_u32(wring + sw * kChainWBox);
+            const uint32_t xa = smem_u32(xring + sx * kChainXStage);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_ss(acc, umma_desc_kmajor<128>(wa + kk * 32),
+                          umma_desc_kmajor<128>(xa + kk * 32), idesc,
+                          (kb > j.k0 || kk > 0) ? 1u : 0u);
+            mma_commit(&w_empty[sw]);
+            mma_commit(&x_empty[sx]);
+          }
+          __syncwarp();
+        }
+        if (lane == 0) mma_commit(&tmem_full[buf]);
+        __syncwarp();
+      }
+    }
+  } else if (warp == 3) {
+    pdl_wait();
+    pdl_trigger();
+  } else {
+    // ---------------- epilogue + glue warps 4..11
+    pdl_wait();
+    pdl_trigger();
+    if (T < 0) T = row_count();
+    const int et = threadIdx.x - 128;          // 0..255
+    const int q = warp & 3;                    // TMEM lane quarter
+    const int grp = (warp - 4) >> 2;           // 0 / 1: alternating 32-token chunks
+    const bool issuer = (warp == 4 + 4 * grp) && lane == 0;
+    int jn = 0, wbuf = 0, sbuf = 0;
+    for (int p = 0; p < a.n_phase; ++p) {
+      const int kind = a.kind[p];
+      if (p > 0) {   // inputs of this phase: every CTA finished phase p - 1
+        if (et == 0) chain_wait_phase(a.bar, (unsigned)(G * p));
+        asm volatile("bar.sync 1, %0;" ::"n"(kChainEpiThreads) : "memory");
+      }
+      bool stored = false;
+      if (T > 0 && (kind == kPhGemmPartial || kind == kPhGemmSwiGLU)) {
+        const int gi = a.gemm[p];
+        const ChainGemm& g = a.g[gi];
+        ChainSched sc;
+        sc.init(g, T, c, G);
+        ChainJob j;
+        for (int i = 0; sc.get(g, i, j); ++i, ++jn) {
+          const int buf = jn & 1;
+          mbar_wait(&tmem_full[buf], (uint32_t)(jn >> 1) & 1u);
+          tc_fence_after();
+          const int t_pad = (j.nt + 15) & ~15;
+          const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kChainPass);
+          for (int cc = 32 * grp; cc < t_pad; cc += 64) {
+            uint32_t r[32];
+            tmem_ld32_issue(tq + (uint32_t)cc, r);
+            tmem_ld_wait(r);
+            float v[32];
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) v[jj] = __uint_as_float(r[jj]);
+            const int nvalid = min(32, j.nt - cc);
+            if (kind == kPhGemmPartial) {
+              // [split][t][n] partials: each warp stages and stores its 32 rows
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                if (hh * 16 >= nvalid) break;
+                float* wst = reinterpret_cast<float*>(stage_out + grp * 16384 + q * 4096 +
+                                                      wbuf * 2048);
+                wbuf ^= 1;
+                if (lane == 0) bulk_wait_read<1>();
+                __syncwarp();
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) wst[jj * 32 + lane] = v[hh * 16 + jj];
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  tma_store_2d(to[gi], wst, j.tile * 128 + q * 32,
+                               j.split * a.rows_cap + j.t0 + cc + 16 * hh);
+                  bulk_commit();
+                }
+              }
+              stored = true;
+            } else {
+              // SwiGLU: rows interleaved [gate_i, up_i]; even lanes finish
+              // tokens 0..15 of the chunk, odd lanes 16..31
+              const bool odd = lane & 1;
+              float out[16];
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) {
+                const float send = odd ? v[jj] : v[jj + 16];
+                const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+                const float gt = odd ? recv : v[jj];
+                const float up = odd ? v[jj + 16] : recv;
+                float th;
+                asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(0.5f * gt));
+                out[jj] = gt * fmaf(0.5f, th, 0.5f) * up;
+              }
+              uint8_t* stg = stage_out + grp * 16384 + sbuf * 8192;
+              sbuf ^= 1;
+              if (issuer) bulk_wait_read<1>();
+              asm volatile("bar.sync %0, 128;" ::"r"(2 + grp) : "memory");
+              __nv_bfloat16* st = reinterpret_cast<__nv_bfloat16*>(stg);
+              const int fi = (q * 32 + lane) >> 1;
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj)
+                st[((odd ? 16 : 0) + jj) * 64 + fi] = __float2bfloat16_rn(out[jj]);
+              fence_proxy_async_smem();
+              asm volatile("bar.sync %0, 128;" ::"r"(2 + grp) : "memory");
+              if (issuer) {
+                tma_store_2d(to[gi], stg, (j.tile * 128) >> 1, j.t0 + cc);
+                bulk_commit();
+              }
+              stored = true;
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(&tmem_empty[buf]);
+        }
+        if (stored && (issuer || (kind == kPhGemmPartial && lane == 0))) {
+          bulk_wait_all();   // this phase's outputs are in global memory ...
+          asm volatile("fence.proxy.async.global;" ::: "memory");   // ... and visible
+        }
+      } else if (T > 0 && (kind == kPhResid || kind == kPhEmbed)) {
+        chain_norm_rows(a, T, p, et, sh);
+      } else if (T > 0 && kind == kPhRope) {
+        chain_rope(a, T, et);
+      }
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"n"(kChainEpiThreads) : "memory");
+      if (et == 0) {
+        const unsigned prev = atomicAdd(a.bar, 1u);
+        // the last arrival of the last phase: every CTA is past every wait
+        if (p == a.n_phase - 1 && prev == (unsigned)(G * a.n_phase) - 1u) atomicExch(a.bar, 0u);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+struct ChainPlan {
+  GemmPlan gp[4];
+  ChainArgs args;
+  int n_gemm = 0;
+};
+
+static int chain_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+// One split count per chain GEMM: about one job per SM at one pass, >= 3 k blocks per job.
+int chain_splits(int N, int K) {
+  const int tiles = (N + 127) / 128, kb = K / 64;
+  int s = chain_sms() / tiles;
+  if (s > 16) s = 16;
+  if (s < 1) s = 1;
+  while (s > 1 && kb / s < 3) --s;
+  return s;
+}
+
+int chain_launch(const void* plan_v, cudaStream_t s) {
+  const ChainPlan& cp = *reinterpret_cast<const ChainPlan*>(plan_v);
+  static bool cfg = false;
+  if (!cfg) {
+    SPECTRE_CUDA_TRY(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kChainSmem));
+    cfg = true;
+  }
+  const GemmPlan* g = cp.gp;
+  SPECTRE_LAUNCH_PDL("k_chain", k_chain, dim3(chain_sms()), dim3(kChainThreads), kChainSmem, s,
+                     g[0].tmap_w, g[1].tmap_w, g[2].tmap_w, g[3].tmap_w, g[0].tmap_x, g[1].tmap_x,
+                     g[2].tmap_x, g[3].tmap_x, g[0].tmap_out, g[1].tmap_out, g[2].tmap_out,
+                     g[3].tmap_out, cp.args);
+  return SPECTRE_OK;
+}
+
+void* chain_alloc() { return new ChainPlan(); }
+void chain_free(void* p) { delete reinterpret_cast<ChainPlan*>(p); }
+ChainArgs* chain_args(void* p) { return &reinterpret_cast<ChainPlan*>(p)->args; }
+
+// Add a GEMM phase: W [N][K], X [rows_cap][K]; epi kPhGemmPartial (partials to
+// part [splits][rows_cap][N]) or kPhGemmSwiGLU (act [rows_cap][N/2]).
+int chain_add_gemm(void* plan_v, const void* W, int N, int K, const void* X, int rows_cap, int epi,
+                   float* part, void* act) {
+  ChainPlan& cp = *reinterpret_cast<ChainPlan*>(plan_v);
+  ChainArgs& a = cp.args;
+  if (cp.n_gemm >= 4 || a.n_phase >= kChainMaxPhases) return arg_fail("chain: too many phases");
+  if (N % 128 || K % 64) return arg_fail("chain: N % 128, K % 64");
+  const int gi = cp.n_gemm++;
+  a.n_gemm = cp.n_gemm;
+  const int splits = epi == kPhGemmSwiGLU ? 1 : chain_splits(N, K);
+  GemmPlan& gp = cp.gp[gi];
+  CHAIN_TRY(gemm_plan(&gp, W, N, K, X, rows_cap, epi == kPhGemmSwiGLU ? kSwiGLU : kPartial, splits, 0,
+                64, 128));
+  CHAIN_TRY(gemm_set_outputs(&gp, part, nullptr, nullptr, act, N / 2));
+  ChainGemm& g = a.g[gi];
+  g.N = N;
+  g.K = K;
+  g.splits = splits;
+  g.tiles = N / 128;
+  g.kb = K / 64;
+  g.epi = epi;
+  a.kind[a.n_phase] = epi;
+  a.gemm[a.n_phase] = gi;
+  ++a.n_phase;
+  return SPECTRE_OK;
+}
+
+// Add a glue phase (kPhEmbed / kPhResid / kPhRope).  Resid / Rope read the
+// split-K partials of the chain's LAST added GEMM.
+int chain_add_glue(void* plan_v, int kind, const float* norm_w) {
+  ChainPlan& cp = *reinterpret_cast<ChainPlan*>(plan_v);
+  ChainArgs& a = cp.args;
+  if (a.n_phase >= kChainMaxPhases) return arg_fail("chain: too many phases");
+  if (kind == kPhResid || kind == kPhRope) {
+    if (cp.n_gemm == 0 || a.g[cp.n_gemm - 1].epi != kPhGemmPartial)
+      return arg_fail("chain: residual / RoPE phases follow a split-K GEMM");
+    if (kind == kPhResid) a.resid_splits[a.n_phase] = a.g[cp.n_gemm - 1].splits;
+    else a.rope_splits = a.g[cp.n_gemm - 1].splits;
+  }
+  a.kind[a.n_phase] = kind;
+  a.gemm[a.n_phase] = -1;
+  a.norm_w[a.n_phase] = norm_w;
+  ++a.n_phase;
+  return SPECTRE_OK;
+}
+
+int chain_set_model(void* plan_v, const ChainModel& m) {
+  ChainArgs& a = reinterpret_cast<ChainPlan*>(plan_v)->args;
+  if (m.d > 16 * kChainEpiThreads) return arg_fail("chain: d_model > 4096");
+  a.rows_cap = m.rows_cap;
+  a.d = m.d;
+  a.n_q = m.n_q;
+  a.n_kv = m.n_kv;
+  a.hd = m.hd;
+  a.ctx_cap = m.ctx_cap;
+  a.eps = m.eps;
+  a.t_dev = m.t_dev;
+  a.tok = m.tok;
+  a.embed = reinterpret_cast<const __nv_bfloat16*>(m.embed);
+  a.h = m.h;
+  a.x = reinterpret_cast<__nv_bfloat16*>(m.x);
+  a.tok_pos = m.tok_pos;
+  a.tok_slot = m.tok_slot;
+  a.rope = m.rope;
+  a.q = reinterpret_cast<__nv_bfloat16*>(m.q);
+  a.kc = reinterpret_cast<__nv_bfloat16*>(m.kc);
+  a.vc = reinterpret_cast<__nv_bfloat16*>(m.vc);
+  a.resid_part = m.part;
+  a.bar = m.bar;
+  a.t_pre_wait = m.t_pre_wait;
+  return SPECTRE_OK;
+}
+
+}  // namespace spectre

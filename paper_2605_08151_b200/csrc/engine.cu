@@ -17,6 +17,7 @@
 #include <memory>
 #include <vector>
 
+#include "chain.h"
 #include "common.cuh"
 #include "engine_state.cuh"
 #include "gemm.h"
@@ -101,6 +102,21 @@ static int pick_splits(int n_tiles, int k_iters, int ctas = 148) {
 struct ModelRT {
   SpectreModelDims dm{};
   SpectreModelWeights w{};
+  // draft decode steps as persistent chains (chain.cu): first = embed + qkv(0) +
+  // RoPE; mid[l] = layer l's o .. layer l+1's RoPE; last = layer L-1's o .. final norm
+  bool use_chain = false;
+  void* ch_first = nullptr;
+  std::vector<void*> ch_mid;
+  void* ch_last = nullptr;
+  unsigned* ch_bar = nullptr;
+  ModelRT() = default;
+  ModelRT(const ModelRT&) = delete;
+  ModelRT& operator=(const ModelRT&) = delete;
+  ~ModelRT() {
+    for (void* p : ch_mid) chain_free(p);
+    if (ch_first) chain_free(ch_first);
+    if (ch_last) chain_free(ch_last);
+  }
   int n_req = 0, rows_cap = 0, ctx_cap = 0, max_new = 1, split_max = 1, rb_cap = 1;
   int sp_qkv = 1, sp_o = 1, sp_d = 1;
   int tr_qkv = 256, tr_o = 256, tr_d = 256;   // weight rows per tile, per GEMM
@@ -146,6 +162,9 @@ struct ModelRT {
     sp_o = pick_splits((d + tr_o - 1) / tr_o, qd / 64, ctas);
     sp_d = pick_splits((d + tr_d - 1) / tr_d, dm.ffn / 64, ctas);
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
+    if (use_chain)
+      part_n = std::max({part_n, (size_t)chain_splits(nqkv(), d) * nqkv(),
+                         (size_t)chain_splits(d, qd) * d, (size_t)chain_splits(d, dm.ffn) * d});
     attn_chunk = attn_chunk_default(n_req * dm.n_kv_heads, ctx_cap);
     split_max = (ctx_cap + attn_chunk - 1) / attn_chunk;
     // m-tiles per request, in whole attention row blocks (2 m-tiles at hd 128, 3 at hd 64)
@@ -168,6 +187,7 @@ struct ModelRT {
     amax_v = b.take<float>((size_t)n_blocks * R);
     amax_i = b.take<int>((size_t)n_blocks * R);
     rope = b.take<float2>((size_t)ctx_cap * dm.head_dim / 2);
+    ch_bar = b.take<unsigned>(64);
     bt.tok = b.take<int>(R);
     bt.pos = b.take<int>(R);
     bt.slot = b.take<int>(R);
@@ -228,6 +248,73 @@ struct ModelRT {
     TRY(make_tmap_bf16(&tm_k32, w.k_cache, dm.head_dim, kv_rows, 32, 64));
     TRY(make_tmap_bf16(&tm_v32, w.v_cache, dm.head_dim, kv_rows, 32, 64));
     plm.args.t_dev = bt.t_dev;
+    if (use_chain) TRY(plan_chains());
+    return SPECTRE_OK;
+  }
+
+  int plan_chains() {
+    const int d = dm.d_model, L = dm.n_layers, qd = dm.n_q_heads * dm.head_dim, F = dm.ffn;
+    auto bf = [](const void* p) { return reinterpret_cast<const __nv_bfloat16*>(p); };
+    const size_t kv_layer = (size_t)n_req * dm.n_kv_heads * ctx_cap * dm.head_dim;
+    auto* kc = reinterpret_cast<__nv_bfloat16*>(w.k_cache);
+    auto* vc = reinterpret_cast<__nv_bfloat16*>(w.v_cache);
+    auto model = [&](int rope_layer, int pre_wait) {
+      ChainModel m{};
+      m.rows_cap = rows_cap;
+      m.d = d;
+      m.n_q = dm.n_q_heads;
+      m.n_kv = dm.n_kv_heads;
+      m.hd = dm.head_dim;
+      m.ctx_cap = ctx_cap;
+      m.eps = dm.rms_eps;
+      m.t_dev = bt.t_dev;
+      m.tok = bt.tok;
+      m.embed = w.embed;
+      m.h = h;
+      m.x = x;
+      m.tok_pos = bt.pos;
+      m.tok_slot = bt.slot;
+      m.rope = rope;
+      m.q = q;
+      m.kc = rope_layer >= 0 ? kc + rope_layer * kv_layer : nullptr;
+      m.vc = rope_layer >= 0 ? vc + rope_layer * kv_layer : nullptr;
+      m.part = part;
+      m.bar = ch_bar;
+      m.t_pre_wait = pre_wait;
+      return m;
+    };
+    auto add_qkv_rope = [&](void* c, int l) {
+      TRY(chain_add_gemm(c, bf(w.wqkv) + (size_t)l * nqkv() * d, nqkv(), d, x, rows_cap,
+                         kPhGemmPartial, part, nullptr));
+      TRY(chain_add_glue(c, kPhRope, nullptr));
+      return SPECTRE_OK;
+    };
+    auto add_mlp_block = [&](void* c, int l) {
+      TRY(chain_add_gemm(c, bf(w.wo) + (size_t)l * d * qd, d, qd, attn, rows_cap, kPhGemmPartial,
+                         part, nullptr));
+      TRY(chain_add_glue(c, kPhResid, w.mlp_norm + (size_t)l * d));
+      TRY(chain_add_gemm(c, bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap,
+                         kPhGemmSwiGLU, nullptr, act));
+      TRY(chain_add_gemm(c, bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPhGemmPartial,
+                         part, nullptr));
+      TRY(chain_add_glue(c, kPhResid,
+                         l + 1 < L ? w.attn_norm + (size_t)(l + 1) * d : w.final_norm));
+      return SPECTRE_OK;
+    };
+    ch_first = chain_alloc();
+    TRY(chain_add_glue(ch_first, kPhEmbed, w.attn_norm));
+    TRY(add_qkv_rope(ch_first, 0));
+    TRY(chain_set_model(ch_first, model(0, 0)));   // follows the batch kernel directly
+    for (int l = 0; l + 1 < L; ++l) {
+      void* c = chain_alloc();
+      ch_mid.push_back(c);
+      TRY(add_mlp_block(c, l));
+      TRY(add_qkv_rope(c, l + 1));
+      TRY(chain_set_model(c, model(l + 1, 1)));
+    }
+    ch_last = chain_alloc();
+    TRY(add_mlp_block(ch_last, L - 1));
+    TRY(chain_set_model(ch_last, model(-1, 1)));
     return SPECTRE_OK;
   }
 
@@ -265,8 +352,17 @@ struct ModelRT {
     const size_t kv_layer = (size_t)n_req * dm.n_kv_heads * ctx_cap * hd;
     auto* kc = reinterpret_cast<__nv_bfloat16*>(w.k_cache);
     auto* vc = reinterpret_cast<__nv_bfloat16*>(w.v_cache);
-    TRY(launch_embed_rmsnorm(bt.tok, bt.t_dev, rows_cap, w.embed, w.attn_norm, h, x, d, eps, s));
-    for (int l = 0; l < L; ++l) {
+    if (use_chain) {
+      TRY(chain_launch(ch_first, s));
+      for (int l = 0; l < L; ++l) {
+        a.layer_row0 = l * n_req * dm.n_kv_heads * ctx_cap;
+        TRY(launch_attention_w(tm_k32, tm_v32, a, hd, rows, s));
+        TRY(chain_launch(l + 1 < L ? ch_mid[l] : ch_last, s));
+      }
+    }
+    if (!use_chain) TRY(launch_embed_rmsnorm(bt.tok, bt.t_dev, rows_cap, w.embed, w.attn_norm, h,
+                                             x, d, eps, s));
+    for (int l = 0; l < L && !use_chain; ++l) {
       TRY(gemm_run(pq[l], s));
       TRY(launch_qkv_rope_kv(part, sp_qkv, rows_cap, bt.t_dev, rows_cap, bt.pos, bt.slot,
                                rope, q, kc + l * kv_layer, vc + l * kv_layer, dm.n_q_heads,
@@ -424,6 +520,14 @@ struct Engine {
     drf.half_gemm = [] {
       const char* v = getenv("SPECTRE_DRAFT_HALF");
       return v ? atoi(v) != 0 : true;
+    }();
+    // the draft's forwards as persistent chains (SPECTRE_DRAFT_CHAIN=0: per-op kernels)
+    drf.use_chain = [&] {
+      const char* v = getenv("SPECTRE_DRAFT_CHAIN");
+      const bool on = v ? atoi(v) != 0 : true;
+      const int qd = d.n_q_heads * d.head_dim, nq = (d.n_q_heads + 2 * d.n_kv_heads) * d.head_dim;
+      return on && d.d_model % 128 == 0 && nq % 128 == 0 && (2 * d.ffn) % 128 == 0 &&
+             qd % 64 == 0 && d.ffn % 64 == 0 && d.d_model <= 4096;
     }();
     tgt.tile_rows = tile_rows_default(256);
     st.n_req = c.n_req;
