@@ -16,12 +16,12 @@
 // activation loads wait for the phase barrier that publishes their producer's
 // output.
 //
-// One CTA per SM (grid = SMs, all co-resident), 12 warps:
+// One CTA per SM (grid = SMs, all co-resident), 11 warps:
 //   warp 0  weight producer (TMA, evict-first), runs across phase boundaries
 //   warp 1  TMEM allocator + single-thread tcgen05.mma issuer
-//   warp 2  activation producer (TMA), waits on the phase barriers
-//   warps 4-11  epilogue (tcgen05.ld -> split-K partial / SwiGLU stores) and
+//   warps 2-9  epilogue (tcgen05.ld -> split-K partial / SwiGLU stores) and
 //           the glue phases (residual + RMSNorm, RoPE, embedding) in between
+//   warp 10 activation producer (TMA), waits on the phase barriers
 // Phase barrier: one monotonic arrival counter per chain launch (each CTA
 // arrives once per phase after its results are globally visible; the last
 // arrival of the last phase resets it for the next launch).
@@ -48,17 +48,22 @@ namespace spectre {
     if (int _r = (x)) return _r; \
   } while (0)
 
-constexpr int kChainThreads = 384;
-constexpr int kChainEpiThreads = 256;          // warps 4..11
+constexpr int kChainThreads = 352;
+constexpr int kChainEpiThreads = 256;          // warps 2..9
 constexpr int kChainMaxPhases = 8;
-constexpr int kChainWStages = 8;               // 16 KB weight boxes (128 rows x 64 k)
-constexpr int kChainXStages = 4;               // up to 128 tokens x 64 k (16 KB)
+// One ring of stages, each holding kChainKS consecutive 64-wide k blocks of a
+// job's weights (128 rows: 16 KB per block) AND its activations (up to 128
+// tokens: 16 KB per block): both producers fill their half of a stage (one
+// full barrier, two arrivals + tx bytes) and ONE MMA commit releases it — the
+// tcgen05 commit is the MMA issuer's expensive step at T = 64.
+constexpr int kChainKS = 2;
+constexpr int kChainStages = 3;
 constexpr int kChainPass = 128;                // tokens per MMA pass
-constexpr int kChainWBox = 128 * 128;
-constexpr int kChainXStage = kChainPass * 128;
+constexpr int kChainWBox = 128 * 128;           // one k block of weights
+constexpr int kChainXBlk = kChainPass * 128;     // one k block of activations
+constexpr int kChainStageBytes = kChainKS * (kChainWBox + kChainXBlk);
 constexpr int kChainStageOut = 2 * 16384;
-constexpr int kChainSmem = 1024 + kChainWStages * kChainWBox + kChainXStages * kChainXStage +
-                           kChainStageOut + 1024;
+constexpr int kChainSmem = 1024 + kChainStages * kChainStageBytes + kChainStageOut + 1024;
 static_assert(kChainSmem <= 232448, "chain smem");
 
 struct ChainGemm {
@@ -92,6 +97,7 @@ struct ChainArgs {
   __nv_bfloat16* vc;
   int rope_splits;
   unsigned* bar;                 // phase arrival counter (self-resetting)
+  unsigned long long* dbg;       // diagnostics: CTA 0's globaltimer stamps [2 + 2 * phases]
 };
 
 struct ChainJob {
@@ -124,6 +130,12 @@ struct ChainSched {
   }
 };
 
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -148,87 +160,162 @@ __device__ __forceinline__ float chain_block_sum(float v, float* sh, int et) {
   return r;
 }
 
-// x[t] = bf16(h[t] * rsqrt(mean(h[t]^2) + eps) * w), h[t] = src (+ sum of split partials)
-__device__ void chain_norm_rows(const ChainArgs& a, int T, int phase, int et, float* sh) {
-  const int d = a.d;
+constexpr int kChainSplitBatch = 8;   // split partials in flight per batch (register budget)
+
+// x[t] = bf16(h[t] * rsqrt(mean(h[t]^2) + eps) * w), h[t] = embedding row or
+// h[t] + sum of the split partials (in split order).  One row per CTA at a time,
+// float4 per thread; every split partial of a float4 is loaded before the
+// fixed-order sum, so the loads overlap instead of forming a latency chain.
+// kJ float4 per thread (d <= 1024 kJ), kB split partials per batch: kJ * kB
+// float4 loads in flight per thread
+template <int kJ, int kB>
+__device__ void chain_norm_rows_t(const ChainArgs& a, int T, int phase, int et, float* sh) {
+  const int d = a.d, nv = d >> 2;
   const bool embed = a.kind[phase] == kPhEmbed;
-  const float* w = a.norm_w[phase];
+  const float4* w4 = reinterpret_cast<const float4*>(a.norm_w[phase]);
   const int splits = a.resid_splits[phase];
-  const size_t sstride = (size_t)a.rows_cap * d;
+  const size_t sstride = (size_t)a.rows_cap * nv;
   for (int t = blockIdx.x; t < T; t += gridDim.x) {
-    float v[16];   // d <= 4096: 16 values per thread
+    float4 v[kJ];
     float ss = 0.f;
-    const __nv_bfloat16* e = embed ? a.embed + (size_t)a.tok[t] * d : nullptr;
-    float* hr = a.h + (size_t)t * d;
+    float4* h4 = reinterpret_cast<float4*>(a.h + (size_t)t * d);
+    const float4* p4 = reinterpret_cast<const float4*>(a.resid_part) + (size_t)t * nv;
+    if (embed) {
+      const __nv_bfloat16* e = a.embed + (size_t)a.tok[t] * d;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int i = et + j * kChainEpiThreads;
-      float acc = 0.f;
-      if (i < d) {
-        if (embed) {
-          acc = __bfloat162float(e[i]);
-        } else {
-          acc = hr[i];
-          const float* p = a.resid_part + (size_t)t * d + i;
-          for (int s = 0; s < splits; ++s) acc += __ldcg(p + s * sstride);
+      for (int j = 0; j < kJ; ++j) {
+        const int i = et + j * kChainEpiThreads;
+        v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < nv) {
+          const uint2 raw = *reinterpret_cast<const uint2*>(e + 4 * i);
+          const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+          const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+          v[j] = make_float4(lo.x, lo.y, hi.x, hi.y);
         }
-        hr[i] = acc;
-        ss += acc * acc;
       }
-      v[j] = acc;
+    } else {
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const int i = et + j * kChainEpiThreads;
+        v[j] = i < nv ? h4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      // every (element, split) load of a batch in flight at once; per element
+      // the sum stays h + p0 + p1 + ... (split order)
+      for (int s0 = 0; s0 < splits; s0 += kB) {
+        float4 ld[kJ][kB];
+#pragma unroll
+        for (int sp = 0; sp < kB; ++sp)
+#pragma unroll
+          for (int j = 0; j < kJ; ++j) {
+            const int i = et + j * kChainEpiThreads;
+            if (s0 + sp < splits && i < nv) ld[j][sp] = __ldcg(p4 + (s0 + sp) * sstride + i);
+          }
+#pragma unroll
+        for (int sp = 0; sp < kB; ++sp)
+#pragma unroll
+          for (int j = 0; j < kJ; ++j)
+            if (s0 + sp < splits) {
+              v[j].x += ld[j][sp].x;
+              v[j].y += ld[j][sp].y;
+              v[j].z += ld[j][sp].z;
+              v[j].w += ld[j][sp].w;
+            }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int i = et + j * kChainEpiThreads;
+      if (i < nv) {
+        h4[i] = v[j];
+        ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
+      }
     }
     ss = chain_block_sum(ss, sh, et);
     const float r = rsqrtf(ss / (float)d + a.eps);
-    __nv_bfloat16* xr = a.x + (size_t)t * d;
+    __nv_bfloat162* xo = reinterpret_cast<__nv_bfloat162*>(a.x + (size_t)t * d);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < kJ; ++j) {
       const int i = et + j * kChainEpiThreads;
-      if (i < d) xr[i] = __float2bfloat16_rn(v[j] * r * w[i]);
+      if (i < nv) {
+        const float4 ww = w4[i];
+        xo[2 * i] = __floats2bfloat162_rn(v[j].x * r * ww.x, v[j].y * r * ww.y);
+        xo[2 * i + 1] = __floats2bfloat162_rn(v[j].z * r * ww.z, v[j].w * r * ww.w);
+      }
     }
   }
 }
 
+__device__ void chain_norm_rows(const ChainArgs& a, int T, int phase, int et, float* sh) {
+  const int nv = a.d >> 2;
+  if (nv <= kChainEpiThreads) chain_norm_rows_t<1, 8>(a, T, phase, et, sh);
+  else chain_norm_rows_t<2, 4>(a, T, phase, et, sh);   // d <= 2048 (chain_set_model)
+}
+
 // RoPE (rotate-half pairs (i, i + hd/2)) on the summed q/k/v partials; q to
-// the q buffer, k / v into the KV cache at (slot, position).
+// the q buffer, k / v into the KV cache at (slot, position).  Four consecutive
+// pairs per item (float4 partial loads), all splits in flight.
 __device__ void chain_rope(const ChainArgs& a, int T, int et) {
   const int half = a.hd / 2;
   const int heads = a.n_q + 2 * a.n_kv;
   const int N = heads * a.hd;
-  const int n_pairs = heads * half;
+  const int n_quads = heads * half / 4;
   const size_t sstride = (size_t)a.rows_cap * N;
-  const int items = T * n_pairs;
+  const int splits = a.rope_splits;
+  const int items = T * n_quads;
   for (int it = blockIdx.x * kChainEpiThreads + et; it < items;
        it += gridDim.x * kChainEpiThreads) {
-    const int t = it / n_pairs;
-    const int c = it % n_pairs;
+    const int t = it / n_quads;
+    const int c = (it % n_quads) * 4;            // first pair index
     const int head = c / half, i = c % half;
     const float* p0 = a.resid_part + (size_t)t * N + head * a.hd + i;
-    float x0 = 0.f, x1 = 0.f;
-    for (int s = 0; s < a.rope_splits; ++s) {
-      x0 += __ldcg(p0 + s * sstride);
-      x1 += __ldcg(p0 + s * sstride + half);
+    float x0[4] = {0.f, 0.f, 0.f, 0.f}, x1[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int s0 = 0; s0 < splits; s0 += kChainSplitBatch / 2) {   // split order kept
+      float4 la[kChainSplitBatch / 2], lb[kChainSplitBatch / 2];
+#pragma unroll
+      for (int sp = 0; sp < kChainSplitBatch / 2; ++sp)
+        if (s0 + sp < splits) {
+          la[sp] = __ldcg(reinterpret_cast<const float4*>(p0 + (s0 + sp) * sstride));
+          lb[sp] = __ldcg(reinterpret_cast<const float4*>(p0 + (s0 + sp) * sstride + half));
+        }
+#pragma unroll
+      for (int sp = 0; sp < kChainSplitBatch / 2; ++sp)
+        if (s0 + sp < splits) {
+          x0[0] += la[sp].x; x0[1] += la[sp].y; x0[2] += la[sp].z; x0[3] += la[sp].w;
+          x1[0] += lb[sp].x; x1[1] += lb[sp].y; x1[2] += lb[sp].z; x1[3] += lb[sp].w;
+        }
     }
     const int pos = a.tok_pos[t];
+    __nv_bfloat16* dst;
+    if (head < a.n_q) dst = a.q + ((size_t)t * a.n_q + head) * a.hd;
+    else if (head < a.n_q + a.n_kv)
+      dst = a.kc + (((size_t)a.tok_slot[t] * a.n_kv + (head - a.n_q)) * a.ctx_cap + pos) * a.hd;
+    else
+      dst = a.vc +
+            (((size_t)a.tok_slot[t] * a.n_kv + (head - a.n_q - a.n_kv)) * a.ctx_cap + pos) * a.hd;
+    float ra[4], rb[4];
     if (head < a.n_q + a.n_kv) {
-      const float2 cs = a.rope[(size_t)pos * half + i];
-      const float ra = x0 * cs.x - x1 * cs.y;
-      const float rb = x1 * cs.x + x0 * cs.y;
-      if (head < a.n_q) {
-        __nv_bfloat16* dst = a.q + ((size_t)t * a.n_q + head) * a.hd;
-        dst[i] = __float2bfloat16_rn(ra);
-        dst[i + half] = __float2bfloat16_rn(rb);
-      } else {
-        const size_t off =
-            (((size_t)a.tok_slot[t] * a.n_kv + (head - a.n_q)) * a.ctx_cap + pos) * a.hd;
-        a.kc[off + i] = __float2bfloat16_rn(ra);
-        a.kc[off + i + half] = __float2bfloat16_rn(rb);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 cs = a.rope[(size_t)pos * half + i + k];
+        ra[k] = x0[k] * cs.x - x1[k] * cs.y;
+        rb[k] = x1[k] * cs.x + x0[k] * cs.y;
       }
     } else {
-      const size_t off =
-          (((size_t)a.tok_slot[t] * a.n_kv + (head - a.n_q - a.n_kv)) * a.ctx_cap + pos) * a.hd;
-      a.vc[off + i] = __float2bfloat16_rn(x0);
-      a.vc[off + i + half] = __float2bfloat16_rn(x1);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        ra[k] = x0[k];
+        rb[k] = x1[k];
+      }
     }
+    __nv_bfloat162 a01 = __floats2bfloat162_rn(ra[0], ra[1]), a23 = __floats2bfloat162_rn(ra[2], ra[3]);
+    __nv_bfloat162 b01 = __floats2bfloat162_rn(rb[0], rb[1]), b23 = __floats2bfloat162_rn(rb[2], rb[3]);
+    uint2 ua, ub;
+    ua.x = *reinterpret_cast<uint32_t*>(&a01);
+    ua.y = *reinterpret_cast<uint32_t*>(&a23);
+    ub.x = *reinterpret_cast<uint32_t*>(&b01);
+    ub.y = *reinterpret_cast<uint32_t*>(&b23);
+    *reinterpret_cast<uint2*>(dst + i) = ua;
+    *reinterpret_cast<uint2*>(dst + i + half) = ub;
   }
 }
 
@@ -244,14 +331,11 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  uint8_t* wring = smem;
-  uint8_t* xring = wring + kChainWStages * kChainWBox;
-  uint8_t* stage_out = xring + kChainXStages * kChainXStage;
-  uint64_t* w_full = reinterpret_cast<uint64_t*>(stage_out + kChainStageOut);
-  uint64_t* w_empty = w_full + kChainWStages;
-  uint64_t* x_full = w_empty + kChainWStages;
-  uint64_t* x_empty = x_full + kChainXStages;
-  uint64_t* tmem_full = x_empty + kChainXStages;   // [2]
+  uint8_t* ring = smem;   // stage s: [KS weight blocks][KS activation blocks]
+  uint8_t* stage_out = ring + kChainStages * kChainStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + kChainStageOut);
+  uint64_t* empty = full + kChainStages;
+  uint64_t* tmem_full = empty + kChainStages;       // [2]
   uint64_t* tmem_empty = tmem_full + 2;            // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   float* sh = reinterpret_cast<float*>(tmem_slot + 4);   // 8 floats (block sums)
@@ -271,13 +355,9 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
   int T = a.t_pre_wait ? row_count() : -1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kChainWStages; ++s) {
-      mbar_init(&w_full[s], 1);
-      mbar_init(&w_empty[s], 1);
-    }
-    for (int s = 0; s < kChainXStages; ++s) {
-      mbar_init(&x_full[s], 1);
-      mbar_init(&x_empty[s], 1);
+    for (int s = 0; s < kChainStages; ++s) {
+      mbar_init(&full[s], 2);    // weight half + activation half
+      mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tmem_full[b], 1);
@@ -311,19 +391,21 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
         sc.init(g, T, c, G);
         ChainJob j;
         for (int i = 0; sc.get(g, i, j); ++i) {
-          for (int kb = j.k0; kb < j.k1; ++kb, ++gw) {
-            const int s = gw % kChainWStages;
-            if (gw >= kChainWStages) {
+          for (int kb = j.k0; kb < j.k1; kb += kChainKS, ++gw) {
+            const int s = gw % kChainStages;
+            const int nk = min(kChainKS, j.k1 - kb);
+            if (gw >= kChainStages) {
               if (!waited) {   // the first ring's worth streams before the predecessor ends
                 pdl_wait();
                 pdl_trigger();
                 waited = true;
               }
-              mbar_wait(&w_empty[s], ((uint32_t)(gw / kChainWStages) - 1u) & 1u);
+              mbar_wait(&empty[s], ((uint32_t)(gw / kChainStages) - 1u) & 1u);
             }
-            mbar_arrive_expect_tx(&w_full[s], kChainWBox);
-            tma_load_2d(wring + s * kChainWBox, tw[a.gemm[p]], &w_full[s], kb * 64, j.tile * 128,
-                        pol);
+            mbar_arrive_expect_tx(&full[s], (uint32_t)nk * kChainWBox);
+            for (int q = 0; q < nk; ++q)
+              tma_load_2d(ring + s * kChainStageBytes + q * kChainWBox, tw[a.gemm[p]], &full[s],
+                          (kb + q) * 64, j.tile * 128, pol);
           }
         }
       }
@@ -336,7 +418,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
       pdl_trigger();
     }
     __syncwarp();
-  } else if (warp == 2) {
+  } else if (warp == 10) {
     // ---------------- activation producer: waits for each phase's inputs
     pdl_wait();
     pdl_trigger();
@@ -360,14 +442,17 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
         }
         for (int i = 0; sc.get(g, i, j); ++i) {
           const int boxes = (j.nt + 63) >> 6;
-          for (int kb = j.k0; kb < j.k1; ++kb, ++gx) {
-            const int s = gx % kChainXStages;
-            if (gx >= kChainXStages)
-              mbar_wait(&x_empty[s], ((uint32_t)(gx / kChainXStages) - 1u) & 1u);
-            mbar_arrive_expect_tx(&x_full[s], (uint32_t)boxes * 8192u);
-            for (int b = 0; b < boxes; ++b)
-              tma_load_2d(xring + s * kChainXStage + b * 8192, tx[a.gemm[p]], &x_full[s], kb * 64,
-                          j.t0 + b * 64, pol);
+          for (int kb = j.k0; kb < j.k1; kb += kChainKS, ++gx) {
+            const int s = gx % kChainStages;
+            const int nk = min(kChainKS, j.k1 - kb);
+            if (gx >= kChainStages)
+              mbar_wait(&empty[s], ((uint32_t)(gx / kChainStages) - 1u) & 1u);
+            mbar_arrive_expect_tx(&full[s], (uint32_t)(nk * boxes) * 8192u);
+            uint8_t* xs = ring + s * kChainStageBytes + kChainKS * kChainWBox;
+            for (int q = 0; q < nk; ++q)
+              for (int b = 0; b < boxes; ++b)
+                tma_load_2d(xs + q * kChainXBlk + b * 8192, tx[a.gemm[p]], &full[s],
+                            (kb + q) * 64, j.t0 + b * 64, pol);
           }
         }
       }
@@ -378,7 +463,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
     pdl_wait();
     pdl_trigger();
     if (T < 0) T = row_count();
-    int gw = 0, gx = 0, jn = 0;
+    int gw = 0, jn = 0;
     for (int p = 0; p < a.n_phase && T > 0; ++p) {
       if (a.kind[p] != kPhGemmPartial && a.kind[p] != kPhGemmSwiGLU) continue;
       const ChainGemm& g = a.g[a.gemm[p]];
@@ -393,21 +478,23 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
           mbar_wait(&tmem_empty[buf], ((uint32_t)(jn >> 1) - 1u) & 1u);
           tc_fence_after();
         }
-        for (int kb = j.k0; kb < j.k1; ++kb, ++gw, ++gx) {
-          const int sw = gw % kChainWStages, sx = gx % kChainXStages;
-          mbar_wait(&w_full[sw], (uint32_t)(gw / kChainWStages) & 1u);
-          mbar_wait(&x_full[sx], (uint32_t)(gx / kChainXStages) & 1u);
+        for (int kb = j.k0; kb < j.k1; kb += kChainKS, ++gw) {
+          const int s = gw % kChainStages;
+          const int nk = min(kChainKS, j.k1 - kb);
+          mbar_wait(&full[s], (uint32_t)(gw / kChainStages) & 1u);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t wa = smem_u32(wring + sw * kChainWBox);
-            const uint32_t xa = smem_u32(xring + sx * kChainXStage);
+            for (int q = 0; q < nk; ++q) {
+              const uint32_t wa = smem_u32(ring + s * kChainStageBytes + q * kChainWBox);
+              const uint32_t xa =
+                  smem_u32(ring + s * kChainStageBytes + kChainKS * kChainWBox + q * kChainXBlk);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_ss(acc, umma_desc_kmajor<128>(wa + kk * 32),
-                          umma_desc_kmajor<128>(xa + kk * 32), idesc,
-                          (kb > j.k0 || kk > 0) ? 1u : 0u);
-            mma_commit(&w_empty[sw]);
-            mma_commit(&x_empty[sx]);
+              for (int kk = 0; kk < 4; ++kk)
+                mma_bf16_ss(acc, umma_desc_kmajor<128>(wa + kk * 32),
+                            umma_desc_kmajor<128>(xa + kk * 32), idesc,
+                            (kb > j.k0 || q > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&empty[s]);
           }
           __syncwarp();
         }
@@ -415,24 +502,24 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
         __syncwarp();
       }
     }
-  } else if (warp == 3) {
-    pdl_wait();
-    pdl_trigger();
   } else {
-    // ---------------- epilogue + glue warps 4..11
+    // ---------------- epilogue + glue warps 2..9
     pdl_wait();
     pdl_trigger();
     if (T < 0) T = row_count();
-    const int et = threadIdx.x - 128;          // 0..255
+    const bool stamp = a.dbg && c == 0 && threadIdx.x == 64;
+    if (stamp) a.dbg[0] = gtimer_ns();
+    const int et = threadIdx.x - 64;           // 0..255
     const int q = warp & 3;                    // TMEM lane quarter
-    const int grp = (warp - 4) >> 2;           // 0 / 1: alternating 32-token chunks
-    const bool issuer = (warp == 4 + 4 * grp) && lane == 0;
+    const int grp = (warp - 2) >> 2;           // 0 / 1: alternating 32-token chunks
+    const bool issuer = (warp == 2 + 4 * grp) && lane == 0;
     int jn = 0, wbuf = 0, sbuf = 0;
     for (int p = 0; p < a.n_phase; ++p) {
       const int kind = a.kind[p];
       if (p > 0) {   // inputs of this phase: every CTA finished phase p - 1
         if (et == 0) chain_wait_phase(a.bar, (unsigned)(G * p));
         asm volatile("bar.sync 1, %0;" ::"n"(kChainEpiThreads) : "memory");
+        if (stamp) a.dbg[1 + 2 * p] = gtimer_ns();       // phase p may start
       }
       bool stored = false;
       if (T > 0 && (kind == kPhGemmPartial || kind == kPhGemmSwiGLU)) {
@@ -523,6 +610,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
       }
       __threadfence();
       asm volatile("bar.sync 1, %0;" ::"n"(kChainEpiThreads) : "memory");
+      if (stamp) a.dbg[2 + 2 * p] = gtimer_ns();         // this CTA finished phase p
       if (et == 0) {
         const unsigned prev = atomicAdd(a.bar, 1u);
         // the last arrival of the last phase: every CTA is past every wait
@@ -635,7 +723,7 @@ int chain_add_glue(void* plan_v, int kind, const float* norm_w) {
 
 int chain_set_model(void* plan_v, const ChainModel& m) {
   ChainArgs& a = reinterpret_cast<ChainPlan*>(plan_v)->args;
-  if (m.d > 16 * kChainEpiThreads) return arg_fail("chain: d_model > 4096");
+  if (m.d > 8 * kChainEpiThreads) return arg_fail("chain: d_model > 2048");
   a.rows_cap = m.rows_cap;
   a.d = m.d;
   a.n_q = m.n_q;
@@ -657,6 +745,7 @@ int chain_set_model(void* plan_v, const ChainModel& m) {
   a.resid_part = m.part;
   a.bar = m.bar;
   a.t_pre_wait = m.t_pre_wait;
+  a.dbg = m.dbg;
   return SPECTRE_OK;
 }
 

@@ -28,6 +28,7 @@ struct ChainModel {
   float* part;              // split-K partials shared by the chain's GEMMs
   unsigned* bar;            // zeroed phase counter
   int t_pre_wait;           // 1: row count written launches back (see chain.cu)
+  unsigned long long* dbg;  // diagnostics (nullptr: off): per-phase globaltimer stamps
 };
 int chain_set_model(void* plan, const ChainModel& m);
 

@@ -109,6 +109,7 @@ struct ModelRT {
   std::vector<void*> ch_mid;
   void* ch_last = nullptr;
   unsigned* ch_bar = nullptr;
+  unsigned long long* ch_dbg = nullptr;   // SPECTRE_CHAIN_DBG: [L + 1][32] phase stamps
   ModelRT() = default;
   ModelRT(const ModelRT&) = delete;
   ModelRT& operator=(const ModelRT&) = delete;
@@ -188,6 +189,8 @@ struct ModelRT {
     amax_i = b.take<int>((size_t)n_blocks * R);
     rope = b.take<float2>((size_t)ctx_cap * dm.head_dim / 2);
     ch_bar = b.take<unsigned>(64);
+    if (use_chain && getenv("SPECTRE_CHAIN_DBG"))
+      ch_dbg = b.take<unsigned long long>((size_t)(dm.n_layers + 1) * 32);
     bt.tok = b.take<int>(R);
     bt.pos = b.take<int>(R);
     bt.slot = b.take<int>(R);
@@ -258,8 +261,10 @@ struct ModelRT {
     const size_t kv_layer = (size_t)n_req * dm.n_kv_heads * ctx_cap * dm.head_dim;
     auto* kc = reinterpret_cast<__nv_bfloat16*>(w.k_cache);
     auto* vc = reinterpret_cast<__nv_bfloat16*>(w.v_cache);
+    int chain_idx = 0;
     auto model = [&](int rope_layer, int pre_wait) {
       ChainModel m{};
+      m.dbg = ch_dbg ? ch_dbg + 32 * chain_idx++ : nullptr;
       m.rows_cap = rows_cap;
       m.d = d;
       m.n_q = dm.n_q_heads;
@@ -527,7 +532,7 @@ struct Engine {
       const bool on = v ? atoi(v) != 0 : true;
       const int qd = d.n_q_heads * d.head_dim, nq = (d.n_q_heads + 2 * d.n_kv_heads) * d.head_dim;
       return on && d.d_model % 128 == 0 && nq % 128 == 0 && (2 * d.ffn) % 128 == 0 &&
-             qd % 64 == 0 && d.ffn % 64 == 0 && d.d_model <= 4096;
+             qd % 64 == 0 && d.ffn % 64 == 0 && d.d_model <= 2048;
     }();
     tgt.tile_rows = tile_rows_default(256);
     st.n_req = c.n_req;
@@ -887,6 +892,17 @@ extern "C" int spectre_engine_run(void* engine, int32_t max_rounds, int32_t use_
     *rounds_run = c.round - c.round_base;
   }
   return SPECTRE_OK;
+}
+
+// Diagnostics: the draft chains' last per-phase globaltimer stamps (CTA 0),
+// [n_layers + 1][32] u64 — only with SPECTRE_CHAIN_DBG set at engine creation.
+extern "C" int spectre_engine_chain_stamps(void* engine, uint64_t* out, int32_t n) {
+  auto* e = reinterpret_cast<Engine*>(engine);
+  if (!e || !out || !e->drf.ch_dbg) return arg_fail("spectre_engine_chain_stamps");
+  const int have = (e->drf.dm.n_layers + 1) * 32;
+  SPECTRE_CUDA_TRY(cudaMemcpy(out, e->drf.ch_dbg, (size_t)std::min(n, have) * 8,
+                              cudaMemcpyDeviceToHost));
+  return std::min(n, have);
 }
 
 extern "C" int spectre_engine_graph_status(void* engine) {
