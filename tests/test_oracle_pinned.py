@@ -112,3 +112,18 @@ def test_out_of_domain_is_refused():
     # conservative round whose replies miss the reply deadline (timeouts)
     with pytest.raises(L.OutOfDomain):
         L.run(dict(batch_size=4, n_requests=4, output_len=8, t_draft=0.03), "parallel")
+
+
+def test_scheduler_restatement_matches_reference():
+    """oracle/scheduler.py:schedule_round == the reference's schedule_round
+    (draft_engine.py:134-155) on 400 random queues (tests/golden/scheduler.json)."""
+    from pathlib import Path
+
+    from oracle import scheduler as S
+    golden = Path(__file__).resolve().parent / "golden" / "scheduler.json"
+    for c in json.loads(golden.read_text())["cases"]:
+        spec, reg, counter, forced = S.schedule_round(list(range(c["n_spec"])),
+                                                      list(range(c["n_reg"])), c["counter"],
+                                                      c["period"], c["capacity"])
+        assert (spec, reg, counter, forced) == (c["spec"], c["reg"], c["counter_after"],
+                                                c["forced"]), c
