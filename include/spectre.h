@@ -245,6 +245,17 @@ typedef struct SpectreDecodeConfig {
                                  sees only the first and the last `keep` prompt
                                  tokens, re-indexed to positions 0 .. 2 keep - 1;
                                  0 (or 2 keep >= prompt_len): the whole prompt */
+  /* background (regular) tenants of the draft model and the speculative-priority
+   * fairness scheduler (draft_engine.py:134-155, 302-394; core.py:79-85):
+   * background_requests greedy draft-model requests of background_output_len
+   * tokens share every draft round with the speculative queries; a round
+   * serves at most draft_capacity items, speculative first; after
+   * fairness_period consecutive speculative rounds with regular work waiting,
+   * one round serves regular items only.  0 requests: no background load. */
+  int32_t background_requests;
+  int32_t background_output_len;
+  int32_t fairness_period;
+  int32_t draft_capacity;
 } SpectreDecodeConfig;
 
 #define SPECTRE_ROLE_BOTH 0
@@ -333,12 +344,20 @@ typedef struct SpectreRoundTrace {
   double* r_star;
   int32_t* n_stale;         /* queried requests whose reply was missing or
                                superseded at commit (target_engine.py:314-331) */
+  int32_t* n_regular;       /* background items scheduled with this round's speculation */
+  int32_t* n_forced;        /* background items of a forced regular round (0: none) */
+  int32_t* fair_counter;    /* FairnessCounter.consecutive_speculative after the round */
 } SpectreRoundTrace;
 int spectre_engine_read(void* engine, int64_t* committed, int32_t* committed_pos,
                         const SpectreRoundTrace* trace, int32_t* n_rounds, void* stream);
 /* Asynchronous device-to-device copy of the committed tokens (int64,
  * [n_req][output_len]) on `stream` — the per-step output of the decode. */
 int spectre_engine_read_committed(void* engine, int64_t* committed, void* stream);
+/* Background tenants: generated tokens [background_requests][background_output_len]
+ * int32 and per-request counts (device pointers), totals[2] = {tokens generated,
+ * requests completed} (host).  Synchronous. */
+int spectre_engine_read_background(void* engine, int32_t* tokens, int32_t* emitted,
+                                   int32_t* totals, void* stream);
 /* One forward pass over a packed ragged batch (tests / roofline):
  * which 0 = target, 1 = draft.  tok/pos/slot [T]; per request q_off, n_new,
  * pos0 [n_req] (n_new 0 = not participating).  out_tok [T] greedy argmax;

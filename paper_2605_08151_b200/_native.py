@@ -112,12 +112,15 @@ class DecodeConfig(C.Structure):
                 ("t_target", C.c_double), ("t_draft", C.c_double), ("ema_decay", C.c_double),
                 ("fixed_threshold_l", C.c_double), ("temperature", C.c_double),
                 ("role", C.c_int32), ("breaker_threshold", C.c_int32),
-                ("breaker_cooldown", C.c_int32), ("draft_prompt_keep", C.c_int32)]
+                ("breaker_cooldown", C.c_int32), ("draft_prompt_keep", C.c_int32),
+                ("background_requests", C.c_int32), ("background_output_len", C.c_int32),
+                ("fairness_period", C.c_int32), ("draft_capacity", C.c_int32)]
 
 
 TRACE_FIELDS = ("mode", "participants", "delta", "n_roll", "content_sum", "content_n",
                 "n_padded", "t_round_ns", "t_verify_ns", "t_draft_ns", "r_hat_ema",
-                "accepted_len_ema", "r_star", "n_stale")
+                "accepted_len_ema", "r_star", "n_stale", "n_regular", "n_forced",
+                "fair_counter")
 
 
 class RoundTraceBufs(C.Structure):
@@ -148,6 +151,7 @@ def _bind_model(L) -> None:
     _sig(L, "spectre_engine_read", C.c_int,
          [_P, _P, _P, C.POINTER(RoundTraceBufs), C.POINTER(i32), _P])
     _sig(L, "spectre_engine_read_committed", C.c_int, [_P, _P, _P])
+    _sig(L, "spectre_engine_read_background", C.c_int, [_P, _P, _P, C.POINTER(i32), _P])
     _sig(L, "spectre_engine_forward", C.c_int,
          [_P, i32, _P, _P, _P, i32, _P, _P, _P, _P, _P, _P])
 

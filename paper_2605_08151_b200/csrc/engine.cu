@@ -447,7 +447,8 @@ struct Engine {
     *cs = prefill_chunk(c.n_req);
     *dnew = 2 * c.gamma + 4;
     *rows_t = round_up(std::max(c.n_req * (c.gamma + 1), c.n_req * *cs), 64);
-    *rows_d = round_up(std::max(c.n_req * *dnew, c.n_req * *cs), 64);
+    const int nd = c.n_req + std::max(0, c.background_requests);   // + background entries
+    *rows_d = round_up(std::max(c.n_req * *dnew + nd - c.n_req, nd * *cs), 64);
   }
 
   void layout(Bump& b) {
@@ -478,7 +479,17 @@ struct Engine {
     st.hist = b.take<uint64_t>((size_t)n * st.hist_cap);
     st.cached_tok = b.take<uint64_t>((size_t)n * G);
     st.cand_tok = b.take<uint64_t>((size_t)n * G);
-    if (st.dprompt_len < cfg.prompt_len) dprompts = b.take<int>((size_t)n * st.dprompt_len);
+    if (st.dprompt_len < cfg.prompt_len || st.n_bg > 0)
+      dprompts = b.take<int>((size_t)(n + st.n_bg) * st.dprompt_len);
+    if (st.n_bg > 0) {
+      const int nb = st.n_bg;
+      st.bg_remaining = b.take<int>(nb);
+      st.bg_ctx = b.take<int>(nb);
+      st.bg_last = b.take<int>(nb);
+      st.bg_emitted = b.take<int>(nb);
+      st.bg_round_left = b.take<int>(nb);
+      st.bg_out = b.take<int>((size_t)nb * st.bg_out_len);
+    }
     st.ctrl = b.take<CtrlDev>(1);
     const int R = cfg.max_rounds;
     st.trace.mode = b.take<int>(R);
@@ -495,6 +506,9 @@ struct Engine {
     st.trace.accepted_len_ema = b.take<double>(R);
     st.trace.r_star = b.take<double>(R);
     st.trace.n_stale = b.take<int>(R);
+    st.trace.n_regular = b.take<int>(R);
+    st.trace.n_forced = b.take<int>(R);
+    st.trace.fair_counter = b.take<int>(R);
     if (st.sampling) {
       st.samp_a = b.take<int>(n);
       st.samp_bonus = b.take<int>(n);
@@ -517,7 +531,7 @@ struct Engine {
     tgt.max_new = std::max(c.gamma + 1, prefill_cs);
     drf.dm = d;
     drf.w = dw;
-    drf.n_req = c.n_req;
+    drf.n_req = c.n_req + std::max(0, c.background_requests);   // KV slots n_req.. : background
     drf.rows_cap = rd;
     drf.ctx_cap = c.ctx_cap;
     drf.max_new = std::max(draft_new_max, prefill_cs);
@@ -541,6 +555,10 @@ struct Engine {
     st.prompt_len = c.prompt_len;
     st.dprompt_len = (c.draft_prompt_keep > 0 && 2 * c.draft_prompt_keep < c.prompt_len)
                          ? 2 * c.draft_prompt_keep : c.prompt_len;
+    st.n_bg = std::max(0, c.background_requests);
+    st.bg_out_len = c.background_output_len > 0 ? c.background_output_len : 128;
+    st.fair_period = c.fairness_period > 0 ? c.fairness_period : 10;
+    st.draft_cap = c.draft_capacity > 0 ? c.draft_capacity : 256;
     st.vocab = d.vocab;
     st.variant = c.variant;
     st.controller = c.controller;
@@ -568,6 +586,11 @@ struct Engine {
 
   // ---- round pieces
   int draft_phase(int which, cudaStream_t s) {
+    if (st.n_bg > 0) {   // a forced regular round (regular items only, one step), if due
+      TRY(launch_bg_forced_prep(st, drf.bt, which, s));
+      TRY(drf.forward(1, s, nullptr, false));
+      TRY(launch_bg_forced_append(st, drf.bt, s));
+    }
     TRY(launch_draft_prep(st, drf.bt, which, s));
     const int steps = which == 'O' ? cfg.gamma - 1 : cfg.gamma;   // 'M': the longest query
     for (int i = 0; i < steps; ++i) {
@@ -780,6 +803,16 @@ extern "C" void* spectre_engine_create(const SpectreModelDims* target,
     arg_fail("spectre_engine_create: decode config");
     return nullptr;
   }
+  if (cfg->background_requests > 0 &&
+      (cfg->role != SPECTRE_ROLE_BOTH || cfg->temperature > 0.0 ||
+       (cfg->draft_capacity > 0 ? cfg->draft_capacity : 256) < cfg->n_req ||
+       cfg->n_req + cfg->background_requests > 1024 ||
+       cfg->prompt_len + (cfg->background_output_len > 0 ? cfg->background_output_len : 128) + 8 >
+           cfg->ctx_cap)) {
+    arg_fail("spectre_engine_create: background tenants need role both, greedy decoding, "
+             "draft_capacity >= n_req, n_req + background <= 1024 and KV room for their output");
+    return nullptr;
+  }
   if (cfg->temperature > 0.0 && cfg->alpha < 1.0) {
     // rejection sampling tests min(1, p/q) against the draft's q; the alpha
     // noise would replace the proposal by a token not drawn from q
@@ -835,23 +868,31 @@ extern "C" int spectre_engine_prefill(void* engine, const int32_t* prompts, void
     if ((m == &e->drf && e->cfg.role == SPECTRE_ROLE_TARGET) ||
         (m == &e->tgt && e->cfg.role == SPECTRE_ROLE_DRAFT))
       continue;   // disaggregated: this side holds only one model
-    // the draft prefills its (possibly compressed) prompt view
+    // the draft prefills its prompt view: the (possibly compressed) prompts,
+    // then the background requests' prompts
     const int* src = prompts;
     int P = e->cfg.prompt_len;
     if (m == &e->drf && e->dprompts) {
-      TRY(launch_compress_prompts(prompts, P, e->cfg.draft_prompt_keep, e->cfg.n_req, e->dprompts,
-                                  s));
+      if (e->st.dprompt_len < P)
+        TRY(launch_compress_prompts(prompts, P, e->cfg.draft_prompt_keep, e->cfg.n_req,
+                                    e->dprompts, s));
+      else
+        SPECTRE_CUDA_TRY(cudaMemcpyAsync(e->dprompts, prompts, (size_t)e->cfg.n_req * P * 4,
+                                         cudaMemcpyDeviceToDevice, s));
       src = e->dprompts;
       P = e->st.dprompt_len;
+      TRY(launch_bg_prompts(e->cfg.seed, e->cfg.n_req, e->st.n_bg, P, e->drf.dm.vocab,
+                            e->dprompts, s));
     }
     for (int c0 = 0; c0 < P; c0 += cs) {
-      TRY(launch_prefill_batch(src, P, e->cfg.n_req, c0, cs, m->bt, s));
+      TRY(launch_prefill_batch(src, P, m->n_req, c0, cs, m->bt, s));
       // only the target's prediction at the last prompt position is read
       // (admission commits it as output token 0)
       TRY(m->forward(cs, s, nullptr, true, m == &e->tgt && c0 + cs >= P));
     }
   }
   TRY(launch_admit(e->st, e->tgt.bt, s));
+  if (e->cfg.role == SPECTRE_ROLE_BOTH) TRY(launch_bg_init(e->st, e->dprompts, e->st.dprompt_len, s));
   return SPECTRE_OK;
 }
 
@@ -956,6 +997,31 @@ extern "C" int spectre_engine_read(void* engine, int64_t* committed, int32_t* co
     TRY(cp(trace->accepted_len_ema, t.accepted_len_ema, R * 8));
     TRY(cp(trace->r_star, t.r_star, R * 8));
     TRY(cp(trace->n_stale, t.n_stale, R * 4));
+    TRY(cp(trace->n_regular, t.n_regular, R * 4));
+    TRY(cp(trace->n_forced, t.n_forced, R * 4));
+    TRY(cp(trace->fair_counter, t.fair_counter, R * 4));
+  }
+  return SPECTRE_OK;
+}
+
+extern "C" int spectre_engine_read_background(void* engine, int32_t* tokens, int32_t* emitted,
+                                              int32_t* totals, void* stream) {
+  auto* e = reinterpret_cast<Engine*>(engine);
+  if (!e || e->st.n_bg <= 0) return arg_fail("spectre_engine_read_background: no background");
+  cudaStream_t s = as_stream(stream);
+  if (tokens)
+    SPECTRE_CUDA_TRY(cudaMemcpyAsync(tokens, e->st.bg_out,
+                                     (size_t)e->st.n_bg * e->st.bg_out_len * 4,
+                                     cudaMemcpyDeviceToDevice, s));
+  if (emitted)
+    SPECTRE_CUDA_TRY(cudaMemcpyAsync(emitted, e->st.bg_emitted, (size_t)e->st.n_bg * 4,
+                                     cudaMemcpyDeviceToDevice, s));
+  CtrlDev c;
+  SPECTRE_CUDA_TRY(cudaMemcpyAsync(&c, e->st.ctrl, sizeof(c), cudaMemcpyDeviceToHost, s));
+  SPECTRE_CUDA_TRY(cudaStreamSynchronize(s));
+  if (totals) {
+    totals[0] = c.bg_tokens;
+    totals[1] = c.bg_completed;
   }
   return SPECTRE_OK;
 }
@@ -991,9 +1057,11 @@ extern "C" int spectre_engine_forward(void* engine, int32_t which, const int32_t
   SPECTRE_CUDA_TRY(d2d(m.bt.q_off, q_off, (size_t)n * 4));
   SPECTRE_CUDA_TRY(d2d(m.bt.n_new, n_new, (size_t)n * 4));
   SPECTRE_CUDA_TRY(d2d(m.bt.pos0, pos0, (size_t)n * 4));
-  std::vector<int> ident(n);
-  for (int i = 0; i < n; ++i) ident[i] = i;
-  SPECTRE_CUDA_TRY(cudaMemcpyAsync(m.bt.rslot, ident.data(), (size_t)n * 4,
+  if (m.n_req > n)   // the draft's background entries do not take part
+    SPECTRE_CUDA_TRY(cudaMemsetAsync(m.bt.n_new + n, 0, (size_t)(m.n_req - n) * 4, s));
+  std::vector<int> ident(m.n_req);
+  for (int i = 0; i < m.n_req; ++i) ident[i] = i;
+  SPECTRE_CUDA_TRY(cudaMemcpyAsync(m.bt.rslot, ident.data(), (size_t)m.n_req * 4,
                                    cudaMemcpyHostToDevice, s));
   SPECTRE_CUDA_TRY(cudaMemcpyAsync(m.bt.t_dev, &T, 4, cudaMemcpyHostToDevice, s));
   int max_new = 1;

@@ -47,6 +47,11 @@ struct CtrlDev {
   // circuit breaker (target_engine.py:337-380); round ids are 1-based as in sim.py:519
   int streak, disabled_until, activations;
   int n_stale;       // this round: queried requests without a matching reply
+  // background (regular) draft tenants and the speculative-priority fairness
+  // scheduler (draft_engine.py:134-155, 302-394): FairnessCounter, totals, and
+  // this round's schedule (regular items in the forced round / the round that
+  // served the speculative queries)
+  int fair_counter, bg_tokens, bg_completed, ph_forced, ph_regular;
 };
 
 struct RoundTraceDev {
@@ -64,6 +69,9 @@ struct RoundTraceDev {
   double* accepted_len_ema;
   double* r_star;
   int* n_stale;
+  int* n_regular;     // regular items scheduled with this round's speculation
+  int* n_forced;      // regular items of a forced regular round (0: none)
+  int* fair_counter;  // FairnessCounter.consecutive_speculative after the round
 };
 
 struct DecodeStateDev {
@@ -107,6 +115,15 @@ struct DecodeStateDev {
   int* q_serial;
   int* r_round;          // [n_req] tag of the reply held in hist / gen_* (draft stamps)
   int* r_serial;
+  // background tenants: draft-model requests decoding autoregressively in the
+  // draft's KV slots n_req .. n_req + n_bg - 1 (batch entries b = n_req + j)
+  int n_bg, bg_out_len, fair_period, draft_cap;
+  int* bg_remaining;     // [n_bg] tokens still to generate
+  int* bg_ctx;           // [n_bg] positions with KV = the next input's position
+  int* bg_last;          // [n_bg] next input token
+  int* bg_emitted;       // [n_bg] tokens generated so far
+  int* bg_round_left;    // [n_bg] tokens still to emit in the current draft round
+  int* bg_out;           // [n_bg][bg_out_len] generated tokens
 };
 
 // launchers (model_protocol.cu)
@@ -118,6 +135,12 @@ int launch_admit(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);
 int launch_round_begin(const DecodeStateDev& st, cudaStream_t s);
 int launch_set_round_limit(const DecodeStateDev& st, int extra, cudaStream_t s);
 int launch_draft_prep(const DecodeStateDev& st, const BatchDev& bt, int which, cudaStream_t s);
+int launch_bg_prompts(uint64_t seed, int n_req, int n_bg, int P, int vocab, int* out,
+                      cudaStream_t s);
+int launch_bg_init(const DecodeStateDev& st, const int* dprompts, int P, cudaStream_t s);
+int launch_bg_forced_prep(const DecodeStateDev& st, const BatchDev& bt, int which,
+                          cudaStream_t s);
+int launch_bg_forced_append(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);
 int launch_draft_append(const DecodeStateDev& st, const BatchDev& bt, int which, int last,
                         cudaStream_t s);
 int launch_verify_prep(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);

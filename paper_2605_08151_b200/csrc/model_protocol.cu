@@ -99,6 +99,7 @@ __global__ void k_admit(DecodeStateDev s, BatchDev bt) {
     c.r_star = 0.0;
     c.streak = c.disabled_until = c.activations = 0;
     c.n_stale = 0;
+    c.fair_counter = c.bg_tokens = c.bg_completed = c.ph_forced = c.ph_regular = 0;
   }
   if (b >= s.n_req) return;
   s.req_mode[b] = 0;
@@ -148,6 +149,7 @@ __device__ int round_choose_mode(DecodeStateDev& s, CtrlDev& c) {
   c.t_draft_begin = c.t_draft_end = 0;
   c.draft_steps = 0;
   c.n_stale = 0;
+  c.ph_forced = c.ph_regular = 0;
   int mode = 0;
   if (c.n_active > 0 && c.error == 0 && c.round < s.max_rounds && c.round < c.round_limit) {
     if (s.variant == SPECTRE_VARIANT_AR) mode = 'F';
@@ -212,6 +214,111 @@ __device__ int round_choose_mode(DecodeStateDev& s, CtrlDev& c) {
   return mode;
 }
 
+// ------------------------------------------------------------ background tenants
+// Regular (non-speculative) draft-model requests sharing the draft server
+// (draft_engine.py:302-394): background request j decodes greedily in the
+// draft's KV slot n_req + j, batch entry b = n_req + j.  Each draft round
+// schedules speculative items first and fills the remaining capacity with
+// ready regular items in FIFO order; once `fair_period` consecutive rounds
+// served speculation while regular work waited, one round serves only regular
+// items (schedule_round, draft_engine.py:134-155).  A scheduled regular item
+// emits min(remaining, steps) tokens, one per draft step (:389-394).
+
+// Synthetic background prompts: TokenStreamOracle prompt stream of request ids
+// 1,000,000 + j (sim.py _BG_BASE) mod V, written after the n_req speculative rows.
+__global__ void k_bg_prompts(uint64_t seed, int n_req, int n_bg, int P, int vocab, int* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_bg * P; i += gridDim.x * blockDim.x) {
+    const int j = i / P, k = i % P;
+    out[(size_t)(n_req + j) * P + k] =
+        (int)(stream_token(seed, 1, 1000000ull + (uint64_t)j, (uint64_t)k) % (uint64_t)vocab);
+  }
+}
+
+// After the draft's prefill: every background request re-feeds its last prompt
+// token (its KV is recomputed bit-identically) and owes bg_out_len tokens.
+__global__ void k_bg_init(DecodeStateDev s, const int* dprompts, int P) {
+  pdl_wait();
+  pdl_trigger();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= s.n_bg) return;
+  s.bg_remaining[j] = s.bg_out_len;
+  s.bg_ctx[j] = P - 1;
+  s.bg_last[j] = dprompts[(size_t)(s.n_req + j) * P + P - 1];
+  s.bg_emitted[j] = 0;
+  s.bg_round_left[j] = 0;
+}
+
+// The draft's greedy token for background request j (row `row` of the pass).
+__device__ __forceinline__ void bg_consume(DecodeStateDev& s, const BatchDev& bt, int j, int row) {
+  const int tok = bt.out_tok[row];
+  if (s.bg_emitted[j] < s.bg_out_len) s.bg_out[(size_t)j * s.bg_out_len + s.bg_emitted[j]] = tok;
+  s.bg_emitted[j] += 1;
+  s.bg_last[j] = tok;
+  s.bg_ctx[j] += 1;
+  s.bg_remaining[j] -= 1;
+  s.bg_round_left[j] -= 1;
+  atomicAdd(&s.ctrl->bg_tokens, 1);
+  if (s.bg_remaining[j] == 0) atomicAdd(&s.ctrl->bg_completed, 1);
+}
+
+// FIFO rank of background entry b among the ready ones (block-wide; every
+// thread of the block must call it).  *total = ready count.
+__device__ int bg_ready_rank(const DecodeStateDev& s, int b, bool ready, int* total, int* sh) {
+  int rank = 0;
+  *total = block_exclusive_scan(ready ? 1 : 0, &rank, b - s.n_req, s.n_bg, sh);
+  return rank;
+}
+
+// Phase start: a forced regular round (one step, regular items only) when the
+// counter is due and regular work waits; otherwise an empty pass.
+__global__ void __launch_bounds__(kProtoThreads) k_bg_forced_prep(DecodeStateDev s, BatchDev bt,
+                                                                  int which_mode) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int sh[kProtoThreads];
+  __shared__ int s_forced;
+  CtrlDev& c = *s.ctrl;
+  const int b = threadIdx.x;
+  const int nb = s.n_req + s.n_bg;
+  const bool selected = which_mode == 'M' || c.mode == which_mode;
+  if (threadIdx.x == 0 && selected) c.t_draft_begin = globaltimer();
+  const int j = b - s.n_req;
+  const bool ready = selected && j >= 0 && j < s.n_bg && s.bg_remaining[j] > 0;
+  int total = 0;
+  const int rank = bg_ready_rank(s, b, ready, &total, sh);
+  if (threadIdx.x == 0) {
+    s_forced = (selected && total > 0 && c.fair_counter >= s.fair_period) ? 1 : 0;
+    c.ph_forced = s_forced ? min(total, s.draft_cap) : 0;
+    if (s_forced) c.fair_counter = 0;
+  }
+  __syncthreads();
+  const bool sched = s_forced && ready && rank < s.draft_cap;
+  if (j >= 0 && j < s.n_bg) s.bg_round_left[j] = sched ? 1 : 0;
+  int off = 0;
+  const int rows = block_exclusive_scan(sched ? 1 : 0, &off, b, nb, sh);
+  if (b < nb) {
+    bt.q_off[b] = off;
+    bt.n_new[b] = sched ? 1 : 0;
+    bt.rslot[b] = b;
+    if (sched) {
+      bt.pos0[b] = s.bg_ctx[j];
+      bt.tok[off] = s.bg_last[j];
+      bt.pos[off] = s.bg_ctx[j];
+      bt.slot[off] = b;
+    }
+  }
+  if (threadIdx.x == 0) *bt.t_dev = rows;
+}
+
+__global__ void __launch_bounds__(kProtoThreads) k_bg_forced_append(DecodeStateDev s,
+                                                                    BatchDev bt) {
+  pdl_wait();
+  pdl_trigger();
+  const int j = threadIdx.x;
+  if (j < s.n_bg && s.bg_round_left[j] > 0 && bt.n_new[s.n_req + j] > 0)
+    bg_consume(s, bt, j, bt.q_off[s.n_req + j]);
+}
+
 // ------------------------------------------------------------ draft phase
 // which_mode: 'O' (repair gamma-1 tokens anchored at committed_pos) or 'P'
 // (speculate gamma tokens from the history tail).  Sync + rebase + catch-up
@@ -226,10 +333,11 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_prep(DecodeStateDev s, 
   const bool mixed = which_mode == 'M';   // per-request modes (disaggregated shards)
   if (!mixed && mode != which_mode) {  // phase not selected this round: empty batch
     if (threadIdx.x == 0) *bt.t_dev = 0;
-    if (threadIdx.x < s.n_req) bt.n_new[threadIdx.x] = 0;
+    if (threadIdx.x < s.n_req + s.n_bg) bt.n_new[threadIdx.x] = 0;
     return;
   }
-  if (threadIdx.x == 0) c.t_draft_begin = globaltimer();
+  // with background tenants the phase started at the forced-round slot
+  if (threadIdx.x == 0 && s.n_bg == 0) c.t_draft_begin = globaltimer();
   const int b = threadIdx.x;
   int n_new = 0, kvd = 0, hl = 0;
   if (b < s.n_req) {
@@ -266,8 +374,39 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_prep(DecodeStateDev s, 
       s.gen_start[b] = hl;
     }
   }
+  if (s.n_bg > 0) {
+    // the round serving this phase's queries: speculative items first, the
+    // remaining capacity to ready regular items (FIFO); steps = the queries'
+    // count, 1 without speculation (draft_engine.py:134-155, 334-344)
+    const int n_spec = __syncthreads_count(b < s.n_req && s.gen_count[b] > 0);
+    const int j = b - s.n_req;
+    const bool ready = j >= 0 && j < s.n_bg && s.bg_remaining[j] > 0;
+    int n_ready = 0;
+    const int rank = bg_ready_rank(s, b, ready, &n_ready, sh);
+    const int reg_cap = max(0, s.draft_cap - n_spec);
+    const bool sched = ready && rank < reg_cap;
+    const int steps_ref = n_spec > 0 ? (which_mode == 'O' ? s.gamma - 1 : s.gamma) : 1;
+    if (j >= 0 && j < s.n_bg) s.bg_round_left[j] = sched ? min(s.bg_remaining[j], steps_ref) : 0;
+    if (sched) n_new = 1;
+    if (threadIdx.x == 0) {
+      c.ph_regular = min(n_ready, reg_cap);
+      c.fair_counter = n_spec > 0 ? min(c.fair_counter + 1, s.fair_period) : 0;
+    }
+  }
   int off = 0;
-  const int total = block_exclusive_scan(n_new, &off, b, s.n_req, sh);
+  const int total = block_exclusive_scan(n_new, &off, b, s.n_req + s.n_bg, sh);
+  if (b >= s.n_req && b < s.n_req + s.n_bg) {   // background rows
+    const int j = b - s.n_req;
+    bt.q_off[b] = off;
+    bt.n_new[b] = n_new;
+    bt.rslot[b] = b;
+    if (n_new) {
+      bt.pos0[b] = s.bg_ctx[j];
+      bt.tok[off] = s.bg_last[j];
+      bt.pos[off] = s.bg_ctx[j];
+      bt.slot[off] = b;
+    }
+  }
   if (b < s.n_req) {
     bt.q_off[b] = off;
     bt.n_new[b] = n_new;
@@ -294,11 +433,16 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_append(DecodeStateDev s
   CtrlDev& c = *s.ctrl;
   if (which_mode != 'M' && c.mode != which_mode) {
     if (threadIdx.x == 0) *bt.t_dev = 0;
-    if (threadIdx.x < s.n_req) bt.n_new[threadIdx.x] = 0;
+    if (threadIdx.x < s.n_req + s.n_bg) bt.n_new[threadIdx.x] = 0;
     return;
   }
   const int b = threadIdx.x;
   int n_new = 0;
+  const int jb = b - s.n_req;   // background entry
+  if (jb >= 0 && jb < s.n_bg && bt.n_new[b] > 0 && s.bg_round_left[jb] > 0) {
+    bg_consume(s, bt, jb, bt.q_off[b]);
+    if (s.bg_round_left[jb] > 0) n_new = 1;
+  }
   if (b < s.n_req && s.gen_count[b] > 0 && s.gen_done[b] < s.gen_count[b]) {
     const int row = bt.q_off[b] + bt.n_new[b] - 1;
     uint64_t* h = s.hist + (size_t)b * s.hist_cap;
@@ -311,7 +455,17 @@ __global__ void __launch_bounds__(kProtoThreads) k_draft_append(DecodeStateDev s
     if (s.gen_done[b] < s.gen_count[b]) n_new = 1;
   }
   int off = 0;
-  const int total = block_exclusive_scan(n_new, &off, b, s.n_req, sh);
+  const int total = block_exclusive_scan(n_new, &off, b, s.n_req + s.n_bg, sh);
+  if (jb >= 0 && jb < s.n_bg) {
+    bt.q_off[b] = off;
+    bt.n_new[b] = n_new;
+    if (n_new) {
+      bt.pos0[b] = s.bg_ctx[jb];
+      bt.tok[off] = s.bg_last[jb];
+      bt.pos[off] = s.bg_ctx[jb];
+      bt.slot[off] = b;
+    }
+  }
   if (b < s.n_req) {
     bt.q_off[b] = off;
     bt.n_new[b] = n_new;
@@ -574,6 +728,9 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
       s.trace.r_hat_ema[ri] = c.ema;
       s.trace.accepted_len_ema[ri] = c.has_L ? c.L : 0.0;
       s.trace.r_star[ri] = c.r_star;
+      s.trace.n_regular[ri] = c.ph_regular;
+      s.trace.n_forced[ri] = c.ph_forced;
+      s.trace.fair_counter[ri] = c.fair_counter;
     }
     c.round = ri + 1;
     if (s.use_handles)
@@ -603,6 +760,30 @@ __global__ void k_set_round_limit(DecodeStateDev s, int extra) {
 }
 
 // ------------------------------------------------------------------ launchers
+int launch_bg_prompts(uint64_t seed, int n_req, int n_bg, int P, int vocab, int* out,
+                      cudaStream_t s) {
+  if (n_bg <= 0) return SPECTRE_OK;
+  k_bg_prompts<<<(n_bg * P + 255) / 256, 256, 0, s>>>(seed, n_req, n_bg, P, vocab, out);
+  SPECTRE_LAUNCH_CHECK("k_bg_prompts");
+  return SPECTRE_OK;
+}
+int launch_bg_init(const DecodeStateDev& st, const int* dprompts, int P, cudaStream_t s) {
+  if (st.n_bg <= 0) return SPECTRE_OK;
+  SPECTRE_LAUNCH_PDL("k_bg_init", k_bg_init, dim3((st.n_bg + 255) / 256), dim3(256), 0, s, st,
+                     dprompts, P);
+  return SPECTRE_OK;
+}
+int launch_bg_forced_prep(const DecodeStateDev& st, const BatchDev& bt, int which,
+                          cudaStream_t s) {
+  SPECTRE_LAUNCH_PDL("k_bg_forced_prep", k_bg_forced_prep, dim3(1), dim3(kProtoThreads), 0, s,
+                     st, bt, which);
+  return SPECTRE_OK;
+}
+int launch_bg_forced_append(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s) {
+  SPECTRE_LAUNCH_PDL("k_bg_forced_append", k_bg_forced_append, dim3(1), dim3(kProtoThreads), 0,
+                     s, st, bt);
+  return SPECTRE_OK;
+}
 int launch_set_round_limit(const DecodeStateDev& st, int extra, cudaStream_t s) {
   SPECTRE_LAUNCH_PDL("k_set_round_limit", k_set_round_limit, dim3(1), dim3(1), 0, s, st, extra);
   return SPECTRE_OK;

@@ -134,17 +134,20 @@ class ModelPair:
     draft: ModelWeights
     n_req: int
     ctx_cap: int
+    n_bg: int = 0       # extra draft KV slots for background tenants
 
 
 def build_pair(target: ModelSpec, draft: ModelSpec, n_req: int, ctx_cap: int, seed: int = 0,
-               target_branch: float = 0.08, draft_branch: float = 0.08) -> ModelPair:
-    """Random-init target/draft coupled through a shared lifted backbone (H6)."""
+               target_branch: float = 0.08, draft_branch: float = 0.08,
+               n_bg: int = 0) -> ModelPair:
+    """Random-init target/draft coupled through a shared lifted backbone (H6).
+    n_bg: draft KV slots for background (regular) tenants of the draft server."""
     torch = _native.require_cuda()
     if target.vocab != draft.vocab:
         raise ValueError("target and draft must share a vocabulary")
     gen = torch.Generator(device="cuda").manual_seed(seed)
     T = ModelWeights(target, n_req, ctx_cap)
-    D = ModelWeights(draft, n_req, ctx_cap)
+    D = ModelWeights(draft, n_req + n_bg, ctx_cap)
     V, dD, dT = draft.vocab, draft.d_model, target.d_model
     D.embed.copy_(torch.randn(V, dD, generator=gen, device="cuda"))
     D.lm_head.copy_(torch.randn(V, dD, generator=gen, device="cuda") / math.sqrt(dD))
@@ -159,7 +162,7 @@ def build_pair(target: ModelSpec, draft: ModelSpec, n_req: int, ctx_cap: int, se
     D.init_layers(gen, draft_branch)
     T.init_layers(gen, target_branch)
     torch.cuda.synchronize()
-    return ModelPair(T, D, n_req, ctx_cap)
+    return ModelPair(T, D, n_req, ctx_cap, n_bg)
 
 
 CONTROLLERS = {"reference": 0, "measured": 1, "round": 2}
@@ -187,6 +190,12 @@ class DecodeSpec:
     compression_p: float = 1.0      # draft prompt compression (core.py compression_p,
                                     # draft_engine.py:123-131): keep floor(p*S/2) head and
                                     # tail prompt tokens in the draft's KV cache
+    # background (regular) tenants of the draft model + the speculative-priority
+    # fairness scheduler (core.py:79-85, draft_engine.py:134-155, 302-394)
+    background_requests: int = 0
+    background_output_len: int = 128
+    fairness_period: int = 10
+    draft_capacity: int = 256
 
     def draft_prompt_keep(self) -> int:
         """compress_prompt (draft_engine.py:123-131): keep = int((p / 2) * S); no
@@ -232,6 +241,8 @@ class SpectreEngine:
             raise ValueError(f"KV capacity {pair.ctx_cap} < needed {spec.ctx_cap()}")
         if spec.n_req != pair.n_req:
             raise ValueError("n_req must match the KV cache allocation")
+        if spec.background_requests != pair.n_bg:
+            raise ValueError("background_requests must match the pair's draft background slots")
         self.max_rounds = spec.max_rounds or spec.output_len + 8
         self.cfg = _native.DecodeConfig(
             seed=spec.seed & ((1 << 64) - 1), n_req=spec.n_req, gamma=spec.gamma,
@@ -244,7 +255,10 @@ class SpectreEngine:
             temperature=float(spec.temperature), role=ROLES[role],
             breaker_threshold=int(spec.breaker_threshold),
             breaker_cooldown=int(spec.breaker_cooldown),
-            draft_prompt_keep=spec.draft_prompt_keep())
+            draft_prompt_keep=spec.draft_prompt_keep(),
+            background_requests=int(spec.background_requests),
+            background_output_len=int(spec.background_output_len),
+            fairness_period=int(spec.fairness_period), draft_capacity=int(spec.draft_capacity))
         self.role = role
         self._tdims = pair.target.spec.dims()
         self._ddims = pair.draft.spec.dims()
@@ -316,6 +330,19 @@ class SpectreEngine:
         torch.cuda.synchronize()
         trace = {f: v[:nr.value].cpu().numpy() for f, v in bufs.items()}
         return committed, pos, trace
+
+    def read_background(self):
+        """Background tenants: (tokens [n_bg][background_output_len] int32 on the
+        device, emitted [n_bg], (tokens generated, requests completed))."""
+        torch = _native.require_cuda()
+        n, OL = self.spec.background_requests, self.spec.background_output_len
+        toks = torch.zeros(n, OL, dtype=torch.int32, device="cuda")
+        emitted = torch.zeros(n, dtype=torch.int32, device="cuda")
+        totals = (C.c_int32 * 2)()
+        _native.check(_native.lib().spectre_engine_read_background(
+            self.handle, toks.data_ptr(), emitted.data_ptr(), totals, _native.stream_ptr()),
+            "spectre_engine_read_background")
+        return toks, emitted, (int(totals[0]), int(totals[1]))
 
     def read_committed(self, stream=None):
         """Committed tokens [n_req][output_len] int64 on the device (no host sync)."""
@@ -426,10 +453,15 @@ def decode(pair: ModelPair, spec: DecodeSpec, variant, prompts=None, use_graph=T
     dev_s = float(trace["t_round_ns"].sum()) * 1e-9
     total = int(pos.sum().item())
     rep = report_from_trace(variant, spec.seed, trace, total, dev_s)
-    rep = MetricsReport(**{**rep.__dict__, "requests_completed":
-                           int((pos >= spec.output_len).sum().item())})
-    status = eng.graph_status()
+    upd = {"requests_completed": int((pos >= spec.output_len).sum().item())}
     extra = {}
+    if spec.background_requests > 0:   # regular tenants of the draft (metrics.py:61-101)
+        bg_toks, bg_emitted, (bg_n, bg_done) = eng.read_background()
+        upd.update(background_tokens=bg_n, background_completed=bg_done,
+                   draft_throughput=bg_n / dev_s if dev_s > 0 else 0.0)
+        extra.update(background_tokens=bg_toks, background_emitted=bg_emitted)
+    rep = MetricsReport(**{**rep.__dict__, **upd})
+    status = eng.graph_status()
     if status == 2:
         extra["graph_error"] = _native.lib().spectre_last_error().decode(errors="replace")
     return ModelRunResult(rep, variant, committed, pos, trace, rounds, dev_s, status, extra)
