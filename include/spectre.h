@@ -256,6 +256,10 @@ typedef struct SpectreDecodeConfig {
   int32_t background_output_len;
   int32_t fairness_period;
   int32_t draft_capacity;
+  /* reply deadline in rounds (core.py:123, reply_timeout = 2 t_target): a
+   * missing draft reply is declared a timeout (breaker strike, sim.py:653-665)
+   * at the commit reply_timeout_rounds - 1 rounds after it was due.  <= 0: 2 */
+  int32_t reply_timeout_rounds;
 } SpectreDecodeConfig;
 
 #define SPECTRE_ROLE_BOTH 0
@@ -347,6 +351,7 @@ typedef struct SpectreRoundTrace {
   int32_t* n_regular;       /* background items scheduled with this round's speculation */
   int32_t* n_forced;        /* background items of a forced regular round (0: none) */
   int32_t* fair_counter;    /* FairnessCounter.consecutive_speculative after the round */
+  int32_t* timeout;         /* round flagged a timeout round (RoundTrace.timeout) */
 } SpectreRoundTrace;
 int spectre_engine_read(void* engine, int64_t* committed, int32_t* committed_pos,
                         const SpectreRoundTrace* trace, int32_t* n_rounds, void* stream);

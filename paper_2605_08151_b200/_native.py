@@ -114,13 +114,14 @@ class DecodeConfig(C.Structure):
                 ("role", C.c_int32), ("breaker_threshold", C.c_int32),
                 ("breaker_cooldown", C.c_int32), ("draft_prompt_keep", C.c_int32),
                 ("background_requests", C.c_int32), ("background_output_len", C.c_int32),
-                ("fairness_period", C.c_int32), ("draft_capacity", C.c_int32)]
+                ("fairness_period", C.c_int32), ("draft_capacity", C.c_int32),
+                ("reply_timeout_rounds", C.c_int32)]
 
 
 TRACE_FIELDS = ("mode", "participants", "delta", "n_roll", "content_sum", "content_n",
                 "n_padded", "t_round_ns", "t_verify_ns", "t_draft_ns", "r_hat_ema",
                 "accepted_len_ema", "r_star", "n_stale", "n_regular", "n_forced",
-                "fair_counter")
+                "fair_counter", "timeout")
 
 
 class RoundTraceBufs(C.Structure):

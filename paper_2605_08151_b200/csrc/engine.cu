@@ -509,6 +509,7 @@ struct Engine {
     st.trace.n_regular = b.take<int>(R);
     st.trace.n_forced = b.take<int>(R);
     st.trace.fair_counter = b.take<int>(R);
+    st.trace.timeout = b.take<int>(R);
     if (st.sampling) {
       st.samp_a = b.take<int>(n);
       st.samp_bonus = b.take<int>(n);
@@ -576,6 +577,7 @@ struct Engine {
     st.sampling = c.temperature > 0.0 ? 1 : 0;
     st.breaker_threshold = c.breaker_threshold > 0 ? c.breaker_threshold : 3;
     st.breaker_cooldown = c.breaker_cooldown > 0 ? c.breaker_cooldown : 5;
+    st.timeout_lag = c.reply_timeout_rounds > 0 ? c.reply_timeout_rounds - 1 : 1;
     qwin = 4 * c.gamma + 4;   // > every candidate-to-speculation position gap
     for (ModelRT* m : {&tgt, &drf}) {
       m->sampling = st.sampling;
@@ -1000,6 +1002,7 @@ extern "C" int spectre_engine_read(void* engine, int64_t* committed, int32_t* co
     TRY(cp(trace->n_regular, t.n_regular, R * 4));
     TRY(cp(trace->n_forced, t.n_forced, R * 4));
     TRY(cp(trace->fair_counter, t.fair_counter, R * 4));
+    TRY(cp(trace->timeout, t.timeout, R * 4));
   }
   return SPECTRE_OK;
 }

@@ -52,6 +52,7 @@ struct CtrlDev {
   // this round's schedule (regular items in the forced round / the round that
   // served the speculative queries)
   int fair_counter, bg_tokens, bg_completed, ph_forced, ph_regular;
+  int pending_timeout;   // last speculative round's unanswered queries (timeout_lag)
 };
 
 struct RoundTraceDev {
@@ -72,6 +73,7 @@ struct RoundTraceDev {
   int* n_regular;     // regular items scheduled with this round's speculation
   int* n_forced;      // regular items of a forced regular round (0: none)
   int* fair_counter;  // FairnessCounter.consecutive_speculative after the round
+  int* timeout;       // the round was flagged a timeout round (breaker input)
 };
 
 struct DecodeStateDev {
@@ -109,6 +111,7 @@ struct DecodeStateDev {
   int* samp_a;           // [n_req] accepted candidates
   int* samp_bonus;       // [n_req] bonus / resampled token
   int breaker_threshold, breaker_cooldown;
+  int timeout_lag;       // rounds between a missing reply and its timeout (reply_timeout / T_T - 1)
   // query / reply versioning (target_engine.py:314-331, sim.py:816-844)
   int* req_mode;         // [n_req] this round's mode per request (draft side: 'M' phases)
   int* q_round;          // [n_req] outstanding query tag (target side)

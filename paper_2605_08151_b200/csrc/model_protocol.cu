@@ -100,6 +100,7 @@ __global__ void k_admit(DecodeStateDev s, BatchDev bt) {
     c.streak = c.disabled_until = c.activations = 0;
     c.n_stale = 0;
     c.fair_counter = c.bg_tokens = c.bg_completed = c.ph_forced = c.ph_regular = 0;
+    c.pending_timeout = 0;
   }
   if (b >= s.n_req) return;
   s.req_mode[b] = 0;
@@ -699,21 +700,29 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
     c.last_mode = mode;
     const int ri = c.round;
     // circuit breaker after a speculative round (sim.py:703-718,
-    // target_engine.py:356-380): a missing reply is a timeout here — the
-    // exchange is synchronous, so a reply absent at commit never arrives
+    // target_engine.py:356-380).  A reply absent at commit never arrives (the
+    // exchange is synchronous); the target declares its query timed out once it
+    // is reply_timeout old (sim.py:653-665): with reply_timeout = 2 T_T that is
+    // at the NEXT round's commit (timeout_lag = 1), as in the reference
+    int timed_out = 0;
     if (mode != 'F') {
+      timed_out = s.timeout_lag > 0 ? (c.pending_timeout > 0) : (c.n_stale > 0);
+      c.pending_timeout = c.n_stale;
       const int round_id = ri + 1;
-      const int streak = c.n_stale > 0 ? c.streak + 1 : 0;
+      const int streak = timed_out ? c.streak + 1 : 0;
       if (streak >= s.breaker_threshold) {
         c.streak = 0;
         c.disabled_until = round_id + s.breaker_cooldown + 1;
         c.activations += 1;
+        c.pending_timeout = 0;   // every outstanding query is abandoned (sim.py:711-718)
         s_trip = 1;
       } else {
         c.streak = streak;
       }
     }
+    if (mode == 'F') c.pending_timeout = 0;   // no queries in flight
     if (ri < s.max_rounds) {
+      s.trace.timeout[ri] = timed_out;
       s.trace.n_stale[ri] = c.n_stale;
       s.trace.mode[ri] = mode;
       s.trace.participants[ri] = P;

@@ -196,6 +196,7 @@ class DecodeSpec:
     background_output_len: int = 128
     fairness_period: int = 10
     draft_capacity: int = 256
+    reply_timeout_rounds: int = 2   # reply_timeout = 2 t_target (core.py:123)
 
     def draft_prompt_keep(self) -> int:
         """compress_prompt (draft_engine.py:123-131): keep = int((p / 2) * S); no
@@ -258,7 +259,8 @@ class SpectreEngine:
             draft_prompt_keep=spec.draft_prompt_keep(),
             background_requests=int(spec.background_requests),
             background_output_len=int(spec.background_output_len),
-            fairness_period=int(spec.fairness_period), draft_capacity=int(spec.draft_capacity))
+            fairness_period=int(spec.fairness_period), draft_capacity=int(spec.draft_capacity),
+            reply_timeout_rounds=int(spec.reply_timeout_rounds))
         self.role = role
         self._tdims = pair.target.spec.dims()
         self._ddims = pair.draft.spec.dims()
@@ -434,7 +436,7 @@ def report_from_trace(variant: PolicyVariant, seed: int, trace: dict, total: int
             1 for i, m in enumerate(trace["mode"])
             if m == ord("F") and (i == 0 or trace["mode"][i - 1] != ord("F"))),
         stale_replies=int(trace["n_stale"].sum()) if "n_stale" in trace else 0,
-        timeout_rounds=int((trace["n_stale"] > 0).sum()) if "n_stale" in trace else 0,
+        timeout_rounds=int(trace["timeout"].sum()) if "timeout" in trace else 0,
         draft_tokens_generated=0)
 
 
