@@ -146,15 +146,19 @@ KERNELS_PER_LAYER = 8   # qkv GEMM, RoPE/KV write, attention, o GEMM, residual+n
 #                          gate/up GEMM (SwiGLU), down GEMM, residual+norm
 
 
-def forward_kernels(n_layers: int, sampling: bool) -> int:
-    """embed + layers + lm_head + (argmax reduce | row sampler)."""
+def forward_kernels(n_layers: int, sampling: bool, chain: bool = False) -> int:
+    """embed + layers + lm_head + (argmax reduce | row sampler).  chain: the
+    draft's persistent chains (chain.cu) — first chain + (attention + chain)
+    per layer + lm_head + reduce."""
+    if chain:
+        return 1 + 2 * n_layers + 2
     return 1 + KERNELS_PER_LAYER * n_layers + 2
 
 
 def kernels_per_round(mode: str, gamma: int, tL: int, dL: int, sampling: bool = False) -> int:
     """Our kernels launched by one device round (the graph body that runs)."""
     fwd_t = forward_kernels(tL, sampling)
-    fwd_d = forward_kernels(dL, sampling) - (1 if sampling else 0)   # draft: per-request sampler
+    fwd_d = forward_kernels(dL, sampling, chain=True) - (1 if sampling else 0)   # per-request sampler
     step_d = fwd_d + 1 + (1 if sampling else 0)                       # + append (+ draft sampler)
     n = 2 + (1 if sampling else 0)  # round_begin + accept (+ accept sampler)
     n += 1 + fwd_t  # verify_prep + target forward
@@ -237,7 +241,7 @@ def run_ours(args):
         cs = max(1, min(16, 512 // B))         # engine prefill chunk (engine.cu:prefill_chunk)
         chunks = (args.prompt_len + cs - 1) // cs
         prefill_launches = 2 * chunks + 1  # batch kernels + admit
-        prefill_launches += chunks * (forward_kernels(32, samp) + forward_kernels(16, samp))
+        prefill_launches += chunks * (forward_kernels(32, samp) + forward_kernels(16, samp, True))
         prefill_launches -= 2 * (2 * chunks - 1)   # lm_head + reduce: target's last chunk only
         results[v] = dict(
             ms_per_step=ms_max / args.steps, value=total_tokens / (ms_max / 1e3),
@@ -292,10 +296,13 @@ def run_ours(args):
     if ws > 1:
         parity["identical"] = bool(allreduce_min(float(parity["identical"]), ws))
 
-    # ---- roofline of the dominant kernel, timed live (CUDA events, its own stream)
-    roof = None
+    # ---- roofline of the dominant kernel, timed live (CUDA events, its own stream):
+    # the draft's chain kernel (largest exclusive time per round, profiles/r02
+    # kprof), with the verify gate/up GEMM (the round-1 headline kernel) beside it
+    roof = roof_gu = None
     if not args.no_roofline and rank == 0:
-        roof = roofline_gate_up(pair, args)
+        roof = roofline_chain(engines[args.variant], pair, args)
+        roof_gu = roofline_gate_up(pair, args)
     # ---- whole-round roofline: algorithmic HBM bytes of one ordinary
     # round at the run's mean context vs the measured ordinary round time
     round_roof = None
@@ -346,7 +353,8 @@ def run_ours(args):
                        "controller": args.controller,
                        "parallelism": f"dp{ws} ({'shards of ' + str(args.batch) + ' requests' if args.shard else 'request batches'})",
                        "l2": "inputs > L2 (15 GB weights + KV streamed per round)"},
-            "e2e": e2e, "roofline": roof, "round_roofline": round_roof, "cpu_baseline": cpu,
+            "e2e": e2e, "roofline": roof, "roofline_gate_up": roof_gu,
+            "round_roofline": round_roof, "cpu_baseline": cpu,
             "parity": parity, "oracle_mode": omode, "alpha_measured": alpha_meas,
             "clocks": head["clocks"], "gpu_launches": head["gpu_launches"],
             "modes": {v: {k: (round(x, 4) if isinstance(x, float) else x)
@@ -383,6 +391,58 @@ def alpha_from_L(L: float, gamma: int) -> float:
         else:
             hi = mid
     return round((lo + hi) / 2, 4)
+
+
+def _traffic(name):
+    tf = ROOT / "profiles" / "r02" / "ncu_traffic.json"
+    return json.loads(tf.read_text()).get(name) if tf.exists() else None
+
+
+def roofline_chain(eng, pair, args):
+    """The draft decode step's chain kernel (chain.cu: o, residual + norm,
+    gate/up, down, residual + norm, next q/k/v, RoPE in one launch), T = B rows
+    at mid context: the mid-layer chains launched back to back (PDL-chained, one
+    pass = 15 launches over distinct weights, > L2), CUDA events on the
+    launching stream.  Algorithmic bytes = the weights a chain streams."""
+    import ctypes as C
+    import torch
+    from paper_2605_08151_b200 import _native
+    peaks, src = load_peaks()
+    L = _native.lib()
+    B = args.batch
+    V = pair.draft.spec.vocab
+    pos = torch.full((B,), args.prompt_len + args.out_len // 2, dtype=torch.int32, device="cuda")
+    ar = torch.arange(B, dtype=torch.int32, device="cuda")
+    tok = (ar * 7919 + 11) % V
+    # one decode-shaped draft forward leaves the draft batch at T = B rows
+    eng.forward(1, tok, pos, ar, ar, torch.ones(B, dtype=torch.int32, device="cuda"), pos)
+    s = torch.cuda.Stream()
+    wb = C.c_int64(0)
+    reps = 4
+    _native.check(L.spectre_engine_launch_chains(eng.handle, 1, C.byref(wb), int(s.cuda_stream)),
+                  "chains")   # warm
+    times = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        n = L.spectre_engine_launch_chains(eng.handle, reps, C.byref(wb), int(s.cuda_stream))
+        e1.record(s)
+        e1.synchronize()
+        if n < 0:
+            _native.check(n, "chains")
+        times.append(e0.elapsed_time(e1) * 1e-3 / n)
+    t = statistics.median(times)
+    n_mid = pair.draft.spec.n_layers - 1
+    bytes_ = wb.value / n_mid
+    gbs = bytes_ / t / 1e9
+    hbm = peaks["hbm_gbs"]
+    return {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(gbs / hbm, 4),
+            "traffic": _traffic("k_chain draft mid-layer chain (o, resid, gate/up, down, resid, "
+                                "qkv, rope; T=64)"),
+            "kernel": f"k_chain draft mid-layer chain, T={B}",
+            "bytes_per_launch": int(bytes_), "us_per_launch": round(t * 1e6, 2),
+            "peak_source": src + " (MEASURED_PEAKS.json)"}
 
 
 def roofline_gate_up(pair, args):
@@ -433,10 +493,7 @@ def roofline_gate_up(pair, args):
     bound = "hbm" if bytes_ / (hbm * 1e9) >= flops / (tc * 1e12) else "tensor"
     ach, peak, unit = (gbs, hbm, "GB/s") if bound == "hbm" else (tfs, tc, "TFLOP/s")
     kname = f"gemm_bf16_swapab<SwiGLU> target gate_up T={T} N={F2} K={K}"
-    traffic = None
-    tf = ROOT / "profiles" / "r01" / "ncu_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get(kname)   # ncu capture of the same launch shape
+    traffic = _traffic(kname)   # ncu capture of the same launch shape
     return {"bound": bound, "achieved": round(ach, 1), "peak": peak, "unit": unit,
             "frac": round(ach / peak, 4), "traffic": traffic,
             "kernel": f"gemm_bf16_swapab<SwiGLU> target gate_up T={T} N={F2} K={K}",

@@ -363,6 +363,11 @@ int spectre_engine_read_committed(void* engine, int64_t* committed, void* stream
  * requests completed} (host).  Synchronous. */
 int spectre_engine_read_background(void* engine, int32_t* tokens, int32_t* emitted,
                                    int32_t* totals, void* stream);
+/* Measurement: launch the draft's mid-layer chain kernels back to back `reps`
+ * times on `stream` (current draft batch); returns the launches issued and the
+ * weight bytes of one pass in *weight_bytes. */
+int spectre_engine_launch_chains(void* engine, int32_t reps, int64_t* weight_bytes,
+                                 void* stream);
 /* One forward pass over a packed ragged batch (tests / roofline):
  * which 0 = target, 1 = draft.  tok/pos/slot [T]; per request q_off, n_new,
  * pos0 [n_req] (n_new 0 = not participating).  out_tok [T] greedy argmax;

@@ -153,6 +153,7 @@ def _bind_model(L) -> None:
          [_P, _P, _P, C.POINTER(RoundTraceBufs), C.POINTER(i32), _P])
     _sig(L, "spectre_engine_read_committed", C.c_int, [_P, _P, _P])
     _sig(L, "spectre_engine_read_background", C.c_int, [_P, _P, _P, C.POINTER(i32), _P])
+    _sig(L, "spectre_engine_launch_chains", C.c_int, [_P, i32, C.POINTER(i64), _P])
     _sig(L, "spectre_engine_forward", C.c_int,
          [_P, i32, _P, _P, _P, i32, _P, _P, _P, _P, _P, _P])
 

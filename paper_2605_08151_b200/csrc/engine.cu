@@ -937,6 +937,31 @@ extern "C" int spectre_engine_run(void* engine, int32_t max_rounds, int32_t use_
   return SPECTRE_OK;
 }
 
+// Roofline timing (bench.py): launch the draft's mid-layer chains back to back
+// `reps` times over the current draft batch (the step's row count; activations
+// are whatever the buffers hold — the weight stream and the phase structure are
+// those of a decode step).  Returns the number of chain launches issued;
+// *weight_bytes = weight bytes one pass over the mid chains streams.
+extern "C" int spectre_engine_launch_chains(void* engine, int32_t reps, int64_t* weight_bytes,
+                                            void* stream) {
+  auto* e = reinterpret_cast<Engine*>(engine);
+  if (!e || reps < 1 || !e->drf.use_chain || e->drf.ch_mid.empty())
+    return arg_fail("spectre_engine_launch_chains: no draft chains");
+  cudaStream_t s = as_stream(stream);
+  const SpectreModelDims& d = e->drf.dm;
+  const long long per_layer = (long long)d.d_model * d.n_q_heads * d.head_dim +
+                              3ll * d.d_model * d.ffn +
+                              (long long)(d.n_q_heads + 2 * d.n_kv_heads) * d.head_dim * d.d_model;
+  if (weight_bytes) *weight_bytes = 2 * per_layer * (long long)e->drf.ch_mid.size();
+  int n = 0;
+  for (int r = 0; r < reps; ++r)
+    for (void* c : e->drf.ch_mid) {
+      TRY(chain_launch(c, s));
+      ++n;
+    }
+  return n;
+}
+
 // Diagnostics: the draft chains' last per-phase globaltimer stamps (CTA 0),
 // [n_layers + 1][32] u64 — only with SPECTRE_CHAIN_DBG set at engine creation.
 extern "C" int spectre_engine_chain_stamps(void* engine, uint64_t* out, int32_t n) {
