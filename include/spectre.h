@@ -260,6 +260,11 @@ typedef struct SpectreDecodeConfig {
    * missing draft reply is declared a timeout (breaker strike, sim.py:653-665)
    * at the commit reply_timeout_rounds - 1 rounds after it was due.  <= 0: 2 */
   int32_t reply_timeout_rounds;
+  /* non-stationary acceptance (config 4 drift workload): from draft output
+   * position alpha_switch_pos on, the draft keep probability is alpha_late
+   * instead of alpha.  alpha_switch_pos <= 0: alpha throughout */
+  int32_t alpha_switch_pos;
+  double alpha_late;
 } SpectreDecodeConfig;
 
 #define SPECTRE_ROLE_BOTH 0

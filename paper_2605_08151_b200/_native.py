@@ -115,7 +115,8 @@ class DecodeConfig(C.Structure):
                 ("breaker_cooldown", C.c_int32), ("draft_prompt_keep", C.c_int32),
                 ("background_requests", C.c_int32), ("background_output_len", C.c_int32),
                 ("fairness_period", C.c_int32), ("draft_capacity", C.c_int32),
-                ("reply_timeout_rounds", C.c_int32)]
+                ("reply_timeout_rounds", C.c_int32), ("alpha_switch_pos", C.c_int32),
+                ("alpha_late", C.c_double)]
 
 
 TRACE_FIELDS = ("mode", "participants", "delta", "n_roll", "content_sum", "content_n",

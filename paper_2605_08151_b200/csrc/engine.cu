@@ -569,6 +569,8 @@ struct Engine {
     st.hist_cap = c.ctx_cap - c.prompt_len;
     st.seed = c.seed;
     st.alpha = c.alpha;
+    st.alpha_switch = c.alpha_switch_pos > 0 ? c.alpha_switch_pos : 0x7fffffff;
+    st.alpha_late = c.alpha_switch_pos > 0 ? c.alpha_late : c.alpha;
     st.t_target = c.t_target;
     st.t_draft = c.t_draft;
     st.ema_decay = c.ema_decay;
@@ -815,7 +817,8 @@ extern "C" void* spectre_engine_create(const SpectreModelDims* target,
              "draft_capacity >= n_req, n_req + background <= 1024 and KV room for their output");
     return nullptr;
   }
-  if (cfg->temperature > 0.0 && cfg->alpha < 1.0) {
+  if (cfg->temperature > 0.0 &&
+      (cfg->alpha < 1.0 || (cfg->alpha_switch_pos > 0 && cfg->alpha_late < 1.0))) {
     // rejection sampling tests min(1, p/q) against the draft's q; the alpha
     // noise would replace the proposal by a token not drawn from q
     arg_fail("spectre_engine_create: temperature > 0 needs alpha == 1 (no draft noise)");

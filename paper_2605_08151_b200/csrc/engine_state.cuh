@@ -44,6 +44,11 @@ struct CtrlDev {
   double rpar;
   int has_rho;       // T_par / T_ord measured at the same context (steady P round vs
   double rho;        // the ordinary EMA at that time): round times grow with context
+  // re-probe: r-hat over ordinary rounds only, its value when r / rho were last
+  // measured, and the parallel rounds still owed by a running probe
+  int has_ema_ord, has_probe_ref, probe_left, probe_round;
+  int p_streak;      // consecutive parallel rounds up to the last accepted one
+  double ema_ord, probe_ref;
   // circuit breaker (target_engine.py:337-380); round ids are 1-based as in sim.py:519
   int streak, disabled_until, activations;
   int n_stale;       // this round: queried requests without a matching reply
@@ -83,6 +88,8 @@ struct DecodeStateDev {
   int hist_cap;      // draft history capacity (output positions)
   uint64_t seed;
   double alpha, t_target, t_draft, ema_decay, fixed_l;
+  int alpha_switch;  // draft output position where alpha_late takes over (INT_MAX: never)
+  double alpha_late;
   // per request (SoA)
   int* pos;          // committed_pos
   int* done;

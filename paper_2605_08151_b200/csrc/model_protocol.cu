@@ -43,11 +43,14 @@ __device__ __forceinline__ double u53(uint64_t h) { return (double)(h >> 11) * (
 
 // draft "controlled noise": keep the draft's greedy token with probability
 // alpha, else replace it with a different token (deterministic per position).
+// From output position alpha_switch on the keep probability is alpha_late
+// (non-stationary acceptance: the drift workload of config 4).
 __device__ __forceinline__ int noisy_draft_token(const DecodeStateDev& s, int req, int pos,
                                                  int tok) {
-  if (s.alpha >= 1.0) return tok;
+  const double alpha = pos >= s.alpha_switch ? s.alpha_late : s.alpha;
+  if (alpha >= 1.0) return tok;
   const uint64_t h = mix64(s.seed, 2, (uint64_t)req, (uint64_t)pos);
-  if (u53(h) < s.alpha) return tok;
+  if (u53(h) < alpha) return tok;
   const uint64_t r = mix64(s.seed, 3, (uint64_t)req, (uint64_t)pos);
   return (int)(((uint64_t)tok + 1 + r % (uint64_t)(s.vocab - 1)) % (uint64_t)s.vocab);
 }
@@ -95,6 +98,9 @@ __global__ void k_admit(DecodeStateDev s, BatchDev bt) {
     c.rpar = 0.0;
     c.has_rho = 0;
     c.rho = 0.0;
+    c.has_ema_ord = c.has_probe_ref = c.probe_left = c.p_streak = 0;
+    c.probe_round = 0;
+    c.ema_ord = c.probe_ref = 0.0;
     c.last_mode = 0;
     c.r_star = 0.0;
     c.streak = c.disabled_until = c.activations = 0;
@@ -183,6 +189,11 @@ __device__ int round_choose_mode(DecodeStateDev& s, CtrlDev& c) {
         } else if (!c.has_tpar) {
           mode = 'P';
           r_star = 0.0;
+        } else if (c.probe_left > 0) {
+          // re-probe in progress: one more parallel round (the steady one)
+          mode = 'P';
+          --c.probe_left;
+          r_star = c.r_star;
         } else {
           // r: the PADDED fraction parallel rounds actually produced (the
           // paper's r) once measured; before that the reference's r-hat.  At
@@ -200,6 +211,17 @@ __device__ int round_choose_mode(DecodeStateDev& s, CtrlDev& c) {
             mode = (r_hat > __dmul_rn(r_star, kExitParallelMargin)) ? 'O' : 'P';
           else
             mode = (r_hat <= r_star) ? 'P' : 'O';
+          // r and T_par / T_ord are only measured in parallel rounds: while
+          // ordinary rounds run they go stale.  When the ordinary-round r-hat
+          // has moved by more than kReprobeDelta since they were measured,
+          // spend two parallel rounds (switch-over + steady) re-measuring them
+          if (mode == 'O' && c.has_ema_ord && c.has_probe_ref &&
+              c.round - c.probe_round >= kReprobeMinRounds &&
+              fabs(__dsub_rn(c.ema_ord, c.probe_ref)) > kReprobeDelta) {
+            mode = 'P';
+            c.probe_left = 1;
+            c.probe_round = c.round;
+          }
         }
       }
       c.r_star = r_star;
@@ -687,16 +709,26 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
     // prepared segments: all PADDED, sim.py:455-458) — neither its time nor
     // its PADDED fraction is the steady parallel round's
     if (mode == 'P' && c.last_mode == 'P') {
-      if (!c.has_tpar) { c.tpar = tr; c.has_tpar = 1; } else { c.tpar = ema_step(d, c.tpar, tr); }
+      // the first steady round of a parallel streak replaces what earlier
+      // streaks measured (stale: other context, other r); later rounds blend
+      const bool fresh = c.p_streak == 1;
+      if (!c.has_tpar || fresh) { c.tpar = tr; c.has_tpar = 1; } else { c.tpar = ema_step(d, c.tpar, tr); }
       const double rp = __ddiv_rn((double)npad, (double)(P > 0 ? P : 1));
-      if (!c.has_rpar) { c.rpar = rp; c.has_rpar = 1; } else { c.rpar = ema_step(d, c.rpar, rp); }
+      if (!c.has_rpar || fresh) { c.rpar = rp; c.has_rpar = 1; } else { c.rpar = ema_step(d, c.rpar, rp); }
       if (c.has_tord) {
         const double rv = __ddiv_rn(tr, c.tord);
-        if (!c.has_rho) { c.rho = rv; c.has_rho = 1; } else { c.rho = ema_step(d, c.rho, rv); }
+        if (!c.has_rho || fresh) { c.rho = rv; c.has_rho = 1; } else { c.rho = ema_step(d, c.rho, rv); }
       }
+      // r / rho are fresh: remember the ordinary-round r-hat they belong to
+      c.probe_ref = c.has_ema_ord ? c.ema_ord : r_hat;
+      c.has_probe_ref = 1;
+      c.probe_round = c.round;
     } else if (mode == 'O') {
       if (!c.has_tord) { c.tord = tr; c.has_tord = 1; } else { c.tord = ema_step(d, c.tord, tr); }
+      if (!c.has_ema_ord) { c.ema_ord = r_hat; c.has_ema_ord = 1; }
+      else { c.ema_ord = ema_step(d, c.ema_ord, r_hat); }
     }
+    c.p_streak = mode == 'P' ? c.p_streak + 1 : 0;
     c.last_mode = mode;
     const int ri = c.round;
     // circuit breaker after a speculative round (sim.py:703-718,

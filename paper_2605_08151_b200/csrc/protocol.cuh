@@ -14,6 +14,11 @@ namespace spectre {
 constexpr uint64_t kPad = ~0ull;                 // core.py:16-18
 constexpr uint64_t kDisagree = 0x5BD1E995ull;    // oracle.py:15
 constexpr double kExitParallelMargin = 1.10;     // sim.py:199
+// `round` controller re-probe (model mode only; not in the reference): the
+// ordinary-round r-hat drift that triggers re-measuring r and T_par / T_ord,
+// and the fewest rounds between two probes
+constexpr double kReprobeDelta = 0.15;
+constexpr int kReprobeMinRounds = 16;
 
 enum CandKind : int32_t { kCached = 1, kRepaired = 2, kPadded = 3, kFallback = 4 };
 

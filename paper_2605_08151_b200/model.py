@@ -197,6 +197,10 @@ class DecodeSpec:
     fairness_period: int = 10
     draft_capacity: int = 256
     reply_timeout_rounds: int = 2   # reply_timeout = 2 t_target (core.py:123)
+    # non-stationary acceptance (config 4 drift workload): from draft output
+    # position alpha_switch_pos on the keep probability is alpha_late
+    alpha_switch_pos: int = 0
+    alpha_late: float = 1.0
 
     def draft_prompt_keep(self) -> int:
         """compress_prompt (draft_engine.py:123-131): keep = int((p / 2) * S); no
@@ -211,7 +215,8 @@ class DecodeSpec:
         return keep
 
     def __post_init__(self):
-        if self.temperature > 0 and self.alpha < 1.0:
+        if self.temperature > 0 and (self.alpha < 1.0 or
+                                     (self.alpha_switch_pos > 0 and self.alpha_late < 1.0)):
             raise ValueError("temperature > 0 (rejection sampling) needs alpha == 1: the "
                              "alpha noise would replace proposals not drawn from q")
 
@@ -260,7 +265,8 @@ class SpectreEngine:
             background_requests=int(spec.background_requests),
             background_output_len=int(spec.background_output_len),
             fairness_period=int(spec.fairness_period), draft_capacity=int(spec.draft_capacity),
-            reply_timeout_rounds=int(spec.reply_timeout_rounds))
+            reply_timeout_rounds=int(spec.reply_timeout_rounds),
+            alpha_switch_pos=int(spec.alpha_switch_pos), alpha_late=float(spec.alpha_late))
         self.role = role
         self._tdims = pair.target.spec.dims()
         self._ddims = pair.draft.spec.dims()

@@ -49,6 +49,7 @@ def main():
     ks = sorted(((e.time_range.start, e.time_range.end, short(e.name)) for e in evs
                  if "Memcpy" not in e.name and "Memset" not in e.name), key=lambda x: x[0])
     phase = "other"
+    tcount = 0
     agg = defaultdict(lambda: [0, 0.0, 0.0])
     spans = defaultdict(float)
     first = {}
@@ -64,6 +65,12 @@ def main():
             phase = "target"
         elif n.startswith("k_accept") or n.startswith("k_round_begin"):
             phase = "other"
+        if phase == "target" and n.startswith("k_verify_prep"):
+            tcount = 0
+        if phase == "target" and n.startswith("gemm_bf16_swapab<0"):
+            # target layer order: q/k/v, o, down (split-K partial GEMMs)
+            n = n + " " + ("qkv", "o", "down")[tcount % 3]
+            tcount += 1
         key = (phase, n)
         agg[key][0] += 1
         agg[key][1] += excl

@@ -29,9 +29,11 @@ from paper_2605_08151_b200 import model as M
 from paper_2605_08151_b200.decoder import PolicyVariant
 
 
-def one(pair, prompts, gamma, alpha, variant, out_len, seed):
+def one(pair, prompts, gamma, alpha, variant, out_len, seed, alpha_late=None, switch=0):
     spec = M.DecodeSpec(n_req=prompts.shape[0], gamma=gamma, output_len=out_len,
-                        prompt_len=prompts.shape[1], alpha=alpha, seed=seed, controller="round")
+                        prompt_len=prompts.shape[1], alpha=alpha, seed=seed, controller="round",
+                        alpha_switch_pos=switch if alpha_late is not None else 0,
+                        alpha_late=alpha if alpha_late is None else alpha_late)
     eng = M.SpectreEngine(pair, spec, variant)
     eng.prefill(prompts)
     eng.run(use_graph=True)           # warm (graph build)
@@ -62,7 +64,7 @@ def one(pair, prompts, gamma, alpha, variant, out_len, seed):
                r_star_last=float(tr["r_star"][-1]) if len(modes) else None,
                r_star_median=float(np.median(tr["r_star"][np.isfinite(tr["r_star"])]))
                if np.isfinite(tr["r_star"]).any() else None,
-               timeline_head=modes[:48])
+               timeline_head=modes[:48], timeline=modes)
     del eng
     return res
 
@@ -77,6 +79,9 @@ def main():
     ap.add_argument("--out-len", type=int, default=512)
     ap.add_argument("--n-req", type=int, default=64)
     ap.add_argument("--out", default="gpurun_out/r_sweep.json")
+    ap.add_argument("--drift", type=float, nargs=2, default=[1.0, 0.1],
+                    help="drift workload: alpha for the first half of the output, then alpha_late")
+    ap.add_argument("--drift-gammas", type=int, nargs="*", default=[8, 4])
     args = ap.parse_args()
     gmax = max(args.gammas)
     ctx = M.DecodeSpec(n_req=args.n_req, gamma=gmax, output_len=args.out_len,
@@ -92,34 +97,75 @@ def main():
                 r = one(pair, prompts, g, a, v, args.out_len, seed=0)
                 rows.append(r)
                 print(json.dumps({k: (round(x, 4) if isinstance(x, float) else x)
-                                  for k, x in r.items() if k != "timeline_head"}), flush=True)
-    # crossover analysis per gamma
+                                  for k, x in r.items() if k not in ("timeline_head", "timeline")}),
+                      flush=True)
+    # crossover analysis per gamma.  Measured switch: where parallel minus
+    # ordinary tok/s changes sign along the sweep (either direction), and the
+    # paper's r (PADDED fraction of parallel rounds) there.  Predicted switch:
+    # the model's fixed point r = r*(L, T_par/T_ord) along the same sweep (the
+    # hybrid's r* per point against the parallel run's r), i.e. where the
+    # controller's rule "parallel iff r <= r*" flips.
+    def sign_change(alphas, f):
+        for i in range(len(alphas) - 1):
+            a, b = f[i], f[i + 1]
+            if a == 0 or (a > 0) != (b > 0):
+                t = 0.0 if a == b else a / (a - b)
+                return i, t
+        return None
+
     summary = []
     for g in args.gammas:
         pts = sorted([r for r in rows if r["gamma"] == g], key=lambda r: -r["alpha"])
         by = {(r["alpha"], r["variant"]): r for r in pts}
         alphas = sorted({r["alpha"] for r in pts}, reverse=True)
         diff = [by[(a, "parallel")]["tok_s"] - by[(a, "ordinary")]["tok_s"] for a in alphas]
+        rpad = [by[(a, "parallel")]["r_pad_parallel"] for a in alphas]
+        rstar = [by[(a, "hybrid")]["r_star_median"] for a in alphas]
+
+        def lerp(v, i, t):
+            return v[i] + t * (v[i + 1] - v[i])
+
         cross = None
-        for i in range(len(alphas) - 1):
-            if diff[i] >= 0 > diff[i + 1]:
-                f = diff[i] / (diff[i] - diff[i + 1])
-                a_c = alphas[i] + f * (alphas[i + 1] - alphas[i])
-                rh = [by[(a, "parallel")]["r_hat"] for a in alphas[i:i + 2]]
-                rp = [by[(a, "parallel")]["r_pad_parallel"] for a in alphas[i:i + 2]]
-                rs = [by[(a, "hybrid")]["r_star_median"] for a in alphas[i:i + 2]]
-                cross = dict(alpha=a_c, r_hat=rh[0] + f * (rh[1] - rh[0]),
-                             r_pad=rp[0] + f * (rp[1] - rp[0]),
-                             predicted_r_star=None if None in rs else rs[0] + f * (rs[1] - rs[0]))
-                break
+        m = sign_change(alphas, diff)
+        if m is not None:
+            i, t = m
+            cross = dict(alpha=lerp(alphas, i, t), r_switch=lerp(rpad, i, t),
+                         r_star_there=None if None in rstar[i:i + 2] else lerp(rstar, i, t),
+                         parallel_wins_below=diff[i + 1] > 0)
+            if None not in rstar:
+                p = sign_change(alphas, [rs - rp for rs, rp in zip(rstar, rpad)])
+                if p is not None:
+                    j, u = p
+                    cross.update(predicted_alpha=lerp(alphas, j, u),
+                                 predicted_r_switch=lerp(rpad, j, u))
+                    cross["rel_err"] = (abs(cross["r_switch"] - cross["predicted_r_switch"])
+                                        / cross["predicted_r_switch"])
         best = [max(by[(a, "parallel")]["tok_s"], by[(a, "ordinary")]["tok_s"]) for a in alphas]
         hyb = [by[(a, "hybrid")]["tok_s"] for a in alphas]
         summary.append(dict(gamma=g, alphas=alphas, parallel_minus_ordinary=diff,
-                            crossover=cross,
+                            r_pad_parallel=rpad, r_star_hybrid=rstar, crossover=cross,
                             hybrid_over_best=[h / b for h, b in zip(hyb, best)]))
         print(json.dumps(summary[-1]), flush=True)
+    drift = []
+    for g in args.drift_gammas:
+        res = {}
+        for v in ("ordinary", "parallel", "hybrid"):
+            res[v] = one(pair, prompts, g, args.drift[0], v, args.out_len, seed=0,
+                         alpha_late=args.drift[1], switch=args.out_len // 2)
+            print(json.dumps({k: (round(x, 4) if isinstance(x, float) else x)
+                              for k, x in res[v].items() if k not in ("timeline_head", "timeline")}),
+                  flush=True)
+        best = max(res["ordinary"]["tok_s"], res["parallel"]["tok_s"])
+        drift.append(dict(gamma=g, alpha=args.drift[0], alpha_late=args.drift[1],
+                          switch_pos=args.out_len // 2,
+                          tok_s={v: r["tok_s"] for v, r in res.items()},
+                          hybrid_over_ordinary=res["hybrid"]["tok_s"] / res["ordinary"]["tok_s"],
+                          hybrid_over_parallel=res["hybrid"]["tok_s"] / res["parallel"]["tok_s"],
+                          hybrid_over_best=res["hybrid"]["tok_s"] / best,
+                          timeline=res["hybrid"]["timeline"], points=list(res.values())))
+        print(json.dumps({k: v for k, v in drift[-1].items() if k != "points"}), flush=True)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
-    Path(args.out).write_text(json.dumps(dict(points=rows, summary=summary,
+    Path(args.out).write_text(json.dumps(dict(points=rows, summary=summary, drift=drift,
                                               branch=args.branch, out_len=args.out_len,
                                               n_req=args.n_req, seconds=time.time() - t0),
                                          indent=1))
