@@ -97,7 +97,10 @@ struct ChainArgs {
   __nv_bfloat16* vc;
   int rope_splits;
   unsigned* bar;                 // phase arrival counter (self-resetting)
-  unsigned long long* dbg;       // diagnostics: CTA 0's globaltimer stamps [2 + 2 * phases]
+  unsigned long long* dbg;       // diagnostics: CTA 0's globaltimer stamps [64]: 0 start,
+                                 // 1 + 2p / 2 + 2p phase p may start / done, 16 + 2p / 17 + 2p
+                                 // first accumulator ready / outputs stored, 32 + p MMA
+                                 // issuer's first full stage of phase p
 };
 
 struct ChainJob {
@@ -483,6 +486,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
           const int nk = min(kChainKS, j.k1 - kb);
           mbar_wait(&full[s], (uint32_t)(gw / kChainStages) & 1u);
           tc_fence_after();
+          if (a.dbg && c == 0 && lane == 0 && i == 0 && kb == j.k0) a.dbg[32 + p] = gtimer_ns();
           if (lane == 0) {
             for (int q = 0; q < nk; ++q) {
               const uint32_t wa = smem_u32(ring + s * kChainStageBytes + q * kChainWBox);
@@ -532,6 +536,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
           const int buf = jn & 1;
           mbar_wait(&tmem_full[buf], (uint32_t)(jn >> 1) & 1u);
           tc_fence_after();
+          if (stamp && i == 0) a.dbg[16 + 2 * p] = gtimer_ns();
           const int t_pad = (j.nt + 15) & ~15;
           const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kChainPass);
           for (int cc = 32 * grp; cc < t_pad; cc += 64) {
@@ -603,6 +608,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
           bulk_wait_all();   // this phase's outputs are in global memory ...
           asm volatile("fence.proxy.async.global;" ::: "memory");   // ... and visible
         }
+        if (stamp) a.dbg[17 + 2 * p] = gtimer_ns();
       } else if (T > 0 && (kind == kPhResid || kind == kPhEmbed)) {
         chain_norm_rows(a, T, p, et, sh);
       } else if (T > 0 && kind == kPhRope) {

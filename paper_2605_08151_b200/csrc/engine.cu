@@ -109,7 +109,7 @@ struct ModelRT {
   std::vector<void*> ch_mid;
   void* ch_last = nullptr;
   unsigned* ch_bar = nullptr;
-  unsigned long long* ch_dbg = nullptr;   // SPECTRE_CHAIN_DBG: [L + 1][32] phase stamps
+  unsigned long long* ch_dbg = nullptr;   // SPECTRE_CHAIN_DBG: [L + 1][64] phase stamps
   ModelRT() = default;
   ModelRT(const ModelRT&) = delete;
   ModelRT& operator=(const ModelRT&) = delete;
@@ -190,7 +190,7 @@ struct ModelRT {
     rope = b.take<float2>((size_t)ctx_cap * dm.head_dim / 2);
     ch_bar = b.take<unsigned>(64);
     if (use_chain && getenv("SPECTRE_CHAIN_DBG"))
-      ch_dbg = b.take<unsigned long long>((size_t)(dm.n_layers + 1) * 32);
+      ch_dbg = b.take<unsigned long long>((size_t)(dm.n_layers + 1) * 64);
     bt.tok = b.take<int>(R);
     bt.pos = b.take<int>(R);
     bt.slot = b.take<int>(R);
@@ -264,7 +264,7 @@ struct ModelRT {
     int chain_idx = 0;
     auto model = [&](int rope_layer, int pre_wait) {
       ChainModel m{};
-      m.dbg = ch_dbg ? ch_dbg + 32 * chain_idx++ : nullptr;
+      m.dbg = ch_dbg ? ch_dbg + 64 * chain_idx++ : nullptr;
       m.rows_cap = rows_cap;
       m.d = d;
       m.n_q = dm.n_q_heads;
@@ -966,11 +966,11 @@ extern "C" int spectre_engine_launch_chains(void* engine, int32_t reps, int64_t*
 }
 
 // Diagnostics: the draft chains' last per-phase globaltimer stamps (CTA 0),
-// [n_layers + 1][32] u64 — only with SPECTRE_CHAIN_DBG set at engine creation.
+// [n_layers + 1][64] u64 — only with SPECTRE_CHAIN_DBG set at engine creation.
 extern "C" int spectre_engine_chain_stamps(void* engine, uint64_t* out, int32_t n) {
   auto* e = reinterpret_cast<Engine*>(engine);
   if (!e || !out || !e->drf.ch_dbg) return arg_fail("spectre_engine_chain_stamps");
-  const int have = (e->drf.dm.n_layers + 1) * 32;
+  const int have = (e->drf.dm.n_layers + 1) * 64;
   SPECTRE_CUDA_TRY(cudaMemcpy(out, e->drf.ch_dbg, (size_t)std::min(n, have) * 8,
                               cudaMemcpyDeviceToHost));
   return std::min(n, have);

@@ -21,14 +21,24 @@ eng = M.SpectreEngine(pair, spec, "ordinary")
 prompts = M.synthetic_prompts(64, 128, M.LLAMA_31_8B.vocab, seed=0)
 eng.prefill(prompts)
 eng.run(max_rounds=20, use_graph=False, sync=True)
-n = (M.LLAMA_32_1B.n_layers + 1) * 32
+n = (M.LLAMA_32_1B.n_layers + 1) * 64
 buf = np.zeros(n, dtype=np.uint64)
 got = L.spectre_engine_chain_stamps(eng.handle, buf.ctypes.data, n)
-st = buf[:got].reshape(-1, 32).astype(np.int64)
+st = buf[:got].reshape(-1, 64).astype(np.int64)
 names = {0: "first: embed | qkv | rope", 16: "last: o | resid | gu | down | resid"}
+kinds = {0: ["embed", "qkv", "rope"], 16: ["o", "resid", "gu", "down", "resid"]}
 for i, row in enumerate(st):
-    t0 = row[0]
-    k = int(np.count_nonzero(row)) 
-    rel = [(int(v) - int(t0)) / 1e3 for v in row[:k]]
-    print(f"chain {i:2d} {names.get(i, 'mid: o | resid | gu | down | resid | qkv | rope')}: "
-          + " ".join(f"{x:7.2f}" for x in rel))
+    t0 = int(row[0])
+    rel = lambda v: (int(v) - t0) / 1e3 if v else float("nan")
+    ph = kinds.get(i, ["o", "resid", "gu", "down", "resid", "qkv", "rope"])
+    cells = []
+    for p, name in enumerate(ph):
+        start = 0.0 if p == 0 else rel(row[1 + 2 * p])
+        cell = f"{name}[{start:5.2f}"
+        if row[32 + p]:
+            cell += f" x{rel(row[32 + p]):5.2f}"
+        if row[16 + 2 * p]:
+            cell += f" acc{rel(row[16 + 2 * p]):5.2f} st{rel(row[17 + 2 * p]):5.2f}"
+        cell += f" ->{rel(row[2 + 2 * p]):5.2f}]"
+        cells.append(cell)
+    print(f"chain {i:2d}: " + " ".join(cells))
