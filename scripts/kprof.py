@@ -32,8 +32,11 @@ def main():
     ap.add_argument("--branch", type=float, default=0.004)
     ap.add_argument("--n-req", type=int, default=64)
     ap.add_argument("--out", default="gpurun_out/kprof.json")
+    ap.add_argument("--temperature", type=float, default=0.0)
+    ap.add_argument("--out-len", type=int, default=1024)
     args = ap.parse_args()
-    spec = M.DecodeSpec(n_req=args.n_req, gamma=4, output_len=1024, prompt_len=128, seed=0)
+    spec = M.DecodeSpec(n_req=args.n_req, gamma=4, output_len=args.out_len, prompt_len=128, seed=0,
+                        temperature=args.temperature)
     pair = M.build_pair(M.LLAMA_31_8B, M.LLAMA_32_1B, n_req=args.n_req,
                         ctx_cap=spec.ctx_cap(), seed=0, target_branch=args.branch,
                         draft_branch=args.branch)
