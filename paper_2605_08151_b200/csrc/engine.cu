@@ -392,8 +392,7 @@ struct ModelRT {
     TRY(gemm_run(plm, s));
     if (sampling) {
       if (sample_rows)
-        TRY(launch_sample_rows(logits, dm.vocab, bt.t_dev, rows_cap, bt.pos, bt.slot, inv_t, seed,
-                               lstat, bt.out_tok, s));
+        TRY(launch_sample_rows(logits, dm.vocab, bt, rows_cap, inv_t, seed, lstat, s));
     } else {
       TRY(launch_argmax_reduce(amax_v, amax_i, (plm.grid) * 8, rows_cap, bt.t_dev, rows_cap,
                                bt.out_tok, nullptr, s));

@@ -156,9 +156,8 @@ int launch_draft_append(const DecodeStateDev& st, const BatchDev& bt, int which,
 int launch_verify_prep(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);
 int launch_accept(const DecodeStateDev& st, const BatchDev& bt, cudaStream_t s);
 // sampling.cu
-int launch_sample_rows(const float* logits, int V, const int* t_dev, int t_cap,
-                       const int* tok_pos, const int* tok_slot, float inv_t, uint64_t seed,
-                       float2* stats, int* out_tok, cudaStream_t s);
+int launch_sample_rows(const float* logits, int V, const BatchDev& bt, int t_cap, float inv_t,
+                       uint64_t seed, float2* stats, cudaStream_t s);
 int launch_draft_sample(const DecodeStateDev& st, const BatchDev& bt, const float* logits, int V,
                         float inv_t, float* qstore, float2* qstat, int W, cudaStream_t s);
 int launch_accept_sample(const DecodeStateDev& st, const BatchDev& bt, const float* logits, int V,

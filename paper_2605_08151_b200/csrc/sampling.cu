@@ -5,13 +5,19 @@
 // min(1, p_i(x) / q_i(x)); at the first rejection resample from
 // norm(max(0, p_i - q_i)); if every candidate survives, the bonus token is
 // drawn from p_{m}.  p = softmax(target logits / T), q = softmax(draft
-// logits / T).  Every random draw is a counter-based uniform keyed by
-// (seed, purpose, request, output position): results are reproducible and
-// independent of batch composition.
+// logits / T).
+//
+// Every draw is a Gumbel-max: argmax_k (log w_k + G_k) with G_k = -log(-log U_k)
+// is an exact sample from w / sum(w), so a draw is ONE coalesced pass over the
+// row (no CDF, no scan), fused with the online (max, sum exp) statistics the
+// ratio tests need.  U_k is counter-based (SplitMix64 of a per-draw key and k),
+// the key is (seed, purpose, request slot, output position): results are
+// reproducible and independent of batch composition, and an AR draw and a
+// speculative bonus draw at the same (request, position) use the same stream.
 //
 // Logits are materialised in fp32 by the lm_head GEMM (partial epilogue, one
-// split) — at most rows x V x 4 bytes (B=64, gamma=4: 164 MB), streamed once
-// per reduction pass.  Every per-row reduction has a fixed order.
+// split) and read once per pass with float4 loads.  Every per-row reduction has
+// a fixed order (per-thread strided order, then a fixed block tree).
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -21,6 +27,7 @@
 namespace spectre {
 
 constexpr int kSampThreads = 512;
+constexpr int kSampWarps = kSampThreads / 32;
 enum : uint64_t { kStreamDraftSample = 4, kStreamAccept = 5, kStreamResample = 6,
                   kStreamRowSample = 7 };
 
@@ -28,163 +35,171 @@ __device__ __forceinline__ double u53s(uint64_t h) {
   return (double)(h >> 11) * (1.0 / 9007199254740992.0);
 }
 
-// Block reductions with a fixed tree (kSampThreads threads).
-__device__ __forceinline__ float block_max(float v, float* sh) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) sh[w] = v;
-  __syncthreads();
-  if (w == 0) {
-    v = l < kSampThreads / 32 ? sh[l] : -INFINITY;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (l == 0) sh[32] = v;
-  }
-  __syncthreads();
-  v = sh[32];
-  __syncthreads();
-  return v;
-}
-__device__ __forceinline__ float block_sum(float v, float* sh) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) sh[w] = v;
-  __syncthreads();
-  if (w == 0) {
-    v = l < kSampThreads / 32 ? sh[l] : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (l == 0) sh[32] = v;
-  }
-  __syncthreads();
-  v = sh[32];
-  __syncthreads();
-  return v;
+// G_k for element k of the draw keyed `key`: SplitMix64 state key + (k+1)*phi,
+// 24-bit uniform in (0, 1), -log(-log U)
+__device__ __forceinline__ float gumbel(uint64_t key, int k) {
+  uint64_t z = key + (uint64_t)(k + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  const float u = ((float)(uint32_t)(z >> 40) + 0.5f) * (1.0f / 16777216.0f);
+  return -__logf(-__logf(u));
 }
 
-// (max, sum exp) of logits/T over V: a thread owns a contiguous chunk.
-struct RowStats {
-  float m, s;
+// One pass's running state: online (max, sum exp) of x = logit / T and the
+// Gumbel-max candidate (g, index).
+struct RowAcc {
+  float m, s, g;
+  int gi;
+  __device__ __forceinline__ void init() {
+    m = -INFINITY;
+    s = 0.f;
+    g = -INFINITY;
+    gi = 0x7fffffff;
+  }
+  __device__ __forceinline__ void add_stat(float x) {
+    if (x > m) {
+      s = s * __expf(m - x) + 1.f;
+      m = x;
+    } else {
+      s += __expf(x - m);
+    }
+  }
+  __device__ __forceinline__ void add_draw(float lw, int k) {   // log weight + Gumbel
+    if (lw > g || (lw == g && k < gi)) {
+      g = lw;
+      gi = k;
+    }
+  }
+  __device__ __forceinline__ void merge(const RowAcc& o) {
+    if (o.m > m) {
+      s = (m == -INFINITY ? 0.f : s * __expf(m - o.m)) + o.s;
+      m = o.m;
+    } else if (o.m != -INFINITY) {
+      s += o.s * __expf(o.m - m);
+    }
+    add_draw(o.g, o.gi);
+  }
 };
-__device__ RowStats row_stats(const float* __restrict__ l, int V, float inv_t, float* sh) {
-  const int per = (V + kSampThreads - 1) / kSampThreads;
-  const int b0 = threadIdx.x * per, b1 = min(V, b0 + per);
-  float m = -INFINITY;
-  for (int y = b0; y < b1; ++y) m = fmaxf(m, l[y] * inv_t);
-  m = block_max(m, sh);
-  float s = 0.f;
-  for (int y = b0; y < b1; ++y) s += __expf(l[y] * inv_t - m);
-  s = block_sum(s, sh);
-  return {m, s};
-}
 
-// Inverse-CDF draw over weights w(y) (>= 0) with total Z: the smallest y with
-// cumsum(w)[y] > u*Z.  Chunked: per-thread sums -> block exclusive scan ->
-// the owning thread scans its chunk.  `wfn(y)` returns the weight.
-template <class W>
-__device__ int sample_index(int V, double u, float Z, W wfn, float* sh, int* shi) {
-  const int per = (V + kSampThreads - 1) / kSampThreads;
-  const int b0 = threadIdx.x * per, b1 = min(V, b0 + per);
-  float part = 0.f;
-  for (int y = b0; y < b1; ++y) part += wfn(y);
-  // inclusive scan of per-thread sums in thread order (fixed)
-  sh[threadIdx.x] = part;
-  __syncthreads();
-  for (int d = 1; d < kSampThreads; d <<= 1) {
-    const float x = threadIdx.x >= d ? sh[threadIdx.x - d] : 0.f;
-    __syncthreads();
-    sh[threadIdx.x] += x;
-    __syncthreads();
-  }
-  const float total = sh[kSampThreads - 1];
-  const float target = (float)(u * (double)total);
-  const float incl = sh[threadIdx.x];
-  const float excl = threadIdx.x > 0 ? sh[threadIdx.x - 1] : 0.f;   // exact chunk bounds
-  if (threadIdx.x == 0) *shi = -1;
-  __syncthreads();
-  if (part > 0.f && target >= excl && target < incl) {
-    float c = excl;
-    int pick = b1 - 1;
-    for (int y = b0; y < b1; ++y) {
-      c += wfn(y);
-      if (c > target) {
-        pick = y;
-        break;
-      }
+// Fixed-tree block merge (xor butterfly in each warp, then warp 0 over the
+// warps in index order); every thread gets the result.
+__device__ RowAcc block_merge(RowAcc a, RowAcc* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    RowAcc b;
+    b.m = __shfl_xor_sync(0xffffffffu, a.m, o);
+    b.s = __shfl_xor_sync(0xffffffffu, a.s, o);
+    b.g = __shfl_xor_sync(0xffffffffu, a.g, o);
+    b.gi = __shfl_xor_sync(0xffffffffu, a.gi, o);
+    // lanes l and l^o merge in the same order (lower lane first): identical results
+    if (threadIdx.x & o) {
+      RowAcc lo = b;
+      lo.merge(a);
+      a = lo;
+    } else {
+      a.merge(b);
     }
-    *shi = pick;   // exactly one thread's chunk contains the target
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sh[w] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    RowAcc r = sh[0];
+    for (int i = 1; i < kSampWarps; ++i) r.merge(sh[i]);
+    sh[kSampWarps] = r;
   }
   __syncthreads();
-  int r = *shi;
-  if (r < 0) {   // rounding at the very top of the CDF: last positive-weight token
-    if (threadIdx.x == 0) {
-      int last = V - 1;
-      while (last > 0 && wfn(last) <= 0.f) --last;
-      *shi = last;
-    }
-    __syncthreads();
-    r = *shi;
-  }
+  const RowAcc r = sh[kSampWarps];
   __syncthreads();
-  (void)Z;
   return r;
 }
 
+// Statistics of x = l / T over a row and a Gumbel-max draw from softmax(x)
+// (key 0: statistics only); kCopy also streams the row to `dst`.
+template <bool kCopy, bool kDraw>
+__device__ RowAcc row_pass(const float* __restrict__ l, int V, float inv_t, uint64_t key,
+                           float* __restrict__ dst, RowAcc* sh) {
+  RowAcc a;
+  a.init();
+  const int V4 = V >> 2;
+  const float4* l4 = reinterpret_cast<const float4*>(l);
+#pragma unroll 4
+  for (int v = threadIdx.x; v < V4; v += kSampThreads) {
+    const float4 q = __ldg(l4 + v);
+    if (kCopy) reinterpret_cast<float4*>(dst)[v] = q;
+    const float x[4] = {q.x * inv_t, q.y * inv_t, q.z * inv_t, q.w * inv_t};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      a.add_stat(x[e]);
+      if (kDraw) a.add_draw(x[e] + gumbel(key, 4 * v + e), 4 * v + e);
+    }
+  }
+  for (int k = 4 * V4 + threadIdx.x; k < V; k += kSampThreads) {   // tail (V % 4)
+    const float q = l[k];
+    if (kCopy) dst[k] = q;
+    a.add_stat(q * inv_t);
+    if (kDraw) a.add_draw(q * inv_t + gumbel(key, k), k);
+  }
+  return block_merge(a, sh);
+}
+
 // ------------------------------------------------ per-row sample + stats
-// Every live row of a forward: (m, s) of logits/T into stats[row], and a
-// token sampled from p into out_tok[row] (used for admission, token 0 of the
-// output, and AR decoding).  Uniform key: (seed, 7, request slot, position).
+// Every live row of a forward: (m, s) of logits/T into stats[row]; the last
+// row of each request also draws a token from p into out_tok[row] (admission,
+// token 0 of the output, AR decoding, the bonus token of a verify pass — the
+// other rows of a verify pass only need their statistics).  Key: (seed, 7,
+// request slot, input position).
+__device__ __forceinline__ uint64_t row_key(uint64_t seed, const BatchDev& bt, int row) {
+  return mix64(seed, kStreamRowSample, (uint64_t)bt.slot[row], (uint64_t)bt.pos[row]);
+}
+
 __global__ void __launch_bounds__(kSampThreads) k_sample_rows(
-    const float* __restrict__ logits, int V, const int* __restrict__ t_dev,
-    const int* __restrict__ tok_pos, const int* __restrict__ tok_slot, float inv_t,
-    uint64_t seed, float2* __restrict__ stats, int* __restrict__ out_tok) {
+    const float* __restrict__ logits, int V, BatchDev bt, float inv_t, uint64_t seed,
+    float2* __restrict__ stats) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float sh[kSampThreads + 64];
-  __shared__ int shi;
-  const int T = *t_dev;
+  __shared__ RowAcc sh[kSampWarps + 1];
+  const int T = *bt.t_dev;
   for (int row = blockIdx.x; row < T; row += gridDim.x) {
+    const int b = bt.slot[row];
     const float* l = logits + (size_t)row * V;
-    const RowStats st = row_stats(l, V, inv_t, sh);
-    if (threadIdx.x == 0) stats[row] = make_float2(st.m, st.s);
-    const double u = u53s(mix64(seed, kStreamRowSample, (uint64_t)tok_slot[row],
-                                (uint64_t)tok_pos[row]));
-    const int y = sample_index(V, u, st.s, [&](int k) { return __expf(l[k] * inv_t - st.m); },
-                               sh, &shi);
-    if (threadIdx.x == 0) out_tok[row] = y;
-    __syncthreads();
+    if (row == bt.q_off[b] + bt.n_new[b] - 1) {
+      const RowAcc r = row_pass<false, true>(l, V, inv_t, row_key(seed, bt, row), nullptr, sh);
+      if (threadIdx.x == 0) {
+        stats[row] = make_float2(r.m, r.s);
+        bt.out_tok[row] = r.gi;
+      }
+    } else {
+      const RowAcc r = row_pass<false, false>(l, V, inv_t, 0, nullptr, sh);
+      if (threadIdx.x == 0) stats[row] = make_float2(r.m, r.s);
+    }
   }
 }
 
 // ------------------------------------------------ draft sampling step
-// The draft's token for request b at draft-history position hl = q-sample of
-// its last row; the logits row and its stats are kept in q-store slot
-// hl % W (the accept step needs q at every candidate position).
+// The draft's token for request b at draft-history position hl = a q-draw
+// from its last row; the logits row (streamed in the same pass) and its
+// stats are kept in q-store slot hl % W (the accept step needs q at every
+// candidate position).
 __global__ void __launch_bounds__(kSampThreads) k_draft_sample(
     DecodeStateDev s, BatchDev bt, const float* __restrict__ logits, int V, float inv_t,
     float* __restrict__ qstore, float2* __restrict__ qstat, int W) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float sh[kSampThreads + 64];
-  __shared__ int shi;
+  __shared__ RowAcc sh[kSampWarps + 1];
   const int b = blockIdx.x;
   if (b >= s.n_req || bt.n_new[b] <= 0) return;
   if (!(s.gen_count[b] > 0 && s.gen_done[b] < s.gen_count[b])) return;
   const int row = bt.q_off[b] + bt.n_new[b] - 1;
   const int hl = s.hist_len[b];                       // output position being drafted
-  const float* l = logits + (size_t)row * V;
-  const RowStats st = row_stats(l, V, inv_t, sh);
-  const double u = u53s(mix64(s.seed, kStreamDraftSample, (uint64_t)b, (uint64_t)hl));
-  const int y = sample_index(V, u, st.s, [&](int k) { return __expf(l[k] * inv_t - st.m); }, sh,
-                             &shi);
   const int slot = hl % W;
-  float* q = qstore + ((size_t)b * W + slot) * V;
-  for (int k = threadIdx.x; k < V; k += kSampThreads) q[k] = l[k];
+  const uint64_t key = mix64(s.seed, kStreamDraftSample, (uint64_t)b, (uint64_t)hl);
+  const RowAcc r = row_pass<true, true>(logits + (size_t)row * V, V, inv_t, key,
+                                        qstore + ((size_t)b * W + slot) * V, sh);
   if (threadIdx.x == 0) {
-    qstat[b * W + slot] = make_float2(st.m, st.s);
-    bt.out_tok[row] = y;
+    qstat[b * W + slot] = make_float2(r.m, r.s);
+    bt.out_tok[row] = r.gi;
   }
 }
 
@@ -199,8 +214,7 @@ __global__ void __launch_bounds__(kSampThreads) k_accept_sample(
     int* __restrict__ out_bonus) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float sh[kSampThreads + 64];
-  __shared__ int shi;
+  __shared__ RowAcc sh[kSampWarps + 1];
   const int b = blockIdx.x;
   if (b >= s.n_req || s.vkind[b] == 0) return;
   const int m = s.vcand_n[b];
@@ -220,7 +234,6 @@ __global__ void __launch_bounds__(kSampThreads) k_accept_sample(
   }
   const float* lp = logits + (size_t)(row0 + a) * V;
   const float2 ts = tstat[row0 + a];
-  const double u2 = u53s(mix64(s.seed, kStreamResample, (uint64_t)b, (uint64_t)(pos + a)));
   // Parallel rounds: the draft's fresh speculation starts AT the bonus position
   // (its head token is a proposal for the token this round emits).  It goes
   // through the same min(1, p/q) test instead of being matched against an
@@ -250,32 +263,43 @@ __global__ void __launch_bounds__(kSampThreads) k_accept_sample(
       head = true;   // rejected: residual resample against the head's q
     }
   }
-  int y;
-  if (a < m || head) {   // resample from norm(max(0, p - q)) at the rejected position
+  // every candidate accepted: the bonus is row m's own draw from p (k_sample_rows)
+  int y = a < m ? -1 : bt.out_tok[row0 + a];
+  if (a < m || head) {
+    // resample from norm(max(0, p - q)) at the rejected position: Gumbel-max
+    // over log(p - q) where positive; an empty residual (p == q) keeps row a's
+    // own draw from p (independent of the acceptance uniforms)
     const int slot = (pos + a) % W;
     const float* lq = qstore + ((size_t)b * W + slot) * V;
     const float2 qs = qstat[b * W + slot];
-    auto wres = [&](int k) {
-      const float p = __expf(lp[k] * inv_t - ts.x) / ts.y;
-      const float q = __expf(lq[k] * inv_t - qs.x) / qs.y;
-      return fmaxf(p - q, 0.f);
+    const uint64_t key = mix64(s.seed, kStreamResample, (uint64_t)b, (uint64_t)(pos + a));
+    const float4* p4 = reinterpret_cast<const float4*>(lp);
+    const float4* q4 = reinterpret_cast<const float4*>(lq);
+    const float inv_sp = 1.f / ts.y, inv_sq = 1.f / qs.y;
+    RowAcc acc;
+    acc.init();
+    auto one = [&](float lpk, float lqk, int k) {
+      const float w = __expf(lpk * inv_t - ts.x) * inv_sp - __expf(lqk * inv_t - qs.x) * inv_sq;
+      if (w > 0.f) acc.add_draw(__logf(w) + gumbel(key, k), k);
     };
-    float z = 0.f;
-    {
-      const int per = (V + kSampThreads - 1) / kSampThreads;
-      const int b0 = threadIdx.x * per, b1 = min(V, b0 + per);
-      for (int k = b0; k < b1; ++k) z += wres(k);
-      z = block_sum(z, sh);
+    const int V4 = V >> 2;
+#pragma unroll 2
+    for (int v = threadIdx.x; v < V4; v += kSampThreads) {
+      const float4 pp = __ldg(p4 + v), qq = __ldg(q4 + v);
+      one(pp.x, qq.x, 4 * v);
+      one(pp.y, qq.y, 4 * v + 1);
+      one(pp.z, qq.z, 4 * v + 2);
+      one(pp.w, qq.w, 4 * v + 3);
     }
-    if (z > 0.f) {
-      y = sample_index(V, u2, z, wres, sh, &shi);
-    } else {   // p == q: the residual is empty, draw from p
-      y = sample_index(V, u2, ts.y, [&](int k) { return __expf(lp[k] * inv_t - ts.x); }, sh,
-                       &shi);
+    for (int k = 4 * V4 + threadIdx.x; k < V; k += kSampThreads) one(lp[k], lq[k], k);
+    const RowAcc r = block_merge(acc, sh);
+    if (r.gi != 0x7fffffff) {
+      y = r.gi;
+    } else if (y < 0) {
+      // empty residual (p == q) below the last row: row a's own draw from p,
+      // the one k_sample_rows would have made (same key)
+      y = row_pass<false, true>(lp, V, inv_t, row_key(s.seed, bt, row0 + a), nullptr, sh).gi;
     }
-  } else {       // every candidate accepted: bonus from p_m
-    y = sample_index(V, u2, ts.y, [&](int k) { return __expf(lp[k] * inv_t - ts.x); }, sh,
-                     &shi);
   }
   if (threadIdx.x == 0) {
     out_a[b] = a;
@@ -284,12 +308,10 @@ __global__ void __launch_bounds__(kSampThreads) k_accept_sample(
 }
 
 // ------------------------------------------------------------------ launchers
-int launch_sample_rows(const float* logits, int V, const int* t_dev, int t_cap,
-                       const int* tok_pos, const int* tok_slot, float inv_t, uint64_t seed,
-                       float2* stats, int* out_tok, cudaStream_t s) {
+int launch_sample_rows(const float* logits, int V, const BatchDev& bt, int t_cap, float inv_t,
+                       uint64_t seed, float2* stats, cudaStream_t s) {
   SPECTRE_LAUNCH_PDL("k_sample_rows", k_sample_rows, dim3((t_cap < 296 ? t_cap : 296)),
-                     dim3(kSampThreads), 0, s, logits, V, t_dev, tok_pos, tok_slot, inv_t, seed,
-                     stats, out_tok);
+                     dim3(kSampThreads), 0, s, logits, V, bt, inv_t, seed, stats);
   return SPECTRE_OK;
 }
 int launch_draft_sample(const DecodeStateDev& st, const BatchDev& bt, const float* logits, int V,
