@@ -516,8 +516,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
     const int et = threadIdx.x - 64;           // 0..255
     const int q = warp & 3;                    // TMEM lane quarter
     const int grp = (warp - 2) >> 2;           // 0 / 1: alternating 32-token chunks
-    const bool issuer = (warp == 2 + 4 * grp) && lane == 0;
-    int jn = 0, wbuf = 0, sbuf = 0;
+    int jn = 0, wbuf = 0;
     for (int p = 0; p < a.n_phase; ++p) {
       const int kind = a.kind[p];
       if (p > 0) {   // inputs of this phase: every CTA finished phase p - 1
@@ -583,19 +582,20 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
                 asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(0.5f * gt));
                 out[jj] = gt * fmaf(0.5f, th, 0.5f) * up;
               }
-              uint8_t* stg = stage_out + grp * 16384 + sbuf * 8192;
-              sbuf ^= 1;
-              if (issuer) bulk_wait_read<1>();
-              asm volatile("bar.sync %0, 128;" ::"r"(2 + grp) : "memory");
-              __nv_bfloat16* st = reinterpret_cast<__nv_bfloat16*>(stg);
-              const int fi = (q * 32 + lane) >> 1;
+              // per-warp [32 tokens][16 features] box (its 16 row pairs)
+              __nv_bfloat16* wst = reinterpret_cast<__nv_bfloat16*>(stage_out + grp * 16384 +
+                                                                      q * 4096 + wbuf * 2048);
+              wbuf ^= 1;
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+              const int fi = lane >> 1;
 #pragma unroll
               for (int jj = 0; jj < 16; ++jj)
-                st[((odd ? 16 : 0) + jj) * 64 + fi] = __float2bfloat16_rn(out[jj]);
+                wst[((odd ? 16 : 0) + jj) * 16 + fi] = __float2bfloat16_rn(out[jj]);
               fence_proxy_async_smem();
-              asm volatile("bar.sync %0, 128;" ::"r"(2 + grp) : "memory");
-              if (issuer) {
-                tma_store_2d(to[gi], stg, (j.tile * 128) >> 1, j.t0 + cc);
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(to[gi], wst, (j.tile * 128 + q * 32) >> 1, j.t0 + cc);
                 bulk_commit();
               }
               stored = true;
@@ -604,7 +604,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
           tc_fence_before();
           mbar_arrive(&tmem_empty[buf]);
         }
-        if (stored && (issuer || (kind == kPhGemmPartial && lane == 0))) {
+        if (stored && lane == 0) {
           bulk_wait_all();   // this phase's outputs are in global memory ...
           asm volatile("fence.proxy.async.global;" ::: "memory");   // ... and visible
         }

@@ -93,7 +93,7 @@ int gemm_set_outputs(GemmPlan* p, float* part, float* amax_val, int* amax_idx, v
   if (p->epi == kSwiGLU && act) {
     if ((ld_act * 2) % 16) return arg_fail("gemm: act rows must be 16-byte aligned");
     if (int e = make_tmap_store(&p->tmap_out, act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                                (uint64_t)ld_act, (uint64_t)p->args.rows_cap, 64, 32))
+                                (uint64_t)ld_act, (uint64_t)p->args.rows_cap, 16, 32))
       return e;
   }
   if (p->args.stream_k && p->args.sk_part) {

@@ -105,9 +105,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// x * sigmoid(x) with the fast reciprocal: the IEEE division expanded to a long
-// sequence with a slow path and was ~40 % of the SwiGLU epilogue at T=256
-__device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 // one MUFU op: sigmoid(x) = 0.5 tanh(x/2) + 0.5 (tanh.approx: ~2^-11 relative,
 // below the bf16 output's precision)
 __device__ __forceinline__ float silu_tanh(float x) {
@@ -663,23 +660,28 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
             const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
             const float g = odd ? recv : v[jj];
             const float u = odd ? v[jj + 16] : recv;
-            out[jj] = (a.diag & 16) ? g * u
-                      : ((a.diag & 32) ? silu_f(g) : silu_tanh(g)) * u;   // diag 16: no SiLU
+            out[jj] = silu_tanh(g) * u;
           }
           if (a.diag & 8) {   // diagnostics: no staging / store
             if (out[0] == 12345.f) a.part[0] = out[1];
             continue;
           }
-          // stage [32 tokens][64 features] bf16, store the box at (f0, c0)
-          stage_begin();
-          __nv_bfloat16* st = reinterpret_cast<__nv_bfloat16*>(stg);
-          const int fi = srow >> 1;
+          // each warp stages its own [32 tokens][16 features] bf16 box (its 32
+          // rows = 16 row pairs) and stores it: no cross-warp barrier per chunk
+          __nv_bfloat16* wst = reinterpret_cast<__nv_bfloat16*>(stage_out + grp * 16384 +
+                                                                  q * 4096 + wbuf * 2048);
+          wbuf ^= 1;
+          if (lane == 0) bulk_wait_read<1>();   // the store two steps back has read it
+          __syncwarp();
+          const int fi = lane >> 1;
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj)
-            st[((odd ? 16 : 0) + jj) * 64 + fi] = __float2bfloat16_rn(out[jj]);
-          stage_end();
-          if (issuer) {
-            tma_store_2d(&tmap_out, stg, (j.tile * a.tile_rows + j.row_off + box * 128) >> 1, c0);
+            wst[((odd ? 16 : 0) + jj) * 16 + fi] = __float2bfloat16_rn(out[jj]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmap_out, wst, (j.tile * a.tile_rows + j.row_off + box * 128 + q * 32) >> 1,
+                         c0);
             bulk_commit();
           }
         }
@@ -715,7 +717,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       if (j.role != 2) ++amax_jobs;
       ++jn;
     }
-    if (issuer || (kEpi == kPartial && lane == 0)) {   // outputs complete (and visible to
+    if (issuer || (kEpi != kArgmax && lane == 0)) {   // outputs complete (and visible to
       bulk_wait_all();                                // generic loads) before the grid does
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
