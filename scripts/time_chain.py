@@ -1,6 +1,6 @@
 """Draft-chain timing sweep (diagnostics): the mid-layer chains back to back
 (as bench.py's roofline leg) and ordinary C2 rounds in context, for each value
-of an environment knob read at chain launch (default SPECTRE_CHAIN_PF).
+of an environment knob (default SPECTRE_CHAIN_PF), one process per value.
     python scripts/time_chain.py [--knob SPECTRE_CHAIN_PF] [--values 0,8,16,32]"""
 import argparse
 import ctypes as C
@@ -19,6 +19,14 @@ ap.add_argument("--values", default="0,8,16,32")
 ap.add_argument("--out-len", type=int, default=384)
 ap.add_argument("--variant", default="ordinary")
 args = ap.parse_args()
+if "," in args.values:
+    # one process per value: the library reads most knobs once per process
+    import subprocess
+    for v in args.values.split(","):
+        subprocess.run([sys.executable, __file__, "--knob", args.knob, "--values", v,
+                        "--out-len", str(args.out_len), "--variant", args.variant],
+                       env={**os.environ, args.knob: v}, check=True)
+    sys.exit(0)
 
 L = _native.lib()
 B, G = 64, 4
