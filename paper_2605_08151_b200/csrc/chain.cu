@@ -251,7 +251,7 @@ __device__ void chain_norm_rows_t(const ChainArgs& a, int T, int phase, int et, 
 __device__ void chain_norm_rows(const ChainArgs& a, int T, int phase, int et, float* sh) {
   const int nv = a.d >> 2;
   if (nv <= kChainEpiThreads) chain_norm_rows_t<1, 8>(a, T, phase, et, sh);
-  else chain_norm_rows_t<2, 4>(a, T, phase, et, sh);   // d <= 2048 (chain_set_model)
+  else chain_norm_rows_t<2, 5>(a, T, phase, et, sh);   // d <= 2048 (chain_set_model)
 }
 
 // RoPE (rotate-half pairs (i, i + hd/2)) on the summed q/k/v partials; q to
@@ -614,11 +614,15 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
       } else if (T > 0 && kind == kPhRope) {
         chain_rope(a, T, et);
       }
-      __threadfence();
+      // arrive: the CTA barrier orders every epilogue thread's results before
+      // thread 0's gpu-scope release (cumulative), which publishes them with
+      // the arrival (one fence per CTA instead of one per thread)
       asm volatile("bar.sync 1, %0;" ::"n"(kChainEpiThreads) : "memory");
       if (stamp) a.dbg[2 + 2 * p] = gtimer_ns();         // this CTA finished phase p
       if (et == 0) {
-        const unsigned prev = atomicAdd(a.bar, 1u);
+        unsigned prev;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;"
+                     : "=r"(prev) : "l"(a.bar) : "memory");
         // the last arrival of the last phase: every CTA is past every wait
         if (p == a.n_phase - 1 && prev == (unsigned)(G * a.n_phase) - 1u) atomicExch(a.bar, 0u);
       }
