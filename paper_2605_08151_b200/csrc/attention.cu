@@ -81,49 +81,37 @@ struct AttnWCfg {
   static constexpr int kBoxBytes = kKeys * 128;               // 32 keys x 64 elements
   static constexpr int kStageBytes = 2 * kBoxes * kBoxBytes;  // K + V
   static constexpr int kWarpRing = NS * kStageBytes;
-  static constexpr int kQBytes = 16 * HD * 2;
-  static constexpr int kSmem = 1024 + NWARP * (kWarpRing + kQBytes) + NWARP * NS * 8 + 64;
+  static constexpr int kSmem = 1024 + NWARP * kWarpRing + NWARP * NS * 8 + 64;
 };
 
 __device__ __forceinline__ uint32_t swz32(int key, int col) {   // 32-row boxes
   return (uint32_t)((col >> 6) * (32 * 128) + key * 128 + ((((col & 63) >> 3) ^ (key & 7)) << 4));
 }
 
-template <int HD, int NWARP, int NS, int NP>
-__global__ void __launch_bounds__(NWARP * 32, 1)
-k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-         AttnArgs a) {
-  // NP warps per item: warp `sub` of the group takes the stages whose
-  // absolute index is sub mod NP (batch invariant), merged at the end.
-  using C = AttnWCfg<HD, NWARP, NS>;
-  static_assert(NWARP % NP == 0, "warp groups");
+// The work-item loop of one attention warp (also run by the draft chain's
+// epilogue warps as its attention phase, chain.cu).  ring: this warp's NS-stage
+// K/V ring (NS * kStageBytes, 1024-aligned), full: its NS initialised
+// mbarriers; NP == 2: xch is the ring of the group's second warp (the state
+// exchange buffer) and bar_id a named barrier for the pair.  warps_per_cta:
+// attention warps per CTA (slot layout).  *waited: griddepcontrol.wait done;
+// before it only keys of earlier rounds (below pos0) are streamed.
+template <int HD, int NS, int NP>
+__device__ void attn_warp_items(const CUtensorMap* tm_k, const CUtensorMap* tm_v,
+                                const AttnArgs& a, int warp, int warps_per_cta, uint8_t* ring,
+                                uint64_t* full, uint8_t* xch_ring, int bar_id, bool* waited_io) {
+  using C = AttnWCfg<HD, 1, NS>;
   using namespace ptx;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = smem + warp * C::kWarpRing;
-  __nv_bfloat16* sQ =
-      reinterpret_cast<__nv_bfloat16*>(smem + NWARP * C::kWarpRing + warp * C::kQBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NWARP * (C::kWarpRing + C::kQBytes)) +
-                   warp * NS;
-  if (lane == 0) {
-    for (int s2 = 0; s2 < NS; ++s2) mbar_init(&full[s2], 1);
-    fence_barrier_init();
-    prefetch_tmap(&tm_k);
-    prefetch_tmap(&tm_v);
-  }
-  __syncwarp();
+  const int lane = threadIdx.x & 31;
   const uint64_t pol = policy_evict_first();
   const int group = a.n_q / a.n_kv;
   const int n_rblk = a.rb_max;                 // 16-row m-tiles per request
   const int n_pairs = a.n_req * a.n_kv;
   const int n_items = n_pairs * a.split_max * n_rblk;
-  const int slots = gridDim.x * (NWARP / NP);
+  const int slots = gridDim.x * (warps_per_cta / NP);
   const int g8 = lane >> 2, tq = lane & 3;
   const int pw = warp / NP, sub = warp % NP;
   int g = 0;                                    // this warp's stage counter
-  bool waited = false;
+  bool waited = *waited_io;
 
   for (int item = pw * gridDim.x + blockIdx.x; item < n_items; item += slots) {
     // (row block, split, request, kv head), row block slowest
@@ -156,8 +144,8 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
       mbar_arrive_expect_tx(&full[sl], C::kStageBytes);
 #pragma unroll
       for (int bx = 0; bx < C::kBoxes; ++bx) {
-        tma_load_2d(dst + bx * C::kBoxBytes, &tm_k, &full[sl], bx * 64, row0 + k0, pol);
-        tma_load_2d(dst + (C::kBoxes + bx) * C::kBoxBytes, &tm_v, &full[sl], bx * 64,
+        tma_load_2d(dst + bx * C::kBoxBytes, tm_k, &full[sl], bx * 64, row0 + k0, pol);
+        tma_load_2d(dst + (C::kBoxes + bx) * C::kBoxBytes, tm_v, &full[sl], bx * 64,
                     row0 + k0, pol);
       }
     };
@@ -174,25 +162,28 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
     }
     if (lane == 0)
       for (int st = pre; st < NS && st < n_stages; ++st) issue(st);
-    // ---- Q rows of this m-tile -> smem -> fragments
-    for (int c = lane; c < 16 * (HD / 8); c += 32) {
-      const int rr = c / (HD / 8), ch = c % (HD / 8);
-      const int R = row_lo + rr;
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (R < rows_total) {
-        const int j = R / group, hh = R % group;
-        v = *reinterpret_cast<const uint4*>(
-            a.q + (((size_t)(a.q_off[b] + j) * a.n_q) + kvh * group + hh) * HD + ch * 8);
-      }
-      *reinterpret_cast<uint4*>(sQ + rr * HD + ((ch ^ (rr & 7)) * 8)) = v;   // 16B-chunk swizzle
-    }
-    __syncwarp();
+    // ---- Q fragments of this m-tile straight from global (m16n8k16 A layout:
+    // regs 0 / 1 rows g8 / g8 + 8 at cols 2tq, regs 2 / 3 the same at cols 2tq + 8)
     uint32_t qf[HD / 16][4];
+    {
+      const __nv_bfloat16* qrow[2];
 #pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      const int rr = lane & 15, ch = kk * 2 + (lane >> 4);
-      ldsm_x4(smem_u32(sQ + rr * HD + ((ch ^ (rr & 7)) * 8)), qf[kk][0], qf[kk][1], qf[kk][2],
-              qf[kk][3]);
+      for (int hr = 0; hr < 2; ++hr) {
+        const int R = row_lo + g8 + hr * 8;
+        qrow[hr] = nullptr;
+        if (R < rows_total) {
+          const int j = R / group, hh = R % group;
+          qrow[hr] = a.q + (((size_t)(a.q_off[b] + j) * a.n_q) + kvh * group + hh) * HD;
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const __nv_bfloat16* qr = qrow[e & 1];
+          qf[kk][e] = qr ? *reinterpret_cast<const uint32_t*>(qr + kk * 16 + (e >> 1) * 8 + 2 * tq)
+                         : 0u;
+        }
     }
     float o[HD / 8][4];
 #pragma unroll
@@ -291,7 +282,7 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
     if (NP == 2) {
       // fold warp 1's state into warp 0's (same lane layout) through warp 1's
       // now idle ring, fixed order (stages of parity 0, then parity 1)
-      float* xch = reinterpret_cast<float*>(smem + (pw * NP + 1) * C::kWarpRing);
+      float* xch = reinterpret_cast<float*>(xch_ring);
       if (sub == 1) {
 #pragma unroll
         for (int n = 0; n < HD / 8; ++n)
@@ -303,7 +294,7 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
           xch[(HD / 2 + hr * 2 + 1) * 32 + lane] = lrow[hr];
         }
       }
-      bar_named(1 + pw, 64);
+      bar_named(bar_id, 64);
       if (sub == 0) {
 #pragma unroll
         for (int hr = 0; hr < 2; ++hr) {
@@ -321,7 +312,7 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
           mrow[hr] = M;
         }
       }
-      bar_named(1 + pw, 64);   // warp 1's ring is free again
+      bar_named(bar_id, 64);   // warp 1's ring is free again
       fence_proxy_async_smem();
       if (sub == 1) continue;
     }
@@ -405,6 +396,34 @@ k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUten
       dst[1] = __floats2bfloat162_rn(O.z * inv, O.w * inv);
     }
   }
+  *waited_io = waited;
+}
+
+template <int HD, int NWARP, int NS, int NP>
+__global__ void __launch_bounds__(NWARP * 32, 1)
+k_attn_w(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+         AttnArgs a) {
+  // NP warps per item: warp `sub` of the group takes the stages whose
+  // absolute index is sub mod NP (batch invariant), merged at the end.
+  using C = AttnWCfg<HD, NWARP, NS>;
+  static_assert(NWARP % NP == 0, "warp groups");
+  using namespace ptx;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NWARP * C::kWarpRing) + warp * NS;
+  if (lane == 0) {
+    for (int s2 = 0; s2 < NS; ++s2) mbar_init(&full[s2], 1);
+    fence_barrier_init();
+    prefetch_tmap(&tm_k);
+    prefetch_tmap(&tm_v);
+  }
+  __syncwarp();
+  bool waited = false;
+  const int pw = warp / NP;
+  attn_warp_items<HD, NS, NP>(&tm_k, &tm_v, a, warp, NWARP, smem + warp * C::kWarpRing, full,
+                              smem + (pw * NP + NP - 1) * C::kWarpRing, 1 + pw, &waited);
   if (!waited) {
     pdl_wait();
     pdl_trigger();
