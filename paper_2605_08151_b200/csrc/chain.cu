@@ -34,6 +34,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "chain.h"
 #include "common.cuh"
@@ -56,15 +57,23 @@ constexpr int kChainMaxPhases = 8;
 // tokens: 16 KB per block): both producers fill their half of a stage (one
 // full barrier, two arrivals + tx bytes) and ONE MMA commit releases it — the
 // tcgen05 commit is the MMA issuer's expensive step at T = 64.
-constexpr int kChainKS = 2;
-constexpr int kChainStages = 3;
-constexpr int kChainPass = 128;                // tokens per MMA pass
 constexpr int kChainWBox = 128 * 128;           // one k block of weights
-constexpr int kChainXBlk = kChainPass * 128;     // one k block of activations
-constexpr int kChainStageBytes = kChainKS * (kChainWBox + kChainXBlk);
 constexpr int kChainStageOut = 2 * 16384;
-constexpr int kChainSmem = 1024 + kChainStages * kChainStageBytes + kChainStageOut + 1024;
-static_assert(kChainSmem <= 232448, "chain smem");
+// kPass tokens per MMA pass: 128 (decode steps of <= 128 requests: two k
+// blocks per stage, three stages) or 256 (larger batches, e.g. config 3's
+// B = 256: one N = 256 MMA chain per job instead of two passes that stream
+// every weight tile twice; one k block per stage, four stages).  Both keep
+// 96 / 64 KB of weights and 192 KB of ring in flight per SM.
+template <int kPass>
+struct ChainCfg {
+  static constexpr int kKS = kPass == 128 ? 2 : 1;
+  static constexpr int kStages = kPass == 128 ? 3 : 4;
+  static constexpr int kXBlk = kPass * 128;     // one k block of activations
+  static constexpr int kStageBytes = kKS * (kChainWBox + kXBlk);
+  static constexpr int kSmem = 1024 + kStages * kStageBytes + kChainStageOut + 1024;
+  static constexpr int kTmemCols = 2 * kPass;   // two accumulator buffers
+  static_assert(kSmem <= 232448, "chain smem");
+};
 
 struct ChainGemm {
   int N, K, splits, tiles, kb;   // kb: K / 64
@@ -109,12 +118,13 @@ struct ChainJob {
 
 // Jobs of GEMM slot `g` owned by CTA c of G: units (pass, split, tile), tile fastest.
 struct ChainSched {
-  int units, c, G, T;
-  __device__ __forceinline__ void init(const ChainGemm& g, int T_, int c_, int G_) {
+  int units, c, G, T, pass_t;
+  __device__ __forceinline__ void init(const ChainGemm& g, int T_, int c_, int G_, int pass_) {
     T = T_;
     c = c_;
     G = G_;
-    const int passes = (T + kChainPass - 1) / kChainPass;
+    pass_t = pass_;
+    const int passes = (T + pass_t - 1) / pass_t;
     units = g.tiles * g.splits * passes;
   }
   __device__ __forceinline__ bool get(const ChainGemm& g, int i, ChainJob& j) const {
@@ -127,8 +137,8 @@ struct ChainSched {
     j.split = r / g.tiles;
     j.k0 = (int)((long long)g.kb * j.split / g.splits);
     j.k1 = (int)((long long)g.kb * (j.split + 1) / g.splits);
-    j.t0 = pass * kChainPass;
-    j.nt = min(kChainPass, T - j.t0);
+    j.t0 = pass * pass_t;
+    j.nt = min(pass_t, T - j.t0);
     return true;
   }
 };
@@ -322,6 +332,7 @@ __device__ void chain_rope(const ChainArgs& a, int T, int et) {
   }
 }
 
+template <int kPass>
 __global__ void __launch_bounds__(kChainThreads, 1)
 k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtensorMap tw1,
         const __grid_constant__ CUtensorMap tw2, const __grid_constant__ CUtensorMap tw3,
@@ -331,6 +342,11 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
         const __grid_constant__ CUtensorMap to2, const __grid_constant__ CUtensorMap to3,
         ChainArgs a) {
   using namespace ptx;
+  using Cfg = ChainCfg<kPass>;
+  constexpr int kChainKS = Cfg::kKS;
+  constexpr int kChainStages = Cfg::kStages;
+  constexpr int kChainXBlk = Cfg::kXBlk;
+  constexpr int kChainStageBytes = Cfg::kStageBytes;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -368,7 +384,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -391,7 +407,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
         if (a.kind[p] != kPhGemmPartial && a.kind[p] != kPhGemmSwiGLU) continue;
         const ChainGemm& g = a.g[a.gemm[p]];
         ChainSched sc;
-        sc.init(g, T, c, G);
+        sc.init(g, T, c, G, kPass);
         ChainJob j;
         for (int i = 0; sc.get(g, i, j); ++i) {
           for (int kb = j.k0; kb < j.k1; kb += kChainKS, ++gw) {
@@ -434,7 +450,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
         if (a.kind[p] != kPhGemmPartial && a.kind[p] != kPhGemmSwiGLU) continue;
         const ChainGemm& g = a.g[a.gemm[p]];
         ChainSched sc;
-        sc.init(g, T, c, G);
+        sc.init(g, T, c, G, kPass);
         ChainJob j;
         // only CTAs with jobs wait: a CTA's own epilogue cannot finish a phase it
         // has jobs in before this wait passed, so no waiter can outlive the
@@ -471,11 +487,11 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
       if (a.kind[p] != kPhGemmPartial && a.kind[p] != kPhGemmSwiGLU) continue;
       const ChainGemm& g = a.g[a.gemm[p]];
       ChainSched sc;
-      sc.init(g, T, c, G);
+      sc.init(g, T, c, G, kPass);
       ChainJob j;
       for (int i = 0; sc.get(g, i, j); ++i, ++jn) {
         const int buf = jn & 1;
-        const uint32_t acc = tmem_base + (uint32_t)(buf * kChainPass);
+        const uint32_t acc = tmem_base + (uint32_t)(buf * kPass);
         const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)((j.nt + 15) & ~15));
         if (jn >= 2) {
           mbar_wait(&tmem_empty[buf], ((uint32_t)(jn >> 1) - 1u) & 1u);
@@ -529,7 +545,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
         const int gi = a.gemm[p];
         const ChainGemm& g = a.g[gi];
         ChainSched sc;
-        sc.init(g, T, c, G);
+        sc.init(g, T, c, G, kPass);
         ChainJob j;
         for (int i = 0; sc.get(g, i, j); ++i, ++jn) {
           const int buf = jn & 1;
@@ -537,7 +553,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
           tc_fence_after();
           if (stamp && i == 0) a.dbg[16 + 2 * p] = gtimer_ns();
           const int t_pad = (j.nt + 15) & ~15;
-          const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kChainPass);
+          const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kPass);
           for (int cc = 32 * grp; cc < t_pad; cc += 64) {
             uint32_t r[32];
             tmem_ld32_issue(tq + (uint32_t)cc, r);
@@ -632,7 +648,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem_base);
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   }
 }
 
@@ -664,20 +680,31 @@ int chain_splits(int N, int K) {
   return s;
 }
 
-int chain_launch(const void* plan_v, cudaStream_t s) {
-  const ChainPlan& cp = *reinterpret_cast<const ChainPlan*>(plan_v);
+template <int kPass>
+static int chain_launch_t(const ChainPlan& cp, cudaStream_t s) {
   static bool cfg = false;
   if (!cfg) {
-    SPECTRE_CUDA_TRY(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kChainSmem));
+    SPECTRE_CUDA_TRY(cudaFuncSetAttribute(k_chain<kPass>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          ChainCfg<kPass>::kSmem));
     cfg = true;
   }
   const GemmPlan* g = cp.gp;
-  SPECTRE_LAUNCH_PDL("k_chain", k_chain, dim3(chain_sms()), dim3(kChainThreads), kChainSmem, s,
-                     g[0].tmap_w, g[1].tmap_w, g[2].tmap_w, g[3].tmap_w, g[0].tmap_x, g[1].tmap_x,
-                     g[2].tmap_x, g[3].tmap_x, g[0].tmap_out, g[1].tmap_out, g[2].tmap_out,
-                     g[3].tmap_out, cp.args);
+  SPECTRE_LAUNCH_PDL("k_chain", k_chain<kPass>, dim3(chain_sms()), dim3(kChainThreads),
+                     ChainCfg<kPass>::kSmem, s, g[0].tmap_w, g[1].tmap_w, g[2].tmap_w,
+                     g[3].tmap_w, g[0].tmap_x, g[1].tmap_x, g[2].tmap_x, g[3].tmap_x,
+                     g[0].tmap_out, g[1].tmap_out, g[2].tmap_out, g[3].tmap_out, cp.args);
   return SPECTRE_OK;
+}
+
+int chain_launch(const void* plan_v, cudaStream_t s, int t_bound) {
+  const ChainPlan& cp = *reinterpret_cast<const ChainPlan*>(plan_v);
+  static const int pass256 = [] {   // SPECTRE_CHAIN_PASS=128: never the 256-token passes
+    const char* v = getenv("SPECTRE_CHAIN_PASS");
+    return v ? atoi(v) != 128 : 1;
+  }();
+  if (pass256 && t_bound > 128) return chain_launch_t<256>(cp, s);
+  return chain_launch_t<128>(cp, s);
 }
 
 void* chain_alloc() { return new ChainPlan(); }

@@ -42,6 +42,7 @@ int chain_add_gemm(void* plan, const void* W, int N, int K, const void* X, int r
 // Glue phase: kPhEmbed / kPhResid (RMSNorm weight norm_w) / kPhRope.
 int chain_add_glue(void* plan, int kind, const float* norm_w);
 int chain_splits(int N, int K);
-int chain_launch(const void* plan, cudaStream_t s);
+// t_bound: upper bound of the forward's token rows (selects 128- or 256-token MMA passes)
+int chain_launch(const void* plan, cudaStream_t s, int t_bound);
 
 }  // namespace spectre

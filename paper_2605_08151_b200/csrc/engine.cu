@@ -358,11 +358,12 @@ struct ModelRT {
     auto* kc = reinterpret_cast<__nv_bfloat16*>(w.k_cache);
     auto* vc = reinterpret_cast<__nv_bfloat16*>(w.v_cache);
     if (use_chain) {
-      TRY(chain_launch(ch_first, s));
+      const int t_bound = std::min(rows_cap, n_req * new_per_req);
+      TRY(chain_launch(ch_first, s, t_bound));
       for (int l = 0; l < L; ++l) {
         a.layer_row0 = l * n_req * dm.n_kv_heads * ctx_cap;
         TRY(launch_attention_w(tm_k32, tm_v32, a, hd, rows, s));
-        TRY(chain_launch(l + 1 < L ? ch_mid[l] : ch_last, s));
+        TRY(chain_launch(l + 1 < L ? ch_mid[l] : ch_last, s, t_bound));
       }
     }
     if (!use_chain) TRY(launch_embed_rmsnorm(bt.tok, bt.t_dev, rows_cap, w.embed, w.attn_norm, h,
@@ -958,7 +959,7 @@ extern "C" int spectre_engine_launch_chains(void* engine, int32_t reps, int64_t*
   int n = 0;
   for (int r = 0; r < reps; ++r)
     for (void* c : e->drf.ch_mid) {
-      TRY(chain_launch(c, s));
+      TRY(chain_launch(c, s, e->drf.n_req));   // decode-shaped: one token per request
       ++n;
     }
   return n;
