@@ -138,7 +138,8 @@ struct GemmSched {
     return iter_lo(cc + 1, G, total) > iter_lo(cc, G, total);
   }
 
-  __device__ __forceinline__ void init(const GemmArgs& a, int T_, int BK, int pass_ = 512) {
+  // chunked: CTA-pair plans cover any T as wide jobs over 256-token chunks
+  __device__ __forceinline__ void init(const GemmArgs& a, int T_, int BK, int pass_, bool chunked) {
     T = T_;
     pass = pass_;
     tile_rows = a.tile_rows;
@@ -146,10 +147,10 @@ struct GemmSched {
     KI = a.K / BK;
     G = gridDim.x;
     c = blockIdx.x;
-    wide = (T <= 256 && tile_rows == 256);
-    sk = a.stream_k && wide;
+    wide = chunked || (T <= 256 && tile_rows == 256);
+    sk = a.stream_k && wide && !chunked;
     splits = sk ? 1 : a.splits;
-    n_phases = wide ? 1 : (tile_rows / 128) * ((T + pass - 1) / pass);
+    n_phases = wide ? (T + 255) / 256 : (tile_rows / 128) * ((T + pass - 1) / pass);
     const int total = n_tiles * KI;
     it = sk ? iter_lo(c, G, total) : 0;
     hi = sk ? iter_lo(c + 1, G, total) : 0;
@@ -178,11 +179,11 @@ struct GemmSched {
     j.k0 = (int)((long long)KI * j.split / splits);
     j.k1 = (int)((long long)KI * (j.split + 1) / splits);
     j.role = 0;
-    if (wide) {
+    if (wide) {   // 256-token chunks (one unless chunked)
       j.row_off = 0;
       j.boxes = 2;
-      j.t0 = 0;
-      j.nt = T;
+      j.t0 = phase * 256;
+      j.nt = min(256, T - j.t0);
     } else {
       const int per = (T + pass - 1) / pass;
       j.row_off = (phase / per) * 128;
@@ -225,14 +226,17 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   constexpr int kRow = BK * 2;              // bytes per K-row segment (swizzle span)
   constexpr int kWBox = 128 * kRow;         // one 128-row weight box
   constexpr int kXBox = 64 * kRow;          // one 64-row activation box
-  const bool wide = (T <= 256 && a.tile_rows == 256);
-  const int w_bytes = wide ? 2 * kWBox : kWBox;
   // CTA pair: each CTA holds its own 256 weight rows and HALF of the token
-  // tile; one M=256 MMA per box spans both CTAs (the leader issues it)
-  const bool pair = kPair && wide && !kHalf;
+  // tile; one M=256 MMA per box spans both CTAs (the leader issues it).  Past
+  // 256 tokens a pair walks the tokens in 256-token chunks (weights re-read
+  // per chunk) so the MMAs stay M=256 x N=256 with both boxes sharing B.
+  const bool pair = kPair && !kHalf && a.pair && a.tile_rows == 256;
+  const int Tc = pair ? min(T, 256) : T;           // tokens per job
+  const bool wide = (Tc <= 256 && a.tile_rows == 256);
+  const int w_bytes = wide ? 2 * kWBox : kWBox;
   const uint32_t crank = kPair ? cluster_rank() : 0u;
   const bool leader = crank == 0;
-  const int x_half = ((T + 15) & ~15) / 2;         // tokens held by each CTA of a pair
+  const int x_half = ((Tc + 15) & ~15) / 2;        // tokens held by each CTA of a pair
   const int x_rows = pair ? ((x_half + 63) & ~63)
                           : (wide ? ((T + 63) & ~63) : min((T + 63) & ~63, Cfg::kPass));
   // a stage holds `ksub` consecutive BK-wide k blocks (one expect-tx, one
@@ -255,7 +259,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   stages = stages > kGemmMaxStages ? kGemmMaxStages : (stages < 1 ? 1 : stages);
   if (a.max_stages > 0 && stages > a.max_stages) stages = a.max_stages;
   // TMEM accumulator buffers: two whenever a job needs <= half the columns
-  const int t_pad_all = (T + 15) & ~15;
+  const int t_pad_all = (Tc + 15) & ~15;
   constexpr int kBufCols = Cfg::kTmemCols / 2;
   const int nbuf = ((wide && t_pad_all <= 128) || (!wide && t_pad_all <= kBufCols)) ? 2 : 1;
   const int half_stride = (wide && t_pad_all <= 128) ? 128 : 256;   // wide: 2nd accumulator
@@ -299,7 +303,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     pdl_trigger();
   }
   GemmSched sched;
-  sched.init(a, T, BK, Cfg::kPass);
+  sched.init(a, T, BK, Cfg::kPass, pair);
   if (a.dbg && threadIdx.x == 64) a.dbg[blockIdx.x * 8 + 0] = gtimer();
   const bool no_work = (T == 0);
 
@@ -332,10 +336,11 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
         if (!pair) mbar_arrive_expect_tx(&full[s2], bytes);
         else if (leader) mbar_arrive_expect_tx(&full[s2], 2 * bytes);
       };
+      // pair: this CTA's half of the job's (chunk's) tokens
+      auto xh_of = [&](const GemmJob& jj) { return ((jj.nt + 15) & ~15) / 2; };
       auto x_boxes_of = [&](const GemmJob& jj) {
-        return pair ? (x_half + 63) >> 6 : (jj.nt + 63) >> 6;
+        return pair ? (xh_of(jj) + 63) >> 6 : (jj.nt + 63) >> 6;
       };
-      const int x_t0 = pair ? (int)crank * x_half : 0;
       if (have) {
         const int x_boxes = x_boxes_of(j);
         const uint32_t tx = (uint32_t)j.boxes * kWBox + (uint32_t)x_boxes * kXBox;
@@ -372,6 +377,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
               for (int b = 0; b < j.boxes; ++b)
                 load_w(st + q * sub_bytes + b * kWBox, s, (k + q) * BK, n0 + b * 128);
           }
+          const int x_t0 = pair ? (int)crank * xh_of(j) : 0;
           for (int q = 0; q < nk; ++q)
             for (int b = 0; b < x_boxes; ++b)
               load_x(st + q * sub_bytes + w_bytes + b * kXBox, s, (k + q) * BK,

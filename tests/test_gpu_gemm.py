@@ -212,10 +212,11 @@ def test_argmax_no_stale_partials(env):
             assert torch.equal(idx[clear], logits.argmax(1)[clear]), (seed, T)
 
 
-@pytest.mark.parametrize("T", [16, 100, 256])
+@pytest.mark.parametrize("T", [16, 100, 256, 300, 512])
 def test_cta_pair_swiglu_at_8b_gate_up(env, T):
     """The verify gate/up GEMM exactly as the engine launches it at the 8B
-    shape (N = 2*14336, K = 4096): CTA pairs (cta_group::2, flag 4000) must be
+    shape (N = 2*14336, K = 4096): CTA pairs (cta_group::2, flag 4000; past 256
+    tokens in 256-token chunks: config 3's verify, prefill) must be
     bit-identical to the single-CTA 256-row kernel (flag 2000: same per-row
     k order) and within bf16 tolerance of the fp32 reference."""
     torch = env[0]
