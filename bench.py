@@ -455,8 +455,9 @@ def roofline_gate_up(pair, args):
     T = args.batch * args.gamma
     W = pair.target.wgu[0]
     F2, K = W.shape
-    X = torch.randn(512, K, device="cuda").bfloat16()
-    act = torch.empty(512, F2 // 2, dtype=torch.bfloat16, device="cuda")
+    rows = max(512, (T + 63) // 64 * 64)   # the kernel clamps T to the buffer's rows
+    X = torch.randn(rows, K, device="cuda").bfloat16()
+    act = torch.empty(rows, F2 // 2, dtype=torch.bfloat16, device="cuda")
     s = torch.cuda.Stream()
     times = []
     n_layers = pair.target.spec.n_layers
@@ -467,7 +468,7 @@ def roofline_gate_up(pair, args):
 
     def launch(layer):
         _native.check(L.spectre_gemm_bf16(X.data_ptr(), pair.target.wgu[layer].data_ptr(), None, T,
-                                          512, F2, K, 1, 2, None, None, None, act.data_ptr(),
+                                          rows, F2, K, 1, 2, None, None, None, act.data_ptr(),
                                           F2 // 2, flags, int(s.cuda_stream)), "gemm")
 
     # back-to-back launches over every layer's weights (> L2, PDL-chained as in

@@ -15,13 +15,13 @@ from paper_2605_08151_b200 import _native
 L = _native.lib()
 F, K, NL = 14336, 4096, 32
 W = torch.randn(NL, 2 * F, K, device="cuda").mul_(0.02).bfloat16()
-X = torch.randn(512, K, device="cuda").bfloat16()
-act = torch.empty(512, F, dtype=torch.bfloat16, device="cuda")
+X = torch.randn(1024, K, device="cuda").bfloat16()
+act = torch.empty(1024, F, dtype=torch.bfloat16, device="cuda")
 s = torch.cuda.Stream()
 for T in [int(a) for a in sys.argv[1:]] or [256, 128, 64]:
     for flags in (2000, 4000):
         def launch(l):
-            _native.check(L.spectre_gemm_bf16(X.data_ptr(), W[l].data_ptr(), None, T, 512, 2 * F,
+            _native.check(L.spectre_gemm_bf16(X.data_ptr(), W[l].data_ptr(), None, T, 1024, 2 * F,
                                               K, 1, 2, None, None, None, act.data_ptr(), F,
                                               flags, int(s.cuda_stream)), "gemm")
         times = []
