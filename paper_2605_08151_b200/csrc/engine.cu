@@ -349,7 +349,11 @@ struct ModelRT {
     a.split_max = split_max;
     a.chunk = attn_chunk;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
-    if (const char* dbg = getenv("SPECTRE_ATTN_DEBUG")) a.debug = atoi(dbg);
+    static const int attn_debug = [] {   // diagnostics (timing only), read once
+      const char* v = getenv("SPECTRE_ATTN_DEBUG");
+      return v ? atoi(v) : 0;
+    }();
+    a.debug = attn_debug;
     a.part_o = att_o;
     a.part_ml = att_ml;
     a.done_cnt = att_cnt;

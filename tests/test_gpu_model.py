@@ -118,6 +118,40 @@ def test_speculative_decoding_is_lossless(M, shapes, alpha):
             assert got.report.total_committed == n * spec.output_len
 
 
+@pytest.mark.parametrize("chain", ["0", "1"])
+def test_draft_per_op_and_chain_paths_agree(M, chain, monkeypatch):
+    """The draft's decode step as persistent chains (default) and as per-op
+    kernels (SPECTRE_DRAFT_CHAIN=0: split-K GEMMs in the half-SM config, RoPE /
+    residual kernels) both give a lossless decode, and the draft's own
+    forward matches the fp32 restatement either way."""
+    import torch
+    from oracle.model_ref import reference_forward
+    monkeypatch.setenv("SPECTRE_DRAFT_CHAIN", chain)
+    n = 8
+    pair = M.build_pair(M.SMALL_TARGET, M.SMALL_DRAFT, n_req=n, ctx_cap=256, seed=17)
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=64, prompt_len=16, alpha=0.8, seed=17)
+    ar = M.decode(pair, spec, "ar")
+    got = M.decode(pair, spec, "hybrid")
+    assert torch.equal(got.committed, ar.committed)
+    eng = M.SpectreEngine(pair, spec, "hybrid")
+    prompts = M.synthetic_prompts(n, 16, M.SMALL_TARGET.vocab, seed=17)
+    cs = 4
+    xs = []
+    for c0 in range(0, 16, cs):
+        tok = prompts[:, c0:c0 + cs].reshape(-1)
+        pos = torch.arange(c0, c0 + cs, device="cuda").repeat(n)
+        slot = torch.arange(n, device="cuda").repeat_interleave(cs)
+        q_off = torch.arange(n, device="cuda") * cs
+        _, x = eng.forward(1, tok, pos, slot, q_off, torch.full((n,), cs, device="cuda"),
+                           torch.full((n,), c0, device="cuda"), want_x=True)
+        xs.append(x.view(n, cs, -1))
+    xs = torch.cat(xs, 1)
+    for r in range(n):
+        x_ref, _ = reference_forward(pair.draft, prompts[r])
+        assert (xs[r].float() - x_ref).abs().mean().item() <= 3e-2 * x_ref.abs().mean().item()
+    eng.close()
+
+
 def test_device_graph_is_used(M):
     n = 4
     pair = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=n, ctx_cap=256, seed=2)
