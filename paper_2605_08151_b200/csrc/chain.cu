@@ -52,11 +52,11 @@ namespace spectre {
 constexpr int kChainThreads = 352;
 constexpr int kChainEpiThreads = 256;          // warps 2..9
 constexpr int kChainMaxPhases = 8;
-// One ring of stages, each holding kChainKS consecutive 64-wide k blocks of a
-// job's weights (128 rows: 16 KB per block) AND its activations (up to 128
-// tokens: 16 KB per block): both producers fill their half of a stage (one
-// full barrier, two arrivals + tx bytes) and ONE MMA commit releases it — the
-// tcgen05 commit is the MMA issuer's expensive step at T = 64.
+// One ring of stages, each holding kKS consecutive 64-wide k blocks of a job's
+// weights (128 rows: 16 KB per block) AND its activations (one pass of up to
+// kPass tokens: kPass * 128 B per block): both producers fill their half of a
+// stage (one full barrier, two arrivals + tx bytes) and ONE MMA commit
+// releases it — the tcgen05 commit is the MMA issuer's expensive step at T = 64.
 constexpr int kChainWBox = 128 * 128;           // one k block of weights
 constexpr int kChainStageOut = 2 * 16384;
 // kPass tokens per MMA pass: 128 (decode steps of <= 128 requests: two k
