@@ -724,7 +724,14 @@ __global__ void __launch_bounds__(kProtoThreads) k_accept(DecodeStateDev s, Batc
       c.has_probe_ref = 1;
       c.probe_round = c.round;
     } else if (mode == 'O') {
-      if (!c.has_tord) { c.tord = tr; c.has_tord = 1; } else { c.tord = ema_step(d, c.tord, tr); }
+      // no T_ord sample from the run's first round: at low L the round
+      // controller's r* = L (1 - T_par / T_ord) / (L - 1) turns a single
+      // noisy sample into a wrong mode for the whole run (config 4, gamma 4,
+      // alpha 0.1: hybrid 0.95 of ordinary), so it explores a second
+      // ordinary round and takes T_ord there, next to its parallel probe
+      if (c.round > 0) {
+        if (!c.has_tord) { c.tord = tr; c.has_tord = 1; } else { c.tord = ema_step(d, c.tord, tr); }
+      }
       if (!c.has_ema_ord) { c.ema_ord = r_hat; c.has_ema_ord = 1; }
       else { c.ema_ord = ema_step(d, c.ema_ord, r_hat); }
     }
