@@ -139,6 +139,11 @@ struct ModelRT {
                                     // 32-key boxes (warp-per-item attention)
   BatchDev bt{};
   std::vector<GemmPlan> pq, po, pgu, pd;
+  // large-T plans (T > 0 sampling only: batch invariance across T is not part
+  // of its contract): 128-row tiles as (tile, split, 256-token pass) units, fewer
+  // splits -> far less fp32 partial traffic at config 3's ~1,280 verify rows
+  std::vector<GemmPlan> pqL, poL, pdL;
+  static constexpr int kLargeT = 768, kSpLqkv = 2, kSpLo = 1, kSpLd = 2;
   GemmPlan plm{};
 
   int nqkv() const { return (dm.n_q_heads + 2 * dm.n_kv_heads) * dm.head_dim; }
@@ -237,6 +242,24 @@ struct ModelRT {
         TRY(gemm_set_outputs(p, part, nullptr, nullptr, nullptr, 0));
       TRY(gemm_set_outputs(&pgu[l], nullptr, nullptr, nullptr, act, F));
       for (GemmPlan* p : {&pq[l], &po[l], &pgu[l], &pd[l]}) p->args.t_dev = bt.t_dev;
+    }
+    if (sampling && !use_chain && !half_gemm && rows_cap >= kLargeT) {
+      pqL.resize(L);
+      poL.resize(L);
+      pdL.resize(L);
+      for (int l = 0; l < L; ++l) {
+        TRY(gemm_plan(&pqL[l], bf(w.wqkv) + (size_t)l * nqkv() * d, nqkv(), d, x, rows_cap,
+                      kPartial, kSpLqkv, 0, 0, 128));
+        TRY(gemm_plan(&poL[l], bf(w.wo) + (size_t)l * d * qd, d, qd, attn, rows_cap, kPartial,
+                      kSpLo, 0, 0, 128));
+        TRY(gemm_plan(&pdL[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial,
+                      kSpLd, 0, 0, 128));
+        for (GemmPlan* p : {&pqL[l], &poL[l], &pdL[l]}) {
+          TRY(gemm_set_pass_units(p, 256));
+          TRY(gemm_set_outputs(p, part, nullptr, nullptr, nullptr, 0));
+          p->args.t_dev = bt.t_dev;
+        }
+      }
     }
     if (sampling) {   // materialise fp32 logits (one split) for the samplers
       TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kPartial, 1, 0, 0, 256));
@@ -372,20 +395,23 @@ struct ModelRT {
     }
     if (!use_chain) TRY(launch_embed_rmsnorm(bt.tok, bt.t_dev, rows_cap, w.embed, w.attn_norm, h,
                                              x, d, eps, s));
+    const bool large = !pqL.empty() && n_req * new_per_req >= kLargeT;
+    const int s_qkv = large ? kSpLqkv : sp_qkv, s_o = large ? kSpLo : sp_o,
+              s_d = large ? kSpLd : sp_d;
     for (int l = 0; l < L && !use_chain; ++l) {
-      TRY(gemm_run(pq[l], s));
-      TRY(launch_qkv_rope_kv(part, sp_qkv, rows_cap, bt.t_dev, rows_cap, bt.pos, bt.slot,
+      TRY(gemm_run(large ? pqL[l] : pq[l], s));
+      TRY(launch_qkv_rope_kv(part, s_qkv, rows_cap, bt.t_dev, rows_cap, bt.pos, bt.slot,
                                rope, q, kc + l * kv_layer, vc + l * kv_layer, dm.n_q_heads,
                                dm.n_kv_heads, hd, ctx_cap, s));
       a.layer_row0 = l * n_req * dm.n_kv_heads * ctx_cap;
       TRY(launch_attention_w(tm_k32, tm_v32, a, hd, rows, s));
-      TRY(gemm_run(po[l], s));
-      TRY(launch_residual_rmsnorm(part, sp_o, rows_cap, bt.t_dev, rows_cap,
+      TRY(gemm_run(large ? poL[l] : po[l], s));
+      TRY(launch_residual_rmsnorm(part, s_o, rows_cap, bt.t_dev, rows_cap,
                                     w.mlp_norm + (size_t)l * d, h, x, d, eps, s));
       TRY(gemm_run(pgu[l], s));
-      TRY(gemm_run(pd[l], s));
+      TRY(gemm_run(large ? pdL[l] : pd[l], s));
       const float* next = (l + 1 < L) ? w.attn_norm + (size_t)(l + 1) * d : w.final_norm;
-      TRY(launch_residual_rmsnorm(part, sp_d, rows_cap, bt.t_dev, rows_cap, next, h, x, d, eps,
+      TRY(launch_residual_rmsnorm(part, s_d, rows_cap, bt.t_dev, rows_cap, next, h, x, d, eps,
                                     s));
     }
     if (!head) {

@@ -264,6 +264,15 @@ int gemm_run(const GemmPlan& p0, cudaStream_t s) {
   }
 }
 
+int gemm_set_pass_units(GemmPlan* p, int tokens) {
+  if (p->half || p->args.tile_rows != 128 || p->epi != kPartial || p->args.stream_k ||
+      tokens < 16 || tokens > 256 || tokens % 16)
+    return arg_fail("gemm_set_pass_units: 128-row partial plans, 16..256 tokens per pass");
+  p->args.pass_units = tokens;
+  p->grid = num_sms();
+  return SPECTRE_OK;
+}
+
 int gemm_set_half(GemmPlan* p) {
   if (p->args.tile_rows != 128 || p->epi == kArgmax || p->args.stream_k || p->bk != 64)
     return arg_fail("gemm_set_half: 128-row tiles, BK 64, partial / SwiGLU epilogue");

@@ -93,6 +93,8 @@ struct GemmArgs {
   int diag;                 // diagnostics (timing only): 1 skip MMAs, 2 skip epilogue math
   int ksub;                 // 1: one BK block per stage; 0: two when >= 2 such stages fit
   int ksub_max;             // most BK blocks per stage (0: 4)
+  int pass_units;           // > 0: one-box plans schedule (tile, split, token pass of this
+                            // many tokens) units over the CTAs (large T without split-K)
   int pair;                 // launched as CTA pairs (cluster 2): M=256 cta_group::2 MMAs
                             // whenever the tile is wide (T <= 256, 256-row tiles)
   unsigned long long* stall;   // diagnostics: per CTA {producer empty-wait, MMA full-wait,
@@ -125,7 +127,7 @@ struct GemmJob {
 
 // The static schedule, computed identically by the three warp roles.
 struct GemmSched {
-  int n_tiles, KI, G, c, T, tile_rows, splits, n_phases, pass;
+  int n_tiles, KI, G, c, T, tile_rows, splits, n_phases, pass, n_pu;
   bool sk, wide;
   int it, hi, unit, phase;
 
@@ -151,6 +153,14 @@ struct GemmSched {
     sk = a.stream_k && wide && !chunked;
     splits = sk ? 1 : a.splits;
     n_phases = wide ? (T + 255) / 256 : (tile_rows / 128) * ((T + pass - 1) / pass);
+    // token-pass units: (tile, split, pass) spread over the CTAs, pass fastest
+    // (CTAs sharing a weight tile run together: one HBM read, L2 for the rest)
+    n_pu = (!wide && a.pass_units > 0 && tile_rows == 128) ? (T + a.pass_units - 1) / a.pass_units
+                                                           : 0;
+    if (n_pu > 0) {
+      pass = a.pass_units;
+      n_phases = 1;
+    }
     const int total = n_tiles * KI;
     it = sk ? iter_lo(c, G, total) : 0;
     hi = sk ? iter_lo(c + 1, G, total) : 0;
@@ -171,6 +181,21 @@ struct GemmSched {
       j.nt = T;
       j.split = 0;
       j.role = j.k0 > 0 ? 2 : (j.k1 < KI ? 1 : 0);
+      return true;
+    }
+    if (n_pu > 0) {
+      if (unit >= n_tiles * splits * n_pu) return false;
+      const int r = unit / n_pu;
+      j.tile = r % n_tiles;
+      j.split = r / n_tiles;
+      j.k0 = (int)((long long)KI * j.split / splits);
+      j.k1 = (int)((long long)KI * (j.split + 1) / splits);
+      j.role = 0;
+      j.row_off = 0;
+      j.boxes = 1;
+      j.t0 = (unit % n_pu) * pass;
+      j.nt = min(pass, T - j.t0);
+      unit += G;
       return true;
     }
     if (unit >= n_tiles * splits) return false;
@@ -237,8 +262,10 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   const uint32_t crank = kPair ? cluster_rank() : 0u;
   const bool leader = crank == 0;
   const int x_half = ((Tc + 15) & ~15) / 2;        // tokens held by each CTA of a pair
+  const bool pu = !wide && a.pass_units > 0 && a.tile_rows == 128;   // token-pass units
   const int x_rows = pair ? ((x_half + 63) & ~63)
-                          : (wide ? ((T + 63) & ~63) : min((T + 63) & ~63, Cfg::kPass));
+                          : (wide ? ((T + 63) & ~63)
+                                  : min((T + 63) & ~63, pu ? a.pass_units : Cfg::kPass));
   // a stage holds `ksub` consecutive BK-wide k blocks (one expect-tx, one
   // MMA commit): fewer commit groups per byte when the MMAs are small (T=64)
   const int sub_bytes = w_bytes + x_rows * kRow;
@@ -259,7 +286,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
   stages = stages > kGemmMaxStages ? kGemmMaxStages : (stages < 1 ? 1 : stages);
   if (a.max_stages > 0 && stages > a.max_stages) stages = a.max_stages;
   // TMEM accumulator buffers: two whenever a job needs <= half the columns
-  const int t_pad_all = (Tc + 15) & ~15;
+  const int t_pad_all = ((pu ? min(Tc, a.pass_units) : Tc) + 15) & ~15;
   constexpr int kBufCols = Cfg::kTmemCols / 2;
   const int nbuf = ((wide && t_pad_all <= 128) || (!wide && t_pad_all <= kBufCols)) ? 2 : 1;
   const int half_stride = (wide && t_pad_all <= 128) ? 128 : 256;   // wide: 2nd accumulator

@@ -123,6 +123,23 @@ def test_parallel_head_token_is_rejection_sampled(M):
 
 
 
+def test_large_verify_batches_follow_target_distribution(M):
+    """160 requests: the verify passes carry >= 768 rows, so the target runs its
+    large-T plans (128-row tiles as (tile, split, 256-token pass) units with
+    fewer splits, engine.cu); still exact in distribution."""
+    from scipy import stats
+    n = 160
+    pair = M.build_pair(M.TINY_TARGET, M.TINY_DRAFT, n_req=n, ctx_cap=128, seed=9,
+                        target_branch=1.0, draft_branch=1.0)
+    spec = M.DecodeSpec(n_req=n, gamma=4, output_len=K_TOKENS + 8, prompt_len=12, seed=9,
+                        temperature=1.0)
+    res = M.decode(pair, spec, "hybrid")
+    assert (res.committed_pos == spec.output_len).all()
+    pit = _pit_values(M, pair, spec, res, np.random.default_rng(2))
+    p = stats.kstest(pit, "uniform").pvalue
+    assert p > KS_PVALUE, p
+
+
 @pytest.mark.parametrize("variant", ["ar", "parallel", "hybrid"])
 def test_committed_tokens_follow_target_distribution_128k_vocab(M, variant):
     """The PIT test at the headline vocabulary (V = 128,256): the sampler's
