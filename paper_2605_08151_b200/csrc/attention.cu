@@ -461,13 +461,17 @@ static int launch_attn_w_t(const CUtensorMap& tk, const CUtensorMap& tv, AttnArg
 int launch_attention_w(const CUtensorMap& tk32, const CUtensorMap& tv32, const AttnArgs& a,
                        int hd, int rows_per_req, cudaStream_t s) {
   if (a.chunk % 64 || a.chunk <= 0) return arg_fail("attention: chunk must be a multiple of 64");
-  static const int v = [] {
-    const char* e = getenv("SPECTRE_ATTN_WPAIR");   // warps per item (1 or 2)
-    return e ? atoi(e) : 2;
-  }();
   if (hd == 128) return launch_attn_w_t<128, 4, 3, 1>(tk32, tv32, a, rows_per_req, s);
   if (hd == 64) {
-    if (v == 1) return launch_attn_w_t<64, 8, 3, 1>(tk32, tv32, a, rows_per_req, s);
+    // two warps per item (even / odd stages) while the (request, kv head,
+    // key split) items of a decode step fit one wave of warp pairs (config 2:
+    // 512), else one warp per item (config 3's B=256: 2,048 items; 40.5 ->
+    // 35.1 us per launch).  Decided by the request count, not by this
+    // forward's row bound (a catch-up step's extra m-tiles are mostly empty),
+    // so one engine always uses one variant.
+    const long long items = (long long)a.n_req * a.n_kv * a.split_max;
+    if (2 * items > 8ll * num_sms())
+      return launch_attn_w_t<64, 8, 3, 1>(tk32, tv32, a, rows_per_req, s);
     return launch_attn_w_t<64, 8, 3, 2>(tk32, tv32, a, rows_per_req, s);
   }
   return arg_fail("attention: head_dim must be 64 or 128");
