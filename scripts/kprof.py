@@ -34,14 +34,19 @@ def main():
     ap.add_argument("--out", default="gpurun_out/kprof.json")
     ap.add_argument("--temperature", type=float, default=0.0)
     ap.add_argument("--out-len", type=int, default=1024)
+    ap.add_argument("--pair", default="c2", choices=("c2", "c5"),
+                    help="c2: Llama-3.1-8B / 3.2-1B shapes; c5: Qwen2.5-32B / 0.5B")
+    ap.add_argument("--gamma", type=int, default=4)
     args = ap.parse_args()
-    spec = M.DecodeSpec(n_req=args.n_req, gamma=4, output_len=args.out_len, prompt_len=128, seed=0,
-                        temperature=args.temperature)
-    pair = M.build_pair(M.LLAMA_31_8B, M.LLAMA_32_1B, n_req=args.n_req,
+    spec = M.DecodeSpec(n_req=args.n_req, gamma=args.gamma, output_len=args.out_len,
+                        prompt_len=128, seed=0, temperature=args.temperature)
+    tgt, drf = ((M.LLAMA_31_8B, M.LLAMA_32_1B) if args.pair == "c2" else
+                (M.QWEN_25_32B, M.QWEN_25_05B))
+    pair = M.build_pair(tgt, drf, n_req=args.n_req,
                         ctx_cap=spec.ctx_cap(), seed=0, target_branch=args.branch,
                         draft_branch=args.branch)
     eng = M.SpectreEngine(pair, spec, args.variant)
-    eng.prefill(M.synthetic_prompts(spec.n_req, spec.prompt_len, M.LLAMA_31_8B.vocab))
+    eng.prefill(M.synthetic_prompts(spec.n_req, spec.prompt_len, tgt.vocab))
     eng.run(max_rounds=args.warm_rounds, use_graph=False)
     torch.cuda.synchronize()
     from torch.profiler import profile, ProfilerActivity
