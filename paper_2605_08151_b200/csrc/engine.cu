@@ -221,19 +221,22 @@ struct ModelRT {
       TRY(gemm_plan(&po[l], bf(w.wo) + (size_t)l * d * qd, d, qd, attn, rows_cap, kPartial,
                     sp_o, 0, 0, tr_o));
       // SwiGLU needs full K per tile: 128-row tiles when they fit one wave
-      // (draft), else 256-row tiles (two accumulators share every X stage)
-      const bool gu128 = (2 * F) / 128 <= gemm_sk_grid();
-      TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
-                    1, 0, 0, gu128 ? 128 : 256));
-      TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
-                    0, 0, tr_d));
+      // (draft); 256-row tiles as CTA pairs when those fit one wave (8B: 112
+      // pair CTAs; two accumulators share every X stage); else 128-row tiles
+      // (32B: 432 tiles in 2.9 waves beat 216 256-row tiles in 1.5 waves:
+      // T=896 591 -> 461 us, T=128 131 -> 125 us; bit-identical per token)
       static const bool gu_pair = [] {   // CTA pairs (cta_group::2) for the 256-row SwiGLU
         const char* v = getenv("SPECTRE_GU_PAIR");   // tiles: half the token tile per CTA,
         return v ? atoi(v) != 0 : true;              // measured 68.7 -> 66.4 us (bit-identical)
       }();
-      if (gu_pair && !gu128 && !half_gemm &&
-          (2 * F / 256) % 2 == 0 && 2 * F / 256 <= gemm_sk_grid())
-        TRY(gemm_set_pair(&pgu[l]));
+      const bool pair_fits = gu_pair && !half_gemm && (2 * F / 256) % 2 == 0 &&
+                             2 * F / 256 <= gemm_sk_grid();
+      const bool gu128 = (2 * F) / 128 <= gemm_sk_grid() || !pair_fits;
+      TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
+                    1, 0, 0, gu128 ? 128 : 256));
+      TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
+                    0, 0, tr_d));
+      if (pair_fits && !gu128) TRY(gemm_set_pair(&pgu[l]));
       if (half_gemm) {
         // partial GEMMs only: the SwiGLU GEMM measured faster in the full config
         for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) TRY(gemm_set_half(p));
