@@ -265,7 +265,10 @@ struct ModelRT {
       }
     }
     if (sampling) {   // materialise fp32 logits (one split) for the samplers
-      TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kPartial, 1, 0, 0, 256));
+      // large verify batches (config 3: ~1,280 rows): 128-row tiles balance
+      // better (1,490 -> 1,351 us at T = 1,280)
+      TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kPartial, 1, 0, 0,
+                    !pqL.empty() ? 128 : 256));
       TRY(gemm_set_outputs(&plm, logits, nullptr, nullptr, nullptr, 0));
     } else {
       // whole 256-row tiles per CTA (no stream-K): logits independent of the
