@@ -124,8 +124,28 @@ __device__ RowAcc row_pass(const float* __restrict__ l, int V, float inv_t, uint
   a.init();
   const int V4 = V >> 2;
   const float4* l4 = reinterpret_cast<const float4*>(l);
-#pragma unroll 4
-  for (int v = threadIdx.x; v < V4; v += kSampThreads) {
+  // kB float4 loads of a thread in flight before any of them is consumed
+  // (the per-element work would otherwise serialise one L2 / HBM round trip
+  // per few loads); element order per thread is unchanged
+  constexpr int kB = 8;
+  int v = threadIdx.x;
+  for (; v + (kB - 1) * kSampThreads < V4; v += kB * kSampThreads) {
+    float4 q[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) q[u] = __ldg(l4 + v + u * kSampThreads);
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int vv = v + u * kSampThreads;
+      if (kCopy) reinterpret_cast<float4*>(dst)[vv] = q[u];
+      const float x[4] = {q[u].x * inv_t, q[u].y * inv_t, q[u].z * inv_t, q[u].w * inv_t};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        a.add_stat(x[e]);
+        if (kDraw) a.add_draw(x[e] + gumbel(key, 4 * vv + e), 4 * vv + e);
+      }
+    }
+  }
+  for (; v < V4; v += kSampThreads) {
     const float4 q = __ldg(l4 + v);
     if (kCopy) reinterpret_cast<float4*>(dst)[v] = q;
     const float x[4] = {q.x * inv_t, q.y * inv_t, q.z * inv_t, q.w * inv_t};
