@@ -120,6 +120,7 @@ struct ModelRT {
   }
   int n_req = 0, rows_cap = 0, ctx_cap = 0, max_new = 1, split_max = 1, rb_cap = 1;
   int sp_qkv = 1, sp_o = 1, sp_d = 1;
+  bool down_pu = false;   // down projection as (tile, split, token pass) units (layout())
   int tr_qkv = 256, tr_o = 256, tr_d = 256;   // weight rows per tile, per GEMM
   int tile_rows = 256;   // weight rows per GEMM CTA (128 for small-T models)
   bool half_gemm = false; // decode GEMMs in the half-SM config (2 CTAs per SM, 128-row tiles)
@@ -167,6 +168,17 @@ struct ModelRT {
     sp_qkv = pick_splits((nqkv() + tr_qkv - 1) / tr_qkv, d / 64, ctas);
     sp_o = pick_splits((d + tr_o - 1) / tr_o, qd / 64, ctas);
     sp_d = pick_splits((d + tr_d - 1) / tr_d, dm.ffn / 64, ctas);
+    // large verify batches (rows_cap >= kLargeT: config 5's 128 x 7 rows): the
+    // down projection as 128-row (tile, split, 256-token pass) units, ~4
+    // waves of them -- one plan for every T of this engine, so still batch
+    // invariant.  Qwen2.5-32B at T=896: 328 -> 297 us, 7 -> 4 splits of partials
+    down_pu = !half_gemm && !use_chain && rows_cap >= kLargeT;
+    if (down_pu) {
+      tr_d = 128;
+      const int units = ((d + 127) / 128) * ((rows_cap + 255) / 256);
+      sp_d = std::max(1, std::min(12, (4 * ctas + units / 2) / units));
+      while (sp_d > 1 && dm.ffn / 64 / sp_d < 3) --sp_d;
+    }
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
     if (use_chain)
       part_n = std::max({part_n, (size_t)chain_splits(nqkv(), d) * nqkv(),
@@ -237,6 +249,7 @@ struct ModelRT {
       TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
                     0, 0, tr_d));
       if (pair_fits && !gu128) TRY(gemm_set_pair(&pgu[l]));
+      if (down_pu) TRY(gemm_set_pass_units(&pd[l], 256));
       if (half_gemm) {
         // partial GEMMs only: the SwiGLU GEMM measured faster in the full config
         for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) TRY(gemm_set_half(p));

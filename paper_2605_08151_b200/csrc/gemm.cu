@@ -312,11 +312,17 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
                                  float* amax_val, int32_t* amax_idx, void* act, int32_t ld_act,
                                  int32_t max_stages, void* stream) {
   GemmPlan p;
-  // test knobs: max_stages < 0 forces 32-wide K blocks; >= 4000 CTA pairs; >= 3000 the
+  // test knobs: max_stages < 0 forces 32-wide K blocks; >= 7000 (+1000: 128-row tiles)
+  // token-pass units; >= 4000 CTA pairs; >= 3000 the
   // half-SM config; >= 2000 disables stream-K; >= 1000 selects 128-row tiles
   bool sk = true;
   bool half = false;
   bool pair = false;
+  bool punits = false;
+  if (max_stages >= 7000) {   // 128-row partial plans as (tile, split, 256-token pass) units
+    punits = true;
+    max_stages -= 7000;
+  }
   if (max_stages >= 4000) {   // CTA-pair launch (256-row tiles, no stream-K)
     pair = true;
     sk = false;
@@ -347,6 +353,8 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
     if (int e = gemm_set_half(&p)) return e;
   if (pair)
     if (int e = gemm_set_pair(&p)) return e;
+  if (punits)
+    if (int e = gemm_set_pass_units(&p, 256)) return e;
   if (int e = gemm_set_outputs(&p, partial, amax_val, amax_idx, act, ld_act)) return e;
   if (const char* dg = getenv("SPECTRE_GEMM_DIAG")) p.args.diag = atoi(dg);
   static unsigned long long* stall = nullptr;
