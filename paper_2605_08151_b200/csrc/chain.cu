@@ -19,7 +19,8 @@
 // One CTA per SM (grid = SMs, all co-resident), 11 warps:
 //   warp 0  weight producer (TMA, evict-first), runs across phase boundaries
 //   warp 1  TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-9  epilogue (tcgen05.ld -> split-K partial / SwiGLU stores) and
+//   warps 2-9  epilogue (tcgen05.ld -> split-K partial / SwiGLU stores straight
+//           from registers: each warp instruction writes whole 32-128 B runs) and
 //           the glue phases (residual + RMSNorm, RoPE, embedding) in between
 //   warp 10 activation producer (TMA), waits on the phase barriers
 // Phase barrier: one monotonic arrival counter per chain launch (each CTA
@@ -58,19 +59,21 @@ constexpr int kChainMaxPhases = 8;
 // stage (one full barrier, two arrivals + tx bytes) and ONE MMA commit
 // releases it — the tcgen05 commit is the MMA issuer's expensive step at T = 64.
 constexpr int kChainWBox = 128 * 128;           // one k block of weights
-constexpr int kChainStageOut = 2 * 16384;
-// kPass tokens per MMA pass: 128 (decode steps of <= 128 requests: two k
-// blocks per stage, three stages) or 256 (larger batches, e.g. config 3's
-// B = 256: one N = 256 MMA chain per job instead of two passes that stream
-// every weight tile twice; one k block per stage, four stages).  Both keep
-// 96 / 64 KB of weights and 192 KB of ring in flight per SM.
-template <int kPass>
+// kPass tokens per MMA pass: 64 (decode steps of <= 64 requests: two k blocks
+// per stage, four stages: 128 KB of weights in flight, the activation half
+// sized to the 64-token box), 128 (<= 128 tokens, e.g. the catch-up step
+// after a fully accepted round: two k blocks per stage, three stages) or 256
+// (larger batches, e.g. config 3's B = 256: one N = 256 MMA chain per job
+// instead of two passes that stream every weight tile twice; one k block per
+// stage, four stages).  They keep 128 / 96 / 64 KB of weights and 192 KB of
+// ring in flight per SM.
+template <int kPass, int kKS_ = (kPass <= 128 ? 2 : 1), int kStages_ = (kPass == 128 ? 3 : 4)>
 struct ChainCfg {
-  static constexpr int kKS = kPass == 128 ? 2 : 1;
-  static constexpr int kStages = kPass == 128 ? 3 : 4;
+  static constexpr int kKS = kKS_;
+  static constexpr int kStages = kStages_;
   static constexpr int kXBlk = kPass * 128;     // one k block of activations
   static constexpr int kStageBytes = kKS * (kChainWBox + kXBlk);
-  static constexpr int kSmem = 1024 + kStages * kStageBytes + kChainStageOut + 1024;
+  static constexpr int kSmem = 1024 + kStages * kStageBytes + 1024;
   static constexpr int kTmemCols = 2 * kPass;   // two accumulator buffers
   static_assert(kSmem <= 232448, "chain smem");
 };
@@ -78,6 +81,7 @@ struct ChainCfg {
 struct ChainGemm {
   int N, K, splits, tiles, kb;   // kb: K / 64
   int epi;                       // kPhGemmPartial / kPhGemmSwiGLU
+  void* out;                     // partials [splits][rows_cap][N] f32 / act [rows_cap][N/2] bf16
 };
 
 struct ChainArgs {
@@ -332,17 +336,15 @@ __device__ void chain_rope(const ChainArgs& a, int T, int et) {
   }
 }
 
-template <int kPass>
+template <int kPass, int kKS, int kStages>
 __global__ void __launch_bounds__(kChainThreads, 1)
 k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtensorMap tw1,
         const __grid_constant__ CUtensorMap tw2, const __grid_constant__ CUtensorMap tw3,
         const __grid_constant__ CUtensorMap tx0, const __grid_constant__ CUtensorMap tx1,
         const __grid_constant__ CUtensorMap tx2, const __grid_constant__ CUtensorMap tx3,
-        const __grid_constant__ CUtensorMap to0, const __grid_constant__ CUtensorMap to1,
-        const __grid_constant__ CUtensorMap to2, const __grid_constant__ CUtensorMap to3,
         ChainArgs a) {
   using namespace ptx;
-  using Cfg = ChainCfg<kPass>;
+  using Cfg = ChainCfg<kPass, kKS, kStages>;
   constexpr int kChainKS = Cfg::kKS;
   constexpr int kChainStages = Cfg::kStages;
   constexpr int kChainXBlk = Cfg::kXBlk;
@@ -351,8 +353,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   uint8_t* ring = smem;   // stage s: [KS weight blocks][KS activation blocks]
-  uint8_t* stage_out = ring + kChainStages * kChainStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + kChainStageOut);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kChainStages * kChainStageBytes);
   uint64_t* empty = full + kChainStages;
   uint64_t* tmem_full = empty + kChainStages;       // [2]
   uint64_t* tmem_empty = tmem_full + 2;            // [2]
@@ -361,7 +362,6 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
 
   const CUtensorMap* tw[4] = {&tw0, &tw1, &tw2, &tw3};
   const CUtensorMap* tx[4] = {&tx0, &tx1, &tx2, &tx3};
-  const CUtensorMap* to[4] = {&to0, &to1, &to2, &to3};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, c = blockIdx.x;
   auto row_count = [&]() {
@@ -532,7 +532,7 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
     const int et = threadIdx.x - 64;           // 0..255
     const int q = warp & 3;                    // TMEM lane quarter
     const int grp = (warp - 2) >> 2;           // 0 / 1: alternating 32-token chunks
-    int jn = 0, wbuf = 0;
+    int jn = 0;
     for (int p = 0; p < a.n_phase; ++p) {
       const int kind = a.kind[p];
       if (p > 0) {   // inputs of this phase: every CTA finished phase p - 1
@@ -540,7 +540,6 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
         asm volatile("bar.sync 1, %0;" ::"n"(kChainEpiThreads) : "memory");
         if (stamp) a.dbg[1 + 2 * p] = gtimer_ns();       // phase p may start
       }
-      bool stored = false;
       if (T > 0 && (kind == kPhGemmPartial || kind == kPhGemmSwiGLU)) {
         const int gi = a.gemm[p];
         const ChainGemm& g = a.g[gi];
@@ -563,31 +562,22 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
             for (int jj = 0; jj < 32; ++jj) v[jj] = __uint_as_float(r[jj]);
             const int nvalid = min(32, j.nt - cc);
             if (kind == kPhGemmPartial) {
-              // [split][t][n] partials: each warp stages and stores its 32 rows
+              // [split][t][n] partials straight from registers: for each token
+              // the warp's 32 lanes write 128 consecutive bytes
+              float* dst = static_cast<float*>(g.out) +
+                           (size_t)(j.split * a.rows_cap + j.t0 + cc) * g.N + j.tile * 128 +
+                           q * 32 + lane;
 #pragma unroll
-              for (int hh = 0; hh < 2; ++hh) {
-                if (hh * 16 >= nvalid) break;
-                float* wst = reinterpret_cast<float*>(stage_out + grp * 16384 + q * 4096 +
-                                                      wbuf * 2048);
-                wbuf ^= 1;
-                if (lane == 0) bulk_wait_read<1>();
-                __syncwarp();
-#pragma unroll
-                for (int jj = 0; jj < 16; ++jj) wst[jj * 32 + lane] = v[hh * 16 + jj];
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                  tma_store_2d(to[gi], wst, j.tile * 128 + q * 32,
-                               j.split * a.rows_cap + j.t0 + cc + 16 * hh);
-                  bulk_commit();
-                }
-              }
-              stored = true;
+              for (int jj = 0; jj < 32; ++jj)
+                if (jj < nvalid) dst[(size_t)jj * g.N] = v[jj];
             } else {
-              // SwiGLU: rows interleaved [gate_i, up_i]; even lanes finish
-              // tokens 0..15 of the chunk, odd lanes 16..31
+              // SwiGLU straight from registers: even lanes tokens 0..15 of the
+              // chunk, odd lanes 16..31; lane pairs share feature lane / 2
               const bool odd = lane & 1;
-              float out[16];
+              const int n2 = g.N >> 1;
+              __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.out) +
+                                   (size_t)(j.t0 + cc + (odd ? 16 : 0)) * n2 +
+                                   ((j.tile * 128 + q * 32) >> 1) + (lane >> 1);
 #pragma unroll
               for (int jj = 0; jj < 16; ++jj) {
                 const float send = odd ? v[jj] : v[jj + 16];
@@ -596,33 +586,13 @@ k_chain(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtenso
                 const float up = odd ? v[jj + 16] : recv;
                 float th;
                 asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(0.5f * gt));
-                out[jj] = gt * fmaf(0.5f, th, 0.5f) * up;
+                if ((odd ? 16 : 0) + jj < nvalid)
+                  dst[(size_t)jj * n2] = __float2bfloat16_rn(gt * fmaf(0.5f, th, 0.5f) * up);
               }
-              // per-warp [32 tokens][16 features] box (its 16 row pairs)
-              __nv_bfloat16* wst = reinterpret_cast<__nv_bfloat16*>(stage_out + grp * 16384 +
-                                                                      q * 4096 + wbuf * 2048);
-              wbuf ^= 1;
-              if (lane == 0) bulk_wait_read<1>();
-              __syncwarp();
-              const int fi = lane >> 1;
-#pragma unroll
-              for (int jj = 0; jj < 16; ++jj)
-                wst[((odd ? 16 : 0) + jj) * 16 + fi] = __float2bfloat16_rn(out[jj]);
-              fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                tma_store_2d(to[gi], wst, (j.tile * 128 + q * 32) >> 1, j.t0 + cc);
-                bulk_commit();
-              }
-              stored = true;
             }
           }
           tc_fence_before();
           mbar_arrive(&tmem_empty[buf]);
-        }
-        if (stored && lane == 0) {
-          bulk_wait_all();   // this phase's outputs are in global memory ...
-          asm volatile("fence.proxy.async.global;" ::: "memory");   // ... and visible
         }
         if (stamp) a.dbg[17 + 2 * p] = gtimer_ns();
       } else if (T > 0 && (kind == kPhResid || kind == kPhEmbed)) {
@@ -680,20 +650,19 @@ int chain_splits(int N, int K) {
   return s;
 }
 
-template <int kPass>
+template <int kPass, int kKS = ChainCfg<kPass>::kKS, int kStages = ChainCfg<kPass>::kStages>
 static int chain_launch_t(const ChainPlan& cp, cudaStream_t s) {
+  using Cfg = ChainCfg<kPass, kKS, kStages>;
   static bool cfg = false;
   if (!cfg) {
-    SPECTRE_CUDA_TRY(cudaFuncSetAttribute(k_chain<kPass>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          ChainCfg<kPass>::kSmem));
+    SPECTRE_CUDA_TRY(cudaFuncSetAttribute(k_chain<kPass, kKS, kStages>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
     cfg = true;
   }
   const GemmPlan* g = cp.gp;
-  SPECTRE_LAUNCH_PDL("k_chain", k_chain<kPass>, dim3(chain_sms()), dim3(kChainThreads),
-                     ChainCfg<kPass>::kSmem, s, g[0].tmap_w, g[1].tmap_w, g[2].tmap_w,
-                     g[3].tmap_w, g[0].tmap_x, g[1].tmap_x, g[2].tmap_x, g[3].tmap_x,
-                     g[0].tmap_out, g[1].tmap_out, g[2].tmap_out, g[3].tmap_out, cp.args);
+  SPECTRE_LAUNCH_PDL("k_chain", (k_chain<kPass, kKS, kStages>), dim3(chain_sms()),
+                     dim3(kChainThreads), Cfg::kSmem, s, g[0].tmap_w, g[1].tmap_w, g[2].tmap_w,
+                     g[3].tmap_w, g[0].tmap_x, g[1].tmap_x, g[2].tmap_x, g[3].tmap_x, cp.args);
   return SPECTRE_OK;
 }
 
@@ -703,7 +672,12 @@ int chain_launch(const void* plan_v, cudaStream_t s, int t_bound) {
     const char* v = getenv("SPECTRE_CHAIN_PASS");
     return v ? atoi(v) != 128 : 1;
   }();
+  static const int pass64 = [] {   // SPECTRE_CHAIN_PASS64=0: never the 64-token passes
+    const char* v = getenv("SPECTRE_CHAIN_PASS64");
+    return v ? atoi(v) != 0 : 1;
+  }();
   if (pass256 && t_bound > 128) return chain_launch_t<256>(cp, s);
+  if (pass64 && t_bound <= 64) return chain_launch_t<64>(cp, s);
   return chain_launch_t<128>(cp, s);
 }
 
@@ -729,6 +703,7 @@ int chain_add_gemm(void* plan_v, const void* W, int N, int K, const void* X, int
   ChainGemm& g = a.g[gi];
   g.N = N;
   g.K = K;
+  g.out = epi == kPhGemmSwiGLU ? act : static_cast<void*>(part);
   g.splits = splits;
   g.tiles = N / 128;
   g.kb = K / 64;
