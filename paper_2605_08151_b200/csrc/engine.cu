@@ -144,7 +144,10 @@ struct ModelRT {
   // of its contract): 128-row tiles as (tile, split, 256-token pass) units, fewer
   // splits -> far less fp32 partial traffic at config 3's ~1,280 verify rows
   std::vector<GemmPlan> pqL, poL, pdL;
-  static constexpr int kLargeT = 768, kSpLqkv = 2, kSpLo = 1, kSpLd = 2;
+  // large-T plans' split counts (config 3, T = 1,280, target ms per round:
+  // down 2 / 3 / 4 / 5 splits 18.78 / 18.46-18.57 / 18.70 / 19.21; o 1 best,
+  // q/k/v 2 and 3 even)
+  static constexpr int kLargeT = 768, kSpLqkv = 2, kSpLo = 1, kSpLd = 3;
   GemmPlan plm{};
 
   int nqkv() const { return (dm.n_q_heads + 2 * dm.n_kv_heads) * dm.head_dim; }
@@ -180,6 +183,8 @@ struct ModelRT {
       while (sp_d > 1 && dm.ffn / 64 / sp_d < 3) --sp_d;
     }
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
+    if (down_pu)   // the large-T plans (sampling engines) share the buffer
+      part_n = std::max({part_n, (size_t)kSpLqkv * nqkv(), (size_t)kSpLo * d, (size_t)kSpLd * d});
     if (use_chain)
       part_n = std::max({part_n, (size_t)chain_splits(nqkv(), d) * nqkv(),
                          (size_t)chain_splits(d, qd) * d, (size_t)chain_splits(d, dm.ffn) * d});
