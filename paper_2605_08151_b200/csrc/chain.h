@@ -42,7 +42,8 @@ int chain_add_gemm(void* plan, const void* W, int N, int K, const void* X, int r
 // Glue phase: kPhEmbed / kPhResid (RMSNorm weight norm_w) / kPhRope.
 int chain_add_glue(void* plan, int kind, const float* norm_w);
 int chain_splits(int N, int K);
-// t_bound: upper bound of the forward's token rows (selects 128- or 256-token MMA passes)
+// t_bound: the forward's token rows, an upper bound or the typical count (selects
+// 64-, 128- or 256-token MMA passes; more rows than the pass run as several passes)
 int chain_launch(const void* plan, cudaStream_t s, int t_bound);
 
 }  // namespace spectre

@@ -379,8 +379,12 @@ struct ModelRT {
   // verify / prefill); the draft's decode steps sample per request instead.
   // head = false: stop after the last layer's residual (prefill chunks whose
   // next-token prediction nobody reads)
+  // t_typical (> 0): the rows the step usually carries, when far below the
+  // bound (the draft's first step of a round: 1-2 catch-up tokens per request,
+  // bounded by the longest possible catch-up); picks the chains' MMA pass width
+  // (a pass narrower than T stays correct, it streams the weights once per pass)
   int forward(int new_per_req, cudaStream_t s, void* out_x = nullptr, bool sample_rows = true,
-              bool head = true) {
+              bool head = true, int t_typical = 0) {
     const int d = dm.d_model, L = dm.n_layers, hd = dm.head_dim;
     const float eps = dm.rms_eps;
     const int rows = new_per_req * group();
@@ -412,7 +416,8 @@ struct ModelRT {
     auto* kc = reinterpret_cast<__nv_bfloat16*>(w.k_cache);
     auto* vc = reinterpret_cast<__nv_bfloat16*>(w.v_cache);
     if (use_chain) {
-      const int t_bound = std::min(rows_cap, n_req * new_per_req);
+      int t_bound = std::min(rows_cap, n_req * new_per_req);
+      if (t_typical > 0) t_bound = std::min(t_bound, t_typical);
       TRY(chain_launch(ch_first, s, t_bound));
       for (int l = 0; l < L; ++l) {
         a.layer_row0 = l * n_req * dm.n_kv_heads * ctx_cap;
@@ -655,7 +660,8 @@ struct Engine {
     TRY(launch_draft_prep(st, drf.bt, which, s));
     const int steps = which == 'O' ? cfg.gamma - 1 : cfg.gamma;   // 'M': the longest query
     for (int i = 0; i < steps; ++i) {
-      TRY(drf.forward(i == 0 ? draft_new_max : 1, s, nullptr, false));
+      TRY(drf.forward(i == 0 ? draft_new_max : 1, s, nullptr, false, true,
+                      i == 0 ? 2 * drf.n_req : 0));
       if (st.sampling)
         TRY(launch_draft_sample(st, drf.bt, drf.logits, drf.dm.vocab, drf.inv_t, qstore, qstat,
                                 qwin, s));

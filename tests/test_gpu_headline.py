@@ -150,17 +150,21 @@ def test_headline_width_layers_vs_fp32_reference(M, pair_name):
     _free()
 
 
-def test_draft_chain_wide_pass_vs_fp32_reference(M):
-    """The draft's persistent chains over more than 128 token rows (config 3's
-    B=256 decode steps, prefill chunks): 256-token MMA passes (N = 256 per job)
-    at the 1B widths, two layers, against the fp32 restatement."""
+@pytest.mark.parametrize("per", [1, 2, 4])
+def test_draft_chain_passes_vs_fp32_reference(M, per):
+    """The draft's persistent chains at every MMA pass width, at the 1B widths,
+    two layers, against the fp32 restatement: 48 rows per forward (64-token
+    passes, C2's decode steps), 96 (128-token passes, the catch-up step after
+    a fully accepted round) and 192 (256-token passes: config 3's B=256 decode
+    steps, prefill chunks).  Draft numerics never change the committed stream
+    (the target verifies), so only this comparison catches a broken pass."""
     n, P = 48, 12
     pair = M.build_pair(_shallow(M.LLAMA_31_8B), _shallow(M.LLAMA_32_1B), n_req=n, ctx_cap=128,
                         seed=41, target_branch=1.0, draft_branch=1.0)
     spec = M.DecodeSpec(n_req=n, gamma=4, output_len=32, prompt_len=P, seed=41)
     eng = M.SpectreEngine(pair, spec, "hybrid")
     prompts = M.synthetic_prompts(n, P, M.LLAMA_31_8B.vocab, seed=41)
-    toks, xs = _verify_shaped_forward(eng, 1, prompts, 4)   # 192 rows per forward
+    toks, xs = _verify_shaped_forward(eng, 1, prompts, per)   # 48 * per rows per forward
     _check_vs_reference(pair.draft, prompts, toks, xs)
     eng.close()
     del eng, pair
