@@ -120,7 +120,7 @@ struct ModelRT {
   }
   int n_req = 0, rows_cap = 0, ctx_cap = 0, max_new = 1, split_max = 1, rb_cap = 1;
   int sp_qkv = 1, sp_o = 1, sp_d = 1;
-  bool down_pu = false;   // down projection as (tile, split, token pass) units (layout())
+  bool down_pu = false;   // split-K GEMMs as (tile, split, token pass) units (layout())
   int tr_qkv = 256, tr_o = 256, tr_d = 256;   // weight rows per tile, per GEMM
   int tile_rows = 256;   // weight rows per GEMM CTA (128 for small-T models)
   bool half_gemm = false; // decode GEMMs in the half-SM config (2 CTAs per SM, 128-row tiles)
@@ -172,15 +172,25 @@ struct ModelRT {
     sp_o = pick_splits((d + tr_o - 1) / tr_o, qd / 64, ctas);
     sp_d = pick_splits((d + tr_d - 1) / tr_d, dm.ffn / 64, ctas);
     // large verify batches (rows_cap >= kLargeT: config 5's 128 x 7 rows): the
-    // down projection as 128-row (tile, split, 256-token pass) units, ~4
-    // waves of them -- one plan for every T of this engine, so still batch
-    // invariant.  Qwen2.5-32B at T=896: 328 -> 297 us, 7 -> 4 splits of partials
+    // split-K GEMMs as 128-row (tile, split, 256-token pass) units over every
+    // SM -- one plan for every T of this engine, so still batch invariant.
+    // Splits for about `waves` waves of units (measured at Qwen2.5-32B, T=896):
+    // down 4 waves (328 -> 297 us, 7 -> 4 splits of partials), q/k/v 4 waves
+    // (3 splits: 83.4 -> 70.5 us), o 2 waves (2 splits: 60.0 -> 51.1 us;
+    // 3 / 4 splits 54.7 / 57.5): target 61.8 -> 60.0 ms per round.
     down_pu = !half_gemm && !use_chain && rows_cap >= kLargeT;
     if (down_pu) {
-      tr_d = 128;
-      const int units = ((d + 127) / 128) * ((rows_cap + 255) / 256);
-      sp_d = std::max(1, std::min(12, (4 * ctas + units / 2) / units));
-      while (sp_d > 1 && dm.ffn / 64 / sp_d < 3) --sp_d;
+      const int passes = (rows_cap + 255) / 256;
+      auto pu_splits = [&](int n, int k, int waves) {
+        const int units = ((n + 127) / 128) * passes;
+        int sp = std::max(1, std::min(12, (waves * ctas + units / 2) / units));
+        while (sp > 1 && k / 64 / sp < 3) --sp;
+        return sp;
+      };
+      tr_qkv = tr_o = tr_d = 128;
+      sp_qkv = pu_splits(nqkv(), d, 4);
+      sp_o = pu_splits(d, qd, 2);
+      sp_d = pu_splits(d, dm.ffn, 4);
     }
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
     if (down_pu)   // the large-T plans (sampling engines) share the buffer
@@ -254,7 +264,8 @@ struct ModelRT {
       TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
                     0, 0, tr_d));
       if (pair_fits && !gu128) TRY(gemm_set_pair(&pgu[l]));
-      if (down_pu) TRY(gemm_set_pass_units(&pd[l], 256));
+      if (down_pu)
+        for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) TRY(gemm_set_pass_units(p, 256));
       if (half_gemm) {
         // partial GEMMs only: the SwiGLU GEMM measured faster in the full config
         for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) TRY(gemm_set_half(p));
