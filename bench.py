@@ -463,8 +463,10 @@ def roofline_gate_up(pair, args):
     n_layers = pair.target.spec.n_layers
 
     # the engine's launch shape: CTA pairs (cta_group::2) unless SPECTRE_GU_PAIR=0,
-    # one 256-row tile per CTA (no stream-K)
-    flags = 4000 if os.environ.get("SPECTRE_GU_PAIR", "1") != "0" else 2000
+    # one 256-row tile per CTA (no stream-K); engines with >= 768 verify rows
+    # (config 3) schedule the pairs over (tile pair, 256-token chunk) units
+    large = args.batch * (args.gamma + 1) >= 768
+    flags = (9000 if large else 4000) if os.environ.get("SPECTRE_GU_PAIR", "1") != "0" else 2000
 
     def launch(layer):
         _native.check(L.spectre_gemm_bf16(X.data_ptr(), pair.target.wgu[layer].data_ptr(), None, T,

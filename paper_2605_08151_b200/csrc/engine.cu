@@ -256,14 +256,21 @@ struct ModelRT {
         const char* v = getenv("SPECTRE_GU_PAIR");   // tiles: half the token tile per CTA,
         return v ? atoi(v) != 0 : true;              // measured 68.7 -> 66.4 us (bit-identical)
       }();
+      // large verify batches (rows_cap >= kLargeT): CTA pairs over (tile pair,
+      // 256-token chunk) units on every SM, neighbouring pairs on the same
+      // tiles (isolated, L2 flushed: 8B T=1280 279.5 -> 207.9 us, 32B T=896
+      // 457.8 (128-row tiles) -> 398.3 us; T=320 109.6 -> 113.6, so not below)
+      const bool pair_units = gu_pair && !half_gemm && (2 * F / 256) % 2 == 0 &&
+                              rows_cap >= kLargeT;
       const bool pair_fits = gu_pair && !half_gemm && (2 * F / 256) % 2 == 0 &&
                              2 * F / 256 <= gemm_sk_grid();
-      const bool gu128 = (2 * F) / 128 <= gemm_sk_grid() || !pair_fits;
+      const bool gu128 = !pair_units && ((2 * F) / 128 <= gemm_sk_grid() || !pair_fits);
       TRY(gemm_plan(&pgu[l], bf(w.wgu) + (size_t)l * 2 * F * d, 2 * F, d, x, rows_cap, kSwiGLU,
                     1, 0, 0, gu128 ? 128 : 256));
       TRY(gemm_plan(&pd[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial, sp_d,
                     0, 0, tr_d));
-      if (pair_fits && !gu128) TRY(gemm_set_pair(&pgu[l]));
+      if (pair_units) TRY(gemm_set_pair_units(&pgu[l]));
+      else if (pair_fits && !gu128) TRY(gemm_set_pair(&pgu[l]));
       if (down_pu)
         for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) TRY(gemm_set_pass_units(p, 256));
       if (half_gemm) {

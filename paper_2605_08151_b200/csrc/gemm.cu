@@ -160,6 +160,19 @@ int gemm_set_pair(GemmPlan* p) {
   return SPECTRE_OK;
 }
 
+// CTA-pair SwiGLU plan scheduled as (tile pair, 256-token chunk) units over
+// every SM (an even grid): for large verify batches and for 256-row tile
+// counts above one wave of CTAs.
+int gemm_set_pair_units(GemmPlan* p) {
+  if (p->half || p->bk != 64 || p->epi != kSwiGLU || p->args.tile_rows != 256 ||
+      p->args.splits != 1 || p->args.stream_k || p->n_tiles % 2)
+    return arg_fail("gemm_set_pair_units: 256-row SwiGLU tiles, an even count, BK 64");
+  p->grid = num_sms() & ~1;
+  p->args.pair = 1;
+  p->args.pair_units = 1;
+  return SPECTRE_OK;
+}
+
 int gemm_default_bk() {
   static const int bk = [] {
     const char* v = getenv("SPECTRE_GEMM_BK");
@@ -313,12 +326,16 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
                                  int32_t max_stages, void* stream) {
   GemmPlan p;
   // test knobs: max_stages < 0 forces 32-wide K blocks; >= 7000 (+1000: 128-row tiles)
-  // token-pass units; >= 4000 CTA pairs; >= 3000 the
+  // token-pass units; >= 9000 CTA pairs over (tile pair, chunk) units; >= 4000 CTA pairs; >= 3000 the
   // half-SM config; >= 2000 disables stream-K; >= 1000 selects 128-row tiles
   bool sk = true;
   bool half = false;
   bool pair = false;
-  bool punits = false;
+  bool punits = false, pair_units = false;
+  if (max_stages >= 9000) {   // CTA pairs as (tile pair, 256-token chunk) units
+    pair_units = true;
+    max_stages -= 5000;
+  }
   if (max_stages >= 7000) {   // 128-row partial plans as (tile, split, 256-token pass) units
     punits = true;
     max_stages -= 7000;
@@ -352,7 +369,7 @@ extern "C" int spectre_gemm_bf16(const void* X, const void* W, const int32_t* t_
   if (half)
     if (int e = gemm_set_half(&p)) return e;
   if (pair)
-    if (int e = gemm_set_pair(&p)) return e;
+    if (int e = pair_units ? gemm_set_pair_units(&p) : gemm_set_pair(&p)) return e;
   if (punits)
     if (int e = gemm_set_pass_units(&p, 256)) return e;
   if (int e = gemm_set_outputs(&p, partial, amax_val, amax_idx, act, ld_act)) return e;

@@ -39,6 +39,7 @@ int gemm_run(const GemmPlan& p, cudaStream_t s);
 // Switch a 128-row-tile partial / SwiGLU plan to the half-SM configuration.
 int gemm_set_half(GemmPlan* p);
 int gemm_set_pair(GemmPlan* p);   // CTA pairs (cta_group::2) for wide single-tile plans
+int gemm_set_pair_units(GemmPlan* p);   // pairs over (tile pair, 256-token chunk) units
 // Large-T partial plans (128-row tiles): (tile, split, `tokens`-token pass) units
 // over every SM instead of split-K alone (fewer splits: less fp32 partial traffic)
 int gemm_set_pass_units(GemmPlan* p, int tokens);

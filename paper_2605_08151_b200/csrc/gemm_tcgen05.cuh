@@ -97,6 +97,8 @@ struct GemmArgs {
                             // many tokens) units over the CTAs (large T without split-K)
   int pair;                 // launched as CTA pairs (cluster 2): M=256 cta_group::2 MMAs
                             // whenever the tile is wide (T <= 256, 256-row tiles)
+  int pair_units;           // pairs: (tile pair, 256-token chunk) units over every SM
+                            // (chunk fastest) instead of one tile per CTA walking its chunks
   unsigned long long* stall;   // diagnostics: per CTA {producer empty-wait, MMA full-wait,
                                // MMA issue, stages} in cycles (null = off)
 };
@@ -127,7 +129,7 @@ struct GemmJob {
 
 // The static schedule, computed identically by the three warp roles.
 struct GemmSched {
-  int n_tiles, KI, G, c, T, tile_rows, splits, n_phases, pass, n_pu;
+  int n_tiles, KI, G, c, T, tile_rows, splits, n_phases, pass, n_pu, n_ch;
   bool sk, wide;
   int it, hi, unit, phase;
 
@@ -161,6 +163,11 @@ struct GemmSched {
       pass = a.pass_units;
       n_phases = 1;
     }
+    // pair units: CTAs c, c + 1 (one cluster; G even) take units c + kG and
+    // c + 1 + kG, i.e. the same chunk of tiles 2tp, 2tp + 1; neighbouring
+    // pairs take the other chunks of the same tiles (one HBM read, L2 for the
+    // rest).  n_tiles even, so both CTAs of a pair run out of units together.
+    n_ch = (chunked && a.pair_units) ? (T + 255) / 256 : 0;
     const int total = n_tiles * KI;
     it = sk ? iter_lo(c, G, total) : 0;
     hi = sk ? iter_lo(c + 1, G, total) : 0;
@@ -195,6 +202,22 @@ struct GemmSched {
       j.boxes = 1;
       j.t0 = (unit % n_pu) * pass;
       j.nt = min(pass, T - j.t0);
+      unit += G;
+      return true;
+    }
+    if (n_ch > 0) {
+      if (unit >= n_tiles * n_ch) return false;
+      const int pr = unit >> 1;
+      const int ch = pr % n_ch;
+      j.tile = 2 * (pr / n_ch) + (unit & 1);
+      j.split = 0;
+      j.k0 = 0;
+      j.k1 = KI;
+      j.role = 0;
+      j.row_off = 0;
+      j.boxes = 2;
+      j.t0 = ch * 256;
+      j.nt = min(256, T - j.t0);
       unit += G;
       return true;
     }

@@ -235,6 +235,26 @@ def test_cta_pair_swiglu_at_8b_gate_up(env, T):
     assert torch.allclose(pair[:T].float(), want, atol=2e-2, rtol=1e-2)
 
 
+@pytest.mark.parametrize("N,K,T", [(2 * 14336, 4096, 100), (2 * 14336, 4096, 300),
+                                   (2 * 14336, 4096, 1000), (2 * 27648, 5120, 128),
+                                   (2 * 27648, 5120, 896)])
+def test_cta_pair_units_swiglu(env, N, K, T):
+    """CTA pairs scheduled as (tile pair, 256-token chunk) units over every SM
+    (flag 9000: config 3's and config 5's verify gate/up, 112 and 216 tiles of
+    256 rows) are bit-identical to the single-CTA 256-row kernel and within
+    bf16 tolerance of the fp32 reference."""
+    torch = env[0]
+    g = torch.Generator(device="cuda").manual_seed(T + N)
+    X = torch.randn(1024, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).bfloat16()
+    _, _, _, single = _run(env, X, W, T, 1024, 1, SWIGLU, max_stages=2000)
+    _, _, _, pair = _run(env, X, W, T, 1024, 1, SWIGLU, max_stages=9000)
+    assert torch.equal(pair[:T], single[:T])
+    Wv = W.view(N // 2, 2, K)
+    want = torch.nn.functional.silu(_ref(torch, X, Wv[:, 0], T)) * _ref(torch, X, Wv[:, 1], T)
+    assert torch.allclose(pair[:T].float(), want, atol=2e-2, rtol=1e-2)
+
+
 @pytest.mark.parametrize("T", [20, 256])
 def test_lm_head_argmax_at_128k_vocab(env, T):
     """Greedy lm_head at V = 128256, K = 4096 (the 8B target's head: several
