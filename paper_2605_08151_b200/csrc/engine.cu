@@ -121,6 +121,7 @@ struct ModelRT {
   int n_req = 0, rows_cap = 0, ctx_cap = 0, max_new = 1, split_max = 1, rb_cap = 1;
   int sp_qkv = 1, sp_o = 1, sp_d = 1;
   bool down_pu = false;   // split-K GEMMs as (tile, split, token pass) units (layout())
+  bool pair_q = false, pair_o = false, pair_d = false;   // ... as CTA-pair units instead
   int tr_qkv = 256, tr_o = 256, tr_d = 256;   // weight rows per tile, per GEMM
   int tile_rows = 256;   // weight rows per GEMM CTA (128 for small-T models)
   bool half_gemm = false; // decode GEMMs in the half-SM config (2 CTAs per SM, 128-row tiles)
@@ -174,10 +175,15 @@ struct ModelRT {
     // large verify batches (rows_cap >= kLargeT: config 5's 128 x 7 rows): the
     // split-K GEMMs as 128-row (tile, split, 256-token pass) units over every
     // SM -- one plan for every T of this engine, so still batch invariant.
-    // Splits for about `waves` waves of units (measured at Qwen2.5-32B, T=896):
-    // down 4 waves (328 -> 297 us, 7 -> 4 splits of partials), q/k/v 4 waves
-    // (3 splits: 83.4 -> 70.5 us), o 2 waves (2 splits: 60.0 -> 51.1 us;
-    // 3 / 4 splits 54.7 / 57.5): target 61.8 -> 60.0 ms per round.
+    // 128-row one-box units: splits for about `waves` waves of units
+    // (measured at Qwen2.5-32B, T=896: down 4 waves, 328 -> 297 us; q/k/v 4
+    // waves, 83.4 -> 70.5 us; o 2 waves, 60.0 -> 51.1 us).  Where the 256-row
+    // tiles pair up (N % 512 == 0), CTA pairs over (tile pair, split, 256-token
+    // chunk) units instead (cta_group::2: 1.5x the MMA rate per SM of one-box
+    // tiles), splits from waves x (k blocks per split + ~30 blocks of per-unit
+    // epilogue); isolated, L2 flushed, vs the one-box units: 32B T=896 down
+    // 293.8 -> 238.6 us (3 splits), q/k/v 91.2 -> 70.7 (1), o 76.8 -> 68.8 (1);
+    // 8B T=1280 down 175.1 -> 138.2 (3), q/k/v 85.0 -> 62.5 (1), o 76.8 -> 59.6 (1).
     down_pu = !half_gemm && !use_chain && rows_cap >= kLargeT;
     if (down_pu) {
       const int passes = (rows_cap + 255) / 256;
@@ -187,10 +193,35 @@ struct ModelRT {
         while (sp > 1 && k / 64 / sp < 3) --sp;
         return sp;
       };
-      tr_qkv = tr_o = tr_d = 128;
-      sp_qkv = pu_splits(nqkv(), d, 4);
-      sp_o = pu_splits(d, qd, 2);
-      sp_d = pu_splits(d, dm.ffn, 4);
+      auto pair_splits = [&](int n, int k) {
+        const int g2 = ctas & ~1;
+        int best = 1;
+        long long best_c = -1;
+        for (int sp = 1; sp <= 8 && k / 64 / sp >= 3; ++sp) {
+          const int units = (n / 256) * sp * passes;
+          const long long c = (long long)((units + g2 - 1) / g2) * (k / 64 * 60 / sp + 30 * 60);
+          if (best_c < 0 || c < best_c) {
+            best_c = c;
+            best = sp;
+          }
+        }
+        return best;
+      };
+      static const bool pair_env = [] {   // SPECTRE_PAIR_UNITS=0: one-box units only
+        const char* v = getenv("SPECTRE_PAIR_UNITS");
+        return v ? atoi(v) != 0 : true;
+      }();
+      // in context (PDL prologues under the previous kernel) the o projection
+      // keeps the one-box units: 32B 50.7 vs 66.6 us, 8B T=1280 37.9 vs 52.1
+      pair_q = pair_env && nqkv() % 512 == 0;
+      pair_o = false;
+      pair_d = pair_env && d % 512 == 0;
+      tr_qkv = pair_q ? 256 : 128;
+      tr_o = pair_o ? 256 : 128;
+      tr_d = pair_d ? 256 : 128;
+      sp_qkv = pair_q ? pair_splits(nqkv(), d) : pu_splits(nqkv(), d, 4);
+      sp_o = pair_o ? pair_splits(d, qd) : pu_splits(d, qd, 2);
+      sp_d = pair_d ? pair_splits(d, dm.ffn) : pu_splits(d, dm.ffn, 4);
     }
     size_t part_n = std::max({(size_t)sp_qkv * nqkv(), (size_t)sp_o * d, (size_t)sp_d * d});
     if (down_pu)   // the large-T plans (sampling engines) share the buffer
@@ -271,8 +302,11 @@ struct ModelRT {
                     0, 0, tr_d));
       if (pair_units) TRY(gemm_set_pair_units(&pgu[l]));
       else if (pair_fits && !gu128) TRY(gemm_set_pair(&pgu[l]));
-      if (down_pu)
-        for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) TRY(gemm_set_pass_units(p, 256));
+      if (down_pu) {
+        TRY(pair_q ? gemm_set_pair_units(&pq[l]) : gemm_set_pass_units(&pq[l], 256));
+        TRY(pair_o ? gemm_set_pair_units(&po[l]) : gemm_set_pass_units(&po[l], 256));
+        TRY(pair_d ? gemm_set_pair_units(&pd[l]) : gemm_set_pass_units(&pd[l], 256));
+      }
       if (half_gemm) {
         // partial GEMMs only: the SwiGLU GEMM measured faster in the full config
         for (GemmPlan* p : {&pq[l], &po[l], &pd[l]}) TRY(gemm_set_half(p));
@@ -291,10 +325,13 @@ struct ModelRT {
                       kPartial, kSpLqkv, 0, 0, 128));
         TRY(gemm_plan(&poL[l], bf(w.wo) + (size_t)l * d * qd, d, qd, attn, rows_cap, kPartial,
                       kSpLo, 0, 0, 128));
+        // down: the normal plan's CTA-pair units where they apply (8B T=1280 in
+        // context: 107.4 -> 102.4 us), else 128-row units in kSpLd splits
         TRY(gemm_plan(&pdL[l], bf(w.wd) + (size_t)l * d * F, d, F, act, rows_cap, kPartial,
-                      kSpLd, 0, 0, 128));
+                      pair_d ? sp_d : kSpLd, 0, 0, pair_d ? 256 : 128));
+        TRY(pair_d ? gemm_set_pair_units(&pdL[l]) : gemm_set_pass_units(&pdL[l], 256));
         for (GemmPlan* p : {&pqL[l], &poL[l], &pdL[l]}) {
-          TRY(gemm_set_pass_units(p, 256));
+          if (p != &pdL[l]) TRY(gemm_set_pass_units(p, 256));
           TRY(gemm_set_outputs(p, part, nullptr, nullptr, nullptr, 0));
           p->args.t_dev = bt.t_dev;
         }
@@ -447,7 +484,7 @@ struct ModelRT {
                                              x, d, eps, s));
     const bool large = !pqL.empty() && n_req * new_per_req >= kLargeT;
     const int s_qkv = large ? kSpLqkv : sp_qkv, s_o = large ? kSpLo : sp_o,
-              s_d = large ? kSpLd : sp_d;
+              s_d = large && !pair_d ? kSpLd : sp_d;
     for (int l = 0; l < L && !use_chain; ++l) {
       TRY(gemm_run(large ? pqL[l] : pq[l], s));
       TRY(launch_qkv_rope_kv(part, s_qkv, rows_cap, bt.t_dev, rows_cap, bt.pos, bt.slot,

@@ -205,14 +205,15 @@ struct GemmSched {
       unit += G;
       return true;
     }
-    if (n_ch > 0) {
-      if (unit >= n_tiles * n_ch) return false;
+    if (n_ch > 0) {   // (tile pair, split, chunk) units, chunk fastest
+      if (unit >= n_tiles * splits * n_ch) return false;
       const int pr = unit >> 1;
       const int ch = pr % n_ch;
-      j.tile = 2 * (pr / n_ch) + (unit & 1);
-      j.split = 0;
-      j.k0 = 0;
-      j.k1 = KI;
+      const int r2 = pr / n_ch;
+      j.tile = 2 * (r2 / splits) + (unit & 1);
+      j.split = r2 % splits;
+      j.k0 = (int)((long long)KI * j.split / splits);
+      j.k1 = (int)((long long)KI * (j.split + 1) / splits);
       j.role = 0;
       j.row_off = 0;
       j.boxes = 2;

@@ -255,6 +255,25 @@ def test_cta_pair_units_swiglu(env, N, K, T):
     assert torch.allclose(pair[:T].float(), want, atol=2e-2, rtol=1e-2)
 
 
+@pytest.mark.parametrize("N,K,T,S", [(4096, 14336, 1280, 3), (4096, 4096, 300, 2),
+                                     (5120, 27648, 896, 4), (7168, 5120, 896, 3)])
+def test_cta_pair_units_partial(env, N, K, T, S):
+    """Split-K partial GEMMs as CTA pairs over (tile pair, split, 256-token
+    chunk) units (flag 9000): every split's partial bit-identical to the
+    single-CTA 256-row kernel with the same split ranges, and the split sum
+    within fp32-accumulation tolerance of the reference."""
+    torch = env[0]
+    g = torch.Generator(device="cuda").manual_seed(T + N + S)
+    RC = (T + 63) // 64 * 64
+    X = torch.randn(RC, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).bfloat16()
+    single, _, _, _ = _run(env, X, W, T, RC, S, PARTIAL, max_stages=2000)
+    pair, _, _, _ = _run(env, X, W, T, RC, S, PARTIAL, max_stages=9000)
+    assert torch.equal(pair[:, :T], single[:, :T])
+    want = _ref(torch, X, W, T)
+    assert torch.allclose(pair[:, :T].sum(0), want, atol=1e-2, rtol=1e-3)
+
+
 @pytest.mark.parametrize("T", [20, 256])
 def test_lm_head_argmax_at_128k_vocab(env, T):
     """Greedy lm_head at V = 128256, K = 4096 (the 8B target's head: several
