@@ -292,7 +292,7 @@ struct ModelRT {
       // tiles (isolated, L2 flushed: 8B T=1280 279.5 -> 207.9 us, 32B T=896
       // 457.8 (128-row tiles) -> 398.3 us; T=320 109.6 -> 113.6, so not below)
       const bool pair_units = gu_pair && !half_gemm && (2 * F / 256) % 2 == 0 &&
-                              rows_cap >= kLargeT;
+                              down_pu;
       const bool pair_fits = gu_pair && !half_gemm && (2 * F / 256) % 2 == 0 &&
                              2 * F / 256 <= gemm_sk_grid();
       const bool gu128 = !pair_units && ((2 * F) / 128 <= gemm_sk_grid() || !pair_fits);
