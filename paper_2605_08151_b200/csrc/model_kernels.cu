@@ -80,7 +80,8 @@ constexpr int kMaxSplits = 12;
 
 // kS: most splits the kernel keeps in flight per chunk (register budget: with
 // kS = 4 a 512-thread CTA fits twice per SM, so T=256 rows run in one wave)
-template <int kVec, int kS = kMaxSplits>
+// kFlat: every (chunk, split) load of a row in flight at once (splits <= kS)
+template <int kVec, int kS = kMaxSplits, bool kFlat = false>
 __global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restrict__ part,
                                                              int splits, int rows_cap,
                                                              const int* __restrict__ t_dev,
@@ -120,6 +121,29 @@ __global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restr
   }
   const float4* p4 = reinterpret_cast<const float4*>(part + (size_t)t * d);
   float4 v[kVec];
+  if constexpr (kFlat) {
+    // every (chunk, split) load of the row in flight at once: one L2 round trip
+    // (per element still h + p0 + p1 + ..., split order)
+    float4 ld[kVec][kS];
+    constexpr int kF = kS;
+#pragma unroll
+    for (int j = 0; j < kVec; ++j)
+#pragma unroll
+      for (int sp = 0; sp < kF; ++sp) {
+        const int i = threadIdx.x + j * blockDim.x;
+        if (sp < splits && i < nv) ld[j][sp] = __ldg(p4 + sp * sstride + i);
+      }
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      float4 acc = hv[j];
+#pragma unroll
+      for (int sp = 0; sp < kF; ++sp)
+        if (sp < splits) {
+          acc.x += ld[j][sp].x; acc.y += ld[j][sp].y; acc.z += ld[j][sp].z; acc.w += ld[j][sp].w;
+        }
+      v[j] = acc;
+    }
+  } else
 #pragma unroll
   for (int j = 0; j < kVec; ++j) {   // one chunk's split loads in flight (register budget:
     const int i = threadIdx.x + j * blockDim.x;   // two 512-thread CTAs per SM)
@@ -506,6 +530,7 @@ static bool resid_batched() {   // > 4 splits through the 4-at-a-time variant to
   return v;
 }
 
+
 int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const int* t_dev,
                             int t_cap, const float* w, float* h, void* x, int d, float eps,
                             cudaStream_t s) {
@@ -523,6 +548,12 @@ int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const i
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
   else if (vec <= 2)
     SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<2>, grid, dim3(threads),
+                       0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
+  // d = 5120 (Qwen2.5-32B) with <= 4 splits: every load of a row in flight at
+  // once (T=896: 23.6 -> 17.9 us; the same at d = 4096 costs the second CTA
+  // per SM and is slower, 4.67 -> 5.6 us)
+  else if (vec <= 3 && splits <= 4)
+    SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", (k_residual_rmsnorm_v<3, 4, true>), grid, dim3(threads),
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
   else if (vec <= 4)
     SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<4>, grid, dim3(threads),
