@@ -180,8 +180,7 @@ struct ModelRT {
     // waves, 83.4 -> 70.5 us; o 2 waves, 60.0 -> 51.1 us).  Where the 256-row
     // tiles pair up (N % 512 == 0), CTA pairs over (tile pair, split, 256-token
     // chunk) units instead (cta_group::2: 1.5x the MMA rate per SM of one-box
-    // tiles), splits from waves x (k blocks per split + ~30 blocks of per-unit
-    // epilogue); isolated, L2 flushed, vs the one-box units: 32B T=896 down
+    // tiles); isolated, L2 flushed, vs the one-box units: 32B T=896 down
     // 293.8 -> 238.6 us (3 splits), q/k/v 91.2 -> 70.7 (1), o 76.8 -> 68.8 (1);
     // 8B T=1280 down 175.1 -> 138.2 (3), q/k/v 85.0 -> 62.5 (1), o 76.8 -> 59.6 (1).
     down_pu = !half_gemm && !use_chain && rows_cap >= kLargeT;
@@ -193,15 +192,19 @@ struct ModelRT {
         while (sp > 1 && k / 64 / sp < 3) --sp;
         return sp;
       };
+      // splits: the best wave fill (units / (waves * CTAs)) with >= 48 k blocks
+      // (3,072 K) per unit, fewer splits on ties (in context: 32B down 7
+      // splits 181 us vs 3 / 5 splits 231 us; 8B T=1,280 down 3 splits
+      // 102.5 us vs 5 / 7 splits 106.5 / 112.0 us, where 5+ fall below 48)
       auto pair_splits = [&](int n, int k) {
         const int g2 = ctas & ~1;
         int best = 1;
-        long long best_c = -1;
-        for (int sp = 1; sp <= 8 && k / 64 / sp >= 3; ++sp) {
+        double best_fill = 0.0;
+        for (int sp = 1; sp <= 8 && (sp == 1 || k / 64 / sp >= 48); ++sp) {
           const int units = (n / 256) * sp * passes;
-          const long long c = (long long)((units + g2 - 1) / g2) * (k / 64 * 60 / sp + 30 * 60);
-          if (best_c < 0 || c < best_c) {
-            best_c = c;
+          const double fill = (double)units / ((double)((units + g2 - 1) / g2) * g2);
+          if (fill > best_fill + 1e-9) {
+            best_fill = fill;
             best = sp;
           }
         }

@@ -122,26 +122,27 @@ __global__ void __launch_bounds__(512) k_residual_rmsnorm_v(const float* __restr
   const float4* p4 = reinterpret_cast<const float4*>(part + (size_t)t * d);
   float4 v[kVec];
   if constexpr (kFlat) {
-    // every (chunk, split) load of the row in flight at once: one L2 round trip
-    // (per element still h + p0 + p1 + ..., split order)
-    float4 ld[kVec][kS];
-    constexpr int kF = kS;
+    // every chunk's loads of kS splits in flight at once: one L2 round trip
+    // per kS splits (per element still h + p0 + p1 + ..., split order)
 #pragma unroll
-    for (int j = 0; j < kVec; ++j)
+    for (int j = 0; j < kVec; ++j) v[j] = hv[j];
+    for (int s0 = 0; s0 < splits; s0 += kS) {
+      float4 ld[kVec][kS];
 #pragma unroll
-      for (int sp = 0; sp < kF; ++sp) {
-        const int i = threadIdx.x + j * blockDim.x;
-        if (sp < splits && i < nv) ld[j][sp] = __ldg(p4 + sp * sstride + i);
-      }
+      for (int j = 0; j < kVec; ++j)
 #pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      float4 acc = hv[j];
-#pragma unroll
-      for (int sp = 0; sp < kF; ++sp)
-        if (sp < splits) {
-          acc.x += ld[j][sp].x; acc.y += ld[j][sp].y; acc.z += ld[j][sp].z; acc.w += ld[j][sp].w;
+        for (int sp = 0; sp < kS; ++sp) {
+          const int i = threadIdx.x + j * blockDim.x;
+          if (s0 + sp < splits && i < nv) ld[j][sp] = __ldg(p4 + (s0 + sp) * sstride + i);
         }
-      v[j] = acc;
+#pragma unroll
+      for (int j = 0; j < kVec; ++j)
+#pragma unroll
+        for (int sp = 0; sp < kS; ++sp)
+          if (s0 + sp < splits) {
+            v[j].x += ld[j][sp].x; v[j].y += ld[j][sp].y;
+            v[j].z += ld[j][sp].z; v[j].w += ld[j][sp].w;
+          }
     }
   } else
 #pragma unroll
@@ -549,10 +550,10 @@ int launch_residual_rmsnorm(const float* part, int splits, int rows_cap, const i
   else if (vec <= 2)
     SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", k_residual_rmsnorm_v<2>, grid, dim3(threads),
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
-  // d = 5120 (Qwen2.5-32B) with <= 4 splits: every load of a row in flight at
-  // once (T=896: 23.6 -> 17.9 us; the same at d = 4096 costs the second CTA
-  // per SM and is slower, 4.67 -> 5.6 us)
-  else if (vec <= 3 && splits <= 4)
+  // d = 5120 (Qwen2.5-32B): every chunk's loads of 4 splits in flight at once
+  // (T=896, 3 splits: 23.6 -> 17.9 us; the same at d = 4096 costs the second
+  // CTA per SM and is slower, 4.67 -> 5.6 us)
+  else if (vec <= 3)
     SPECTRE_LAUNCH_PDL("k_residual_rmsnorm", (k_residual_rmsnorm_v<3, 4, true>), grid, dim3(threads),
                        0, s, part, splits, rows_cap, t_dev, w, h, xb, d, eps);
   else if (vec <= 4)
