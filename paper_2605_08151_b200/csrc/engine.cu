@@ -348,11 +348,14 @@ struct ModelRT {
       TRY(gemm_set_outputs(&plm, logits, nullptr, nullptr, nullptr, 0));
     } else {
       // whole tiles per CTA (no stream-K): logits independent of the CTA
-      // budget.  256-row tiles (128-row neutral at T=256), 128-row ones for
-      // large verify batches (Qwen2.5-32B, T=896: 1,558 -> 1,427 us); argmax
-      // over full-K logits is exact either way
+      // budget.  256-row tiles (128-row neutral at T=256); for large verify
+      // batches CTA-pair units where the 256-row tiles pair up (Qwen2.5-32B,
+      // 594 tiles, T=896 isolated: 1,413 -> 1,312 us), else 128-row tiles
+      // (1,558 -> 1,427 us); argmax over full-K logits is exact either way
+      const bool lm_pair = down_pu && pair_d && (dm.vocab % 512) == 0;
       TRY(gemm_plan(&plm, w.lm_head, dm.vocab, d, x, rows_cap, kArgmax, 1, 0, 0,
-                    down_pu ? 128 : 256));
+                    down_pu && !lm_pair ? 128 : 256));
+      if (lm_pair) TRY(gemm_set_pair_units(&plm));
       TRY(gemm_set_outputs(&plm, nullptr, amax_v, amax_i, nullptr, 0));
     }
     const uint64_t kv_rows = (uint64_t)L * n_req * dm.n_kv_heads * ctx_cap;

@@ -164,9 +164,9 @@ int gemm_set_pair(GemmPlan* p) {
 // every SM (an even grid): for large verify batches and for 256-row tile
 // counts above one wave of CTAs.
 int gemm_set_pair_units(GemmPlan* p) {
-  if (p->half || p->bk != 64 || p->epi == kArgmax || p->args.tile_rows != 256 ||
-      p->args.stream_k || p->n_tiles % 2)
-    return arg_fail("gemm_set_pair_units: 256-row SwiGLU / partial tiles, an even count, BK 64");
+  if (p->half || p->bk != 64 || p->args.tile_rows != 256 || p->args.stream_k || p->n_tiles % 2 ||
+      (p->epi == kArgmax && p->args.splits != 1))
+    return arg_fail("gemm_set_pair_units: 256-row tiles, an even count, BK 64");
   p->grid = num_sms() & ~1;
   p->args.pair = 1;
   p->args.pair_units = 1;
@@ -255,8 +255,9 @@ int gemm_run(const GemmPlan& p0, cudaStream_t s) {
   }
   const GemmPlan& p = *pp;
   if (p.args.pair) {
-    if (p.epi == kArgmax || p.bk != 64) return arg_fail("gemm: CTA pairs: SwiGLU / partial, BK 64");
+    if (p.bk != 64) return arg_fail("gemm: CTA pairs: BK 64");
     if (p.epi == kPartial) return launch_one<kPartial, 64, 0, 1>(p, s);
+    if (p.epi == kArgmax) return launch_one<kArgmax, 64, 0, 1>(p, s);
     return launch_one<kSwiGLU, 64, 0, 1>(p, s);
   }
   if (p.half) {

@@ -543,6 +543,16 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
     };
     int jn = 0;
     int amax_jobs = 0;   // jobs that wrote argmax slots (contributor segments do not)
+    // pair units: a CTA's units cover scattered chunks, so its warps' slots
+    // start at the identity and every unit merges (same lane writes and merges
+    // a token: lane = token % 32)
+    const bool amax_init = kEpi == kArgmax && sched.n_ch > 0 && !(a.diag & 2);
+    if (amax_init)
+      for (int t = lane; t < T; t += 32) {
+        const size_t slot = ((size_t)blockIdx.x * 8 + ewarp) * a.rows_cap + t;
+        a.amax_val[slot] = -INFINITY;
+        a.amax_idx[slot] = 0x7fffffff;
+      }
     GemmJob j;
     while (sched.next(j)) {
       const int buf = jn % nbuf;
@@ -693,7 +703,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
             int oi = bi[0];
             // first coverage of a token by this warp: the CTA's first unit,
             // first row pass; later jobs merge with what the warp wrote
-            if (!(amax_jobs < sched.n_phases && j.row_off == 0)) {
+            if (amax_init || !(amax_jobs < sched.n_phases && j.row_off == 0)) {
               const float pv = a.amax_val[slot];
               const int pi = a.amax_idx[slot];
               if (pv > ov || (pv == ov && pi < oi)) {
@@ -778,7 +788,7 @@ gemm_bf16_swapab(const __grid_constant__ CUtensorMap tmap_w,
       bulk_wait_all();                                // generic loads) before the grid does
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
-    if (kEpi == kArgmax && !(a.diag & 2)) {
+    if (kEpi == kArgmax && !(a.diag & 2) && !amax_init) {
       // every (CTA, warp) slot of every live token is defined: fill the tokens
       // this warp never covered (no job, or the other group's chunks of a
       // one-box pass) with the identity

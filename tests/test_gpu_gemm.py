@@ -274,6 +274,38 @@ def test_cta_pair_units_partial(env, N, K, T, S):
     assert torch.allclose(pair[:, :T].sum(0), want, atol=1e-2, rtol=1e-3)
 
 
+def _argmax_of_slots(torch, av, ai, T):
+    """(max, lowest index) over the per-(CTA, warp) partial slots of T tokens."""
+    v, i = av[:, :T], ai[:, :T]
+    m = v.max(0).values
+    big = torch.full_like(i, 2 ** 31 - 1)
+    return m, torch.where(v == m[None], i, big).min(0).values
+
+
+@pytest.mark.parametrize("T", [128, 300, 896])
+def test_cta_pair_units_argmax_at_152k_vocab(env, T):
+    """Greedy lm_head as CTA pairs over (tile pair, 256-token chunk) units
+    (flag 9000; Qwen2.5-32B's head: V = 152064 = 594 tiles of 256 rows, each CTA
+    covering scattered chunks): the (max, lowest index) of every token equals the
+    single-CTA 256-row kernel's, and the fp32 argmax where the top-2 margin is
+    clear."""
+    torch = env[0]
+    V, K = 152064, 5120
+    g = torch.Generator(device="cuda").manual_seed(V + T)
+    RC = (T + 63) // 64 * 64
+    X = torch.randn(RC, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(V, K, device="cuda", generator=g) * 0.02).bfloat16()
+    _, av1, ai1, _ = _run(env, X, W, T, RC, 1, ARGMAX, max_stages=2000)
+    _, av2, ai2, _ = _run(env, X, W, T, RC, 1, ARGMAX, max_stages=9000)
+    m1, i1 = _argmax_of_slots(torch, av1, ai1, T)
+    m2, i2 = _argmax_of_slots(torch, av2, ai2, T)
+    assert torch.equal(m1, m2) and torch.equal(i1, i2)
+    logits = _ref(torch, X, W, T)
+    top2 = logits.topk(2, dim=1).values
+    clear = (top2[:, 0] - top2[:, 1]) > 1e-2
+    assert torch.equal(i2[clear].long(), logits.argmax(1)[clear])
+
+
 @pytest.mark.parametrize("T", [20, 256])
 def test_lm_head_argmax_at_128k_vocab(env, T):
     """Greedy lm_head at V = 128256, K = 4096 (the 8B target's head: several
