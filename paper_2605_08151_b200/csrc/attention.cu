@@ -461,7 +461,11 @@ static int launch_attn_w_t(const CUtensorMap& tk, const CUtensorMap& tv, AttnArg
 int launch_attention_w(const CUtensorMap& tk32, const CUtensorMap& tv32, const AttnArgs& a,
                        int hd, int rows_per_req, cudaStream_t s) {
   if (a.chunk % 64 || a.chunk <= 0) return arg_fail("attention: chunk must be a multiple of 64");
-  if (hd == 128) return launch_attn_w_t<128, 4, 3, 1>(tk32, tv32, a, rows_per_req, s);
+  // hd 128: 7 warps with 2-stage rings (one more warp per SM sub-partition
+  // than 4 warps x 3 stages: the kernel is warp-latency bound, 1 warp per
+  // SMSP issued every ~3.8 cycles; ncu r02f): config 3 (4,096 m-tile items)
+  // 107.0 -> 90.3 us per launch, config 2 34.4 -> 33.4 us; 6 x 2: 103.3 / 33.6
+  if (hd == 128) return launch_attn_w_t<128, 7, 2, 1>(tk32, tv32, a, rows_per_req, s);
   if (hd == 64) {
     // two warps per item (even / odd stages) while the (request, kv head,
     // key split) items of a decode step fit one wave of warp pairs (config 2:
@@ -470,8 +474,10 @@ int launch_attention_w(const CUtensorMap& tk32, const CUtensorMap& tv32, const A
     // forward's row bound (a catch-up step's extra m-tiles are mostly empty),
     // so one engine always uses one variant.
     const long long items = (long long)a.n_req * a.n_kv * a.split_max;
+    // (one warp per item: 14 warps with 2-stage rings, 54.2 -> 48.6 us at
+    // config 3; 12 x 2: 59.5 us)
     if (2 * items > 8ll * num_sms())
-      return launch_attn_w_t<64, 8, 3, 1>(tk32, tv32, a, rows_per_req, s);
+      return launch_attn_w_t<64, 14, 2, 1>(tk32, tv32, a, rows_per_req, s);
     return launch_attn_w_t<64, 8, 3, 2>(tk32, tv32, a, rows_per_req, s);
   }
   return arg_fail("attention: head_dim must be 64 or 128");
